@@ -1,0 +1,151 @@
+"""Generate the golden fixtures in this directory from the UNMODIFIED reference.
+
+Run once in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``gridse`` from /root/reference/pkg/src and the reference's own
+synthetic-grid generator from /root/reference/pkg/tests/conftest.py, runs
+``solve_multiarea`` / ``fused_accumulate`` / ``schur_condense`` /
+``assemble_boundary`` on the BASELINE.json configurations (and a few edge
+cases), and stores inputs + outputs as ``.npz``.  Nothing at test time reads
+/root/reference: the tests load these files only.
+
+Also writes the reference partitioner's ``area_of_bus`` for the three named
+shapes to ``paper_2604_23175_b200/cases/part_<shape>.json`` (the reference
+partitioner takes 23 s / 141 s / 79 s there).
+"""
+
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/tests")
+
+import numpy as np  # noqa: E402
+import gridse as R  # noqa: E402
+from conftest import make_path4, random_network  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CASES = os.path.join(HERE, "..", "..", "paper_2604_23175_b200", "cases")
+SHAPES = {"pegase2869": (2869, 4582, 8), "pegase9241": (9241, 16049, 16),
+          "activsg10k": (10000, 12706, 32)}
+
+
+def solve_and_record(name, net, ms, part, detail, cfg=None, recipe=None):
+    cfg = cfg or R.SolverConfig()
+    bord, maps = R.build_variable_maps(net, part)
+    out = {
+        "recipe": json.dumps(recipe or {}),
+        "area_of_bus": part.area_of_bus.astype(np.int32),
+        "n_gamma": bord.n_gamma,
+        "z_sum": np.array([ms.z.sum(), np.abs(ms.z).sum(), ms.weight.sum()]),
+    }
+    if detail:
+        out.update(z=ms.z, weight=ms.weight, mtype=ms.mtype.astype(np.int32),
+                   target=ms.target.astype(np.int32))
+    # flat-start blocks, Schur blocks and the boundary system (first iteration)
+    st = R.StateVector.flat_start(net)
+    xg = bord.gather(st.va, st.vm)
+    schurs = []
+    for a, m in enumerate(maps):
+        blk = R.fused_accumulate(m, ms, m.gather_interior(st.va, st.vm), xg[m.boundary_selector])
+        cache = R.symbolic_analyze(blk.g_ii)
+        R.numeric_refactor(cache, blk.g_ii.data)
+        sch = R.schur_condense(cache, blk.g_ib, blk.g_bb, blk.b_i, blk.b_b)
+        schurs.append(sch)
+        out[f"a{a}_dims"] = np.array([m.n_interior, m.n_boundary, blk.g_ii.nnz, blk.g_ib.nnz])
+        out[f"a{a}_sel"] = m.boundary_selector.astype(np.int32)
+        if detail:
+            out[f"a{a}_ii_ptr"] = blk.g_ii.indptr.astype(np.int32)
+            out[f"a{a}_ii_idx"] = blk.g_ii.indices.astype(np.int32)
+            out[f"a{a}_ib_ptr"] = blk.g_ib.indptr.astype(np.int32)
+            out[f"a{a}_ib_idx"] = blk.g_ib.indices.astype(np.int32)
+            out[f"a{a}_data_ii"] = blk.g_ii.data
+            out[f"a{a}_data_ib"] = blk.g_ib.data
+            out[f"a{a}_g_bb"] = blk.g_bb
+            out[f"a{a}_s_b"] = sch.s_b
+        else:  # fingerprints only (sums are order-sensitive at 1e-16, compared at 1e-12)
+            out[f"a{a}_sum_ii"] = np.array([blk.g_ii.data.sum(), np.abs(blk.g_ii.data).sum()])
+            out[f"a{a}_sb_diag"] = np.diag(sch.s_b).copy()
+        out[f"a{a}_b_i"] = blk.b_i
+        out[f"a{a}_b_b"] = blk.b_b
+        out[f"a{a}_b_hat"] = sch.b_hat
+    if bord.n_gamma:
+        bs = R.assemble_boundary(schurs, [m.boundary_selector for m in maps], bord.n_gamma)
+        dxg = R.dense_cholesky_solve(bs.s_gamma, bs.b_gamma)
+        if detail:
+            out["s_gamma"] = bs.s_gamma
+        out["s_gamma_diag"] = np.diag(bs.s_gamma).copy()
+        out["b_gamma"] = bs.b_gamma
+        out["dx_gamma"] = dxg
+    # the solve itself
+    trace = []
+    t0 = time.perf_counter()
+    est, rep = R.solve_multiarea(net, ms, part, maps=(bord, maps), config=cfg,
+                                 on_iteration=lambda it, s, d: trace.append((s, d)))
+    wall = time.perf_counter() - t0
+    out.update(iterations=rep.iterations, converged=rep.converged, objective=rep.objective,
+               deltas=np.array([d for _, d in trace]), va=est.va, vm=est.vm,
+               ref_wall_s=wall, ref_timings=json.dumps(rep.timings))
+    if detail:
+        out["trace_va"] = np.array([s.va for s, _ in trace])
+        out["trace_vm"] = np.array([s.vm for s, _ in trace])
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(f"{name}: iters {rep.iterations} conv {rep.converged} J {rep.objective!r} "
+          f"n_gamma {bord.n_gamma} wall {wall:.2f}s", flush=True)
+
+
+def main(which):
+    if "small" in which:
+        net = R.load_case("/root/reference/pkg/cases/ieee14.m")
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=0))
+        for k in (1, 2, 3, 14):
+            solve_and_record(f"ieee14_k{k}", net, ms, R.partition_network(net, k, seed=0), True,
+                             recipe={"case": "ieee14.m", "meas_seed": 0, "k": k, "part_seed": 0})
+        net = R.load_case("/root/reference/pkg/cases/ieee118.m")
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=0))
+        for k in (3, 6):
+            solve_and_record(f"ieee118_k{k}", net, ms, R.partition_network(net, k, seed=0), True,
+                             recipe={"case": "ieee118.m", "meas_seed": 0, "k": k, "part_seed": 0})
+        # slack on the boundary, noiseless (reference test_solver.py:95-102)
+        net = make_path4(slack_pos=1)
+        ms = R.generate_measurements(net, R.MeasurementConfig(sigma_vm=0.0, sigma_power=0.0))
+        solve_and_record("path4_slack_boundary", net, ms, R.load_partition(net, [0, 0, 1, 1]), True,
+                         cfg=R.SolverConfig(convergence_tol=1e-10),
+                         recipe={"gen": "make_path4(slack_pos=1)", "sigma": 0.0,
+                                 "area_of_bus": [0, 0, 1, 1], "tol": 1e-10})
+        # random grids, one with a masked family (reference test_assembly.py:200-216)
+        net = random_network(300, 11)
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=4))
+        solve_and_record("rand300_k3_maskpf", net, R.apply_mask(ms, R.MeasurementType.PF),
+                         R.partition_network(net, 3, seed=0), True,
+                         recipe={"gen": "random_network(300, 11)", "meas_seed": 4, "k": 3,
+                                 "mask": "PF"})
+        net = random_network(120, 3, 0.3)
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=2))
+        solve_and_record("rand120_k4", net, ms, R.partition_network(net, 4, seed=1), True,
+                         recipe={"gen": "random_network(120, 3, 0.3)", "meas_seed": 2, "k": 4,
+                                 "part_seed": 1})
+    for shape in ("pegase2869", "pegase9241", "activsg10k"):
+        if shape not in which:
+            continue
+        n, nbr, k = SHAPES[shape]
+        net = random_network(n, seed=n, extra_frac=(nbr - (n - 1)) / n)
+        path = os.path.join(CASES, f"part_{shape}.json")
+        if os.path.exists(path):
+            part = R.load_partition(net, json.load(open(path))["area_of_bus"])
+        else:
+            part = R.partition_network(net, k, seed=0)
+            with open(path, "w") as fh:
+                json.dump({"k": k, "area_of_bus": [int(a) for a in part.area_of_bus]}, fh)
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=0))
+        solve_and_record(f"{shape}_k{k}", net, ms, part, detail=(shape == "pegase2869"),
+                         recipe={"gen": f"random_network({n}, seed={n}, extra_frac=({nbr}-{n - 1})/{n})",
+                                 "meas_seed": 0, "k": k, "part_seed": 0})
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["small", "pegase2869", "pegase9241", "activsg10k"])
