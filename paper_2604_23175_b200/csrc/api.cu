@@ -1,0 +1,540 @@
+// api.cu -- C ABI of libgridse_b200.so (include/gridse_b200.h): plan lifetime, the
+// device-resident Gauss-Newton loop (CUDA-graph captured), phase-level entry points and
+// readback in the reference's layouts.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace gse;
+
+namespace {
+
+template <class T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t n = 0;
+    cudaError_t upload(const std::vector<T>& h) {
+        n = h.size();
+        cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+        if (e != cudaSuccess) return e;
+        if (n) e = cudaMemcpy(ptr, h.data(), n * sizeof(T), cudaMemcpyHostToDevice);
+        return e;
+    }
+    cudaError_t alloc(size_t count, bool zero = true) {
+        n = count;
+        cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+        if (e == cudaSuccess && zero) e = cudaMemset(ptr, 0, std::max<size_t>(n, 1) * sizeof(T));
+        return e;
+    }
+    void release() { if (ptr) cudaFree(ptr); ptr = nullptr; }
+};
+
+struct LevelLaunch { int pclass; int first, count; size_t smem; int phase; };
+struct BwdLaunch { int first, count, max_u, phase; };
+
+}  // namespace
+
+struct gse_plan {
+    HostProgram hp;
+    gse_error err{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool coordinator = true;
+
+    // network + measurements
+    DevBuf<int32_t> y_ptr, y_idx, br_from, br_to, m_type, m_target;
+    DevBuf<double> y_g, y_b, br_y, z, w;
+    // evaluation units
+    DevBuf<int32_t> vm_bus, vm_row, vm_slot, fl_branch, fl_from, fl_to, fl_row, fl_slot;
+    DevBuf<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq;
+    DevBuf<double> g, gw, wrg;
+    // accumulation programs
+    DevBuf<int32_t> acc_ptr, acc_a, acc_b, racc_ptr, racc_a, racc_b;
+    DevBuf<double> gval, refval;
+    // fronts
+    DevBuf<int32_t> f_p, f_u1, f_T, f_nchild, f_child_ptr, f_children, f_rel_off, f_rel, f_reg_off, f_reg_ptr;
+    DevBuf<int32_t> f_rows_off, f_rows;
+    DevBuf<uint32_t> orig_pos;
+    DevBuf<int64_t> f_gval_off, f_l_off, f_u_off;
+    DevBuf<TaskRec> tasks;
+    DevBuf<int32_t> bwd_fronts;
+    DevBuf<double> lbuf, ubuf, xsol;
+    DevBuf<int32_t> upd_bus, upd_quant, upd_pos;
+    DevBuf<double> obj_partial, status;       // status: [delta bits as double slot, err as double] (MAX-reducible)
+    DevBuf<unsigned long long> flags;         // [0] delta_inf bits, [1] failure code (min)
+    unsigned long long* h_flags = nullptr;    // pinned
+    double* h_obj = nullptr;                  // pinned
+    std::vector<LevelLaunch> fwd;
+    std::vector<BwdLaunch> bwd;
+    EvalProg ep{};
+    FrontTab ft{};
+
+    cudaGraphExec_t graph = nullptr;
+    const double* graph_va = nullptr;
+    const double* graph_vm = nullptr;
+    cudaEvent_t ev[8] = {};
+    int launches_per_iter = 0;
+    long long launches_last = 0;
+
+    ~gse_plan();
+};
+
+namespace {
+
+int fail(gse_plan* p, int code, const std::string& msg, int area = -1, int pivot = -1) {
+    p->err.code = code; p->err.area = area; p->err.pivot = pivot;
+    snprintf(p->err.message, sizeof(p->err.message), "%s", msg.c_str());
+    return code;
+}
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(plan, GSE_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// all kernels of one outer iteration on plan->stream; phase boundaries marked with events if timed
+int enqueue_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
+    launch_eval(plan->ep, va, vm, plan->stream);
+    launch_accumulate(plan->acc_ptr.ptr, plan->acc_a.ptr, plan->acc_b.ptr, plan->g.ptr, plan->gw.ptr, plan->wrg.ptr,
+                      plan->gval.ptr, (int64_t)plan->hp.n_gval, plan->stream);
+    return 2;
+}
+int enqueue_fwd(gse_plan* plan, int phase) {
+    int n = 0;
+    for (auto& L : plan->fwd) {
+        if (L.phase != phase) continue;
+        launch_front_tasks(L.pclass, plan->ft, plan->tasks.ptr + L.first, L.count, L.smem, plan->gval.ptr, plan->lbuf.ptr,
+                           plan->ubuf.ptr, plan->flags.ptr + 1, plan->stream);
+        ++n;
+    }
+    return n;
+}
+int enqueue_bwd(gse_plan* plan, int phase) {
+    int n = 0;
+    for (auto& B : plan->bwd) {
+        if (B.phase != phase) continue;
+        launch_backward(plan->ft, plan->bwd_fronts.ptr + B.first, B.count, B.max_u, plan->lbuf.ptr, plan->xsol.ptr, plan->stream);
+        ++n;
+    }
+    return n;
+}
+int enqueue_update(gse_plan* plan, double* va, double* vm) {
+    launch_update(plan->upd_bus.ptr, plan->upd_quant.ptr, plan->upd_pos.ptr, (int)plan->upd_bus.n, plan->xsol.ptr, va, vm,
+                  plan->flags.ptr, plan->stream);
+    return 1;
+}
+
+int enqueue_iteration(gse_plan* plan, double* va, double* vm, bool events) {
+    cudaStream_t s = plan->stream;
+    int n = 0;
+    cudaMemsetAsync(plan->flags.ptr, 0, sizeof(unsigned long long), s);
+    if (events) cudaEventRecord(plan->ev[0], s);
+    n += enqueue_phase_assemble(plan, va, vm);
+    if (events) cudaEventRecord(plan->ev[1], s);
+    n += enqueue_fwd(plan, 1);
+    if (events) cudaEventRecord(plan->ev[2], s);
+    n += enqueue_fwd(plan, 2);
+    if (events) cudaEventRecord(plan->ev[3], s);
+    n += enqueue_fwd(plan, 3);
+    n += enqueue_bwd(plan, 3);
+    if (events) cudaEventRecord(plan->ev[4], s);
+    n += enqueue_bwd(plan, 4);
+    n += enqueue_update(plan, va, vm);
+    if (events) cudaEventRecord(plan->ev[5], s);
+    cudaMemcpyAsync(plan->h_flags, plan->flags.ptr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    return n;
+}
+
+int decode_failure(gse_plan* plan, unsigned long long code) {
+    const int f = (int)(code >> 32), k = (int)(code & 0xffffffffull);
+    const Front& fr = plan->hp.fronts[f];
+    const int pos = fr.rows[k];
+    const int orig = plan->hp.perm_orig[pos];
+    char buf[160];
+    if (fr.kind == 3) {
+        snprintf(buf, sizeof buf, "boundary system not positive definite at pivot %d", orig);
+        return fail(plan, GSE_E_NOT_SPD_BOUNDARY, buf, -1, orig);
+    }
+    snprintf(buf, sizeof buf, "area %d interior block not positive definite at pivot %d", fr.area, orig);
+    return fail(plan, GSE_E_NOT_SPD_AREA, buf, fr.area, orig);
+}
+
+int ensure_graph(gse_plan* plan, double* va, double* vm) {
+    if (plan->graph && plan->graph_va == va && plan->graph_vm == vm) return GSE_OK;
+    if (plan->graph) { cudaGraphExecDestroy(plan->graph); plan->graph = nullptr; }
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+    plan->launches_per_iter = enqueue_iteration(plan, va, vm, false);
+    CU(cudaStreamEndCapture(plan->stream, &g));
+    CU(cudaGraphInstantiate(&plan->graph, g, 0));
+    cudaGraphDestroy(g);
+    plan->graph_va = va; plan->graph_vm = vm;
+    return GSE_OK;
+}
+
+}  // namespace
+
+gse_plan::~gse_plan() {
+    cudaSetDevice(device);
+    if (graph) cudaGraphExecDestroy(graph);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (h_flags) cudaFreeHost(h_flags);
+    if (h_obj) cudaFreeHost(h_obj);
+    DevBuf<int32_t>* ib[] = {&y_ptr, &y_idx, &br_from, &br_to, &m_type, &m_target, &vm_bus, &vm_row, &vm_slot, &fl_branch,
+                             &fl_from, &fl_to, &fl_row, &fl_slot, &inj_bus, &inj_rowp, &inj_rowq, &inj_slotp, &inj_slotq,
+                             &acc_ptr, &acc_a, &acc_b, &racc_ptr, &racc_a, &racc_b, &f_p, &f_u1, &f_T, &f_nchild,
+                             &f_child_ptr, &f_children, &f_rel_off, &f_rel, &f_reg_off, &f_reg_ptr, &f_rows_off, &f_rows,
+                             &bwd_fronts, &upd_bus, &upd_quant, &upd_pos};
+    for (auto* b : ib) b->release();
+    DevBuf<double>* db[] = {&y_g, &y_b, &br_y, &z, &w, &g, &gw, &wrg, &gval, &refval, &lbuf, &ubuf, &xsol, &obj_partial, &status};
+    for (auto* b : db) b->release();
+    orig_pos.release(); f_gval_off.release(); f_l_off.release(); f_u_off.release(); tasks.release(); flags.release();
+}
+
+extern "C" {
+
+const char* gse_version(void) { return "gridse-b200 0.1.0 (sm_100a)"; }
+
+const gse_error* gse_last_error(const gse_plan* plan) { return &plan->err; }
+
+int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan** out) {
+    if (!d || !out) return GSE_E_INVALID;
+    gse_plan* plan = new gse_plan();
+    *out = plan;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(plan, GSE_E_NO_DEVICE, "no CUDA device visible: gridse-b200 has no CPU fallback");
+    plan->device = opt ? opt->device : 0;
+    CU(cudaSetDevice(plan->device));
+    BuildOptions bo;
+    if (opt) {
+        bo.dense = opt->backend_dense != 0;
+        if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
+        if (opt->max_pivots == 32 || opt->max_pivots == 64) bo.max_pivots = opt->max_pivots;
+        bo.rank = opt->rank; bo.world = std::max(1, opt->world);
+        if (opt->area_rank) bo.area_rank.assign(opt->area_rank, opt->area_rank + d->n_areas);
+    }
+    plan->coordinator = bo.rank == 0;
+    HostProgram& hp = plan->hp;
+    std::string msg = build_host_program(*d, bo, hp);
+    if (!msg.empty()) return fail(plan, GSE_E_INVALID, msg);
+    if (hp.max_front >= 65535) return fail(plan, GSE_E_INVALID, "front order exceeds 65534");
+
+    CU(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+    CU(configure_kernels());
+    for (auto& e : plan->ev) CU(cudaEventCreate(&e));
+    CU(cudaMallocHost(&plan->h_flags, 2 * sizeof(unsigned long long)));
+    CU(cudaMallocHost(&plan->h_obj, sizeof(double)));
+
+    // ---- network / measurements ----
+    const int nb = d->n_bus, nnz = d->y_ptr[nb];
+    CU(plan->y_ptr.upload(std::vector<int32_t>(d->y_ptr, d->y_ptr + nb + 1)));
+    CU(plan->y_idx.upload(std::vector<int32_t>(d->y_idx, d->y_idx + nnz)));
+    CU(plan->y_g.upload(std::vector<double>(d->y_g, d->y_g + nnz)));
+    CU(plan->y_b.upload(std::vector<double>(d->y_b, d->y_b + nnz)));
+    CU(plan->br_from.upload(std::vector<int32_t>(d->br_from, d->br_from + d->n_branch)));
+    CU(plan->br_to.upload(std::vector<int32_t>(d->br_to, d->br_to + d->n_branch)));
+    CU(plan->br_y.upload(std::vector<double>(d->br_y, d->br_y + 8 * (size_t)d->n_branch)));
+    CU(plan->m_type.upload(std::vector<int32_t>(d->m_type, d->m_type + d->n_rows)));
+    CU(plan->m_target.upload(std::vector<int32_t>(d->m_target, d->m_target + d->n_rows)));
+    CU(plan->z.upload(std::vector<double>(d->m_z, d->m_z + d->n_rows)));
+    CU(plan->w.upload(std::vector<double>(d->m_w, d->m_w + d->n_rows)));
+    // ---- evaluation units ----
+    CU(plan->vm_bus.upload(hp.vm_bus)); CU(plan->vm_row.upload(hp.vm_row)); CU(plan->vm_slot.upload(hp.vm_slot));
+    CU(plan->fl_branch.upload(hp.fl_branch)); CU(plan->fl_from.upload(hp.fl_from)); CU(plan->fl_to.upload(hp.fl_to));
+    CU(plan->fl_row.upload(hp.fl_row)); CU(plan->fl_slot.upload(hp.fl_slot));
+    CU(plan->inj_bus.upload(hp.inj_bus)); CU(plan->inj_rowp.upload(hp.inj_rowp)); CU(plan->inj_rowq.upload(hp.inj_rowq));
+    CU(plan->inj_slotp.upload(hp.inj_slotp)); CU(plan->inj_slotq.upload(hp.inj_slotq));
+    CU(plan->g.alloc(hp.n_slots)); CU(plan->gw.alloc(hp.n_slots)); CU(plan->wrg.alloc(hp.n_slots));
+    CU(plan->acc_ptr.upload(hp.acc_ptr)); CU(plan->acc_a.upload(hp.acc_a)); CU(plan->acc_b.upload(hp.acc_b));
+    CU(plan->racc_ptr.upload(hp.racc_ptr)); CU(plan->racc_a.upload(hp.racc_a)); CU(plan->racc_b.upload(hp.racc_b));
+    CU(plan->gval.alloc(hp.n_gval)); CU(plan->refval.alloc(hp.n_ref_vals));
+    EvalProg& ep = plan->ep;
+    ep.y_ptr = plan->y_ptr.ptr; ep.y_idx = plan->y_idx.ptr; ep.y_g = plan->y_g.ptr; ep.y_b = plan->y_b.ptr;
+    ep.br_y = plan->br_y.ptr; ep.z = plan->z.ptr; ep.w = plan->w.ptr; ep.slack = d->slack;
+    ep.n_vm = (int)hp.vm_bus.size(); ep.n_fl = (int)hp.fl_branch.size(); ep.n_inj = (int)hp.inj_bus.size();
+    ep.vm_bus = plan->vm_bus.ptr; ep.vm_row = plan->vm_row.ptr; ep.vm_slot = plan->vm_slot.ptr;
+    ep.fl_branch = plan->fl_branch.ptr; ep.fl_from = plan->fl_from.ptr; ep.fl_to = plan->fl_to.ptr;
+    ep.fl_row = plan->fl_row.ptr; ep.fl_slot = plan->fl_slot.ptr;
+    ep.inj_bus = plan->inj_bus.ptr; ep.inj_rowp = plan->inj_rowp.ptr; ep.inj_rowq = plan->inj_rowq.ptr;
+    ep.inj_slotp = plan->inj_slotp.ptr; ep.inj_slotq = plan->inj_slotq.ptr;
+    ep.g = plan->g.ptr; ep.gw = plan->gw.ptr; ep.wrg = plan->wrg.ptr;
+
+    // ---- front tables ----
+    const size_t nf = hp.fronts.size();
+    std::vector<int32_t> fp(nf), fu(nf), fT(nf), fnc(nf), fcp(nf), frel_off(nf), frows_off(nf), children, rel, rows;
+    std::vector<int64_t> fg(nf), fl(nf), fuo(nf);
+    for (size_t i = 0; i < nf; ++i) {
+        const Front& f = hp.fronts[i];
+        fp[i] = f.p; fu[i] = f.u1; fT[i] = std::max(f.T, 1); fnc[i] = (int)f.children.size(); fcp[i] = (int)children.size();
+        children.insert(children.end(), f.children.begin(), f.children.end());
+        frel_off[i] = (int)rel.size(); rel.insert(rel.end(), f.rel.begin(), f.rel.end());
+        frows_off[i] = (int)rows.size(); rows.insert(rows.end(), f.rows.begin(), f.rows.end());
+        fg[i] = f.gval_off; fl[i] = f.l_off; fuo[i] = f.u_off;
+    }
+    CU(plan->f_p.upload(fp)); CU(plan->f_u1.upload(fu)); CU(plan->f_T.upload(fT)); CU(plan->f_nchild.upload(fnc));
+    CU(plan->f_child_ptr.upload(fcp)); CU(plan->f_children.upload(children)); CU(plan->f_rel_off.upload(frel_off));
+    CU(plan->f_rel.upload(rel)); CU(plan->f_reg_off.upload(hp.front_reg_off)); CU(plan->f_reg_ptr.upload(hp.reg_ptr));
+    CU(plan->f_rows_off.upload(frows_off)); CU(plan->f_rows.upload(rows)); CU(plan->orig_pos.upload(hp.orig_pos));
+    CU(plan->f_gval_off.upload(fg)); CU(plan->f_l_off.upload(fl)); CU(plan->f_u_off.upload(fuo));
+    CU(plan->lbuf.alloc(hp.n_lbuf)); CU(plan->ubuf.alloc(hp.n_ubuf)); CU(plan->xsol.alloc(hp.n_pos + 2));
+    FrontTab& ft = plan->ft;
+    ft.p = plan->f_p.ptr; ft.u1 = plan->f_u1.ptr; ft.T = plan->f_T.ptr; ft.nchild = plan->f_nchild.ptr;
+    ft.child_ptr = plan->f_child_ptr.ptr; ft.children = plan->f_children.ptr; ft.rel_off = plan->f_rel_off.ptr;
+    ft.rel = plan->f_rel.ptr; ft.reg_off = plan->f_reg_off.ptr; ft.reg_ptr = plan->f_reg_ptr.ptr;
+    ft.orig_pos = plan->orig_pos.ptr; ft.gval_off = plan->f_gval_off.ptr; ft.l_off = plan->f_l_off.ptr;
+    ft.u_off = plan->f_u_off.ptr; ft.rows_off = plan->f_rows_off.ptr; ft.rows = plan->f_rows.ptr;
+
+    // ---- level launches: tasks grouped by (level, pivot class) ----
+    std::vector<TaskRec> trecs;
+    for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
+        for (int pclass : {64, 32, 0}) {
+            LevelLaunch L{pclass, (int)trecs.size(), 0, 0, hp.level_phase[lv]};
+            for (const Task& t : hp.fwd_levels[lv]) {
+                const Front& f = hp.fronts[t.front];
+                const int cls = f.p == 0 ? 0 : f.p <= 32 ? 32 : 64;
+                if (cls != pclass) continue;
+                const int ni = std::min(f.T, f.u1 - t.ci * f.T), nj = std::min(f.T, f.u1 - t.cj * f.T);
+                L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, t.ci == t.cj));
+                trecs.push_back({t.front, t.ci, t.cj, 0});
+                ++L.count;
+            }
+            if (L.count) {
+                if (L.smem > 227 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
+                plan->fwd.push_back(L);
+            }
+        }
+    }
+    CU(plan->tasks.upload(trecs));
+    std::vector<int32_t> bfronts;
+    for (size_t i = 0; i < hp.bwd_levels.size(); ++i) {
+        BwdLaunch B{(int)bfronts.size(), (int)hp.bwd_levels[i].size(), 0, hp.bwd_phase[i]};
+        for (int f : hp.bwd_levels[i]) { B.max_u = std::max(B.max_u, hp.fronts[f].u1); bfronts.push_back(f); }
+        if (B.max_u > 15000) return fail(plan, GSE_E_INVALID, "update set too large for the backward kernel");
+        plan->bwd.push_back(B);
+    }
+    CU(plan->bwd_fronts.upload(bfronts));
+    CU(plan->upd_bus.upload(hp.upd_bus)); CU(plan->upd_quant.upload(hp.upd_quant)); CU(plan->upd_pos.upload(hp.upd_pos));
+    CU(plan->obj_partial.alloc(objective_blocks(d->n_rows) + 1));
+    CU(plan->status.alloc(2));
+    CU(plan->flags.alloc(2));
+    CU(cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long)));
+    CU(cudaDeviceSynchronize());
+    plan->err.code = GSE_OK; plan->err.area = -1; plan->err.pivot = -1; plan->err.message[0] = 0;
+    return GSE_OK;
+}
+
+void gse_plan_destroy(gse_plan* plan) { delete plan; }
+
+int gse_set_weights(gse_plan* plan, const double* w) {
+    CU(cudaSetDevice(plan->device));
+    CU(cudaMemcpy(plan->w.ptr, w, sizeof(double) * plan->hp.n_rows, cudaMemcpyHostToDevice));
+    return GSE_OK;
+}
+int gse_set_measurements(gse_plan* plan, const double* z) {
+    CU(cudaSetDevice(plan->device));
+    CU(cudaMemcpy(plan->z.ptr, z, sizeof(double) * plan->hp.n_rows, cudaMemcpyHostToDevice));
+    return GSE_OK;
+}
+
+int gse_check(gse_plan* plan) {
+    CU(cudaSetDevice(plan->device));
+    unsigned long long code = 0;
+    CU(cudaStreamSynchronize(plan->stream));
+    CU(cudaMemcpy(&code, plan->flags.ptr + 1, sizeof code, cudaMemcpyDeviceToHost));
+    if (code == ~0ull) return GSE_OK;
+    CU(cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long)));
+    return decode_failure(plan, code);
+}
+
+int gse_iterate(gse_plan* plan, double* va, double* vm, double* delta_inf) {
+    CU(cudaSetDevice(plan->device));
+    int rc = ensure_graph(plan, va, vm);
+    if (rc) return rc;
+    CU(cudaGraphLaunch(plan->graph, plan->stream));
+    CU(cudaStreamSynchronize(plan->stream));
+    plan->launches_last = plan->launches_per_iter;
+    if (plan->h_flags[1] != ~0ull) {
+        unsigned long long code = plan->h_flags[1];
+        cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+        return decode_failure(plan, code);
+    }
+    double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
+    if (delta_inf) *delta_inf = dv;
+    return GSE_OK;
+}
+
+int gse_objective(gse_plan* plan, const double* va, const double* vm, double* j_out) {
+    CU(cudaSetDevice(plan->device));
+    launch_objective(plan->ep, plan->m_type.ptr, plan->m_target.ptr, plan->br_from.ptr, plan->br_to.ptr, plan->hp.n_rows, va, vm,
+                     plan->obj_partial.ptr, plan->obj_partial.ptr + objective_blocks(plan->hp.n_rows), plan->stream);
+    CU(cudaMemcpyAsync(plan->h_obj, plan->obj_partial.ptr + objective_blocks(plan->hp.n_rows), sizeof(double),
+                       cudaMemcpyDeviceToHost, plan->stream));
+    CU(cudaStreamSynchronize(plan->stream));
+    *j_out = *plan->h_obj;
+    return GSE_OK;
+}
+
+int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse_report* rep) {
+    CU(cudaSetDevice(plan->device));
+    memset(rep, 0, sizeof *rep);
+    const int max_it = std::min(cfg->max_outer_iterations, 64);
+    const bool timed = cfg->time_phases != 0;
+    if (!timed) { int rc = ensure_graph(plan, va, vm); if (rc) return rc; }
+    plan->launches_last = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    int status = GSE_OK;
+    for (int it = 1; it <= max_it; ++it) {
+        if (timed) plan->launches_last += enqueue_iteration(plan, va, vm, true);
+        else { CU(cudaGraphLaunch(plan->graph, plan->stream)); plan->launches_last += plan->launches_per_iter; }
+        CU(cudaStreamSynchronize(plan->stream));
+        if (timed)
+            for (int ph = 0; ph < 5; ++ph) { float ms = 0; cudaEventElapsedTime(&ms, plan->ev[ph], plan->ev[ph + 1]); rep->phase_s[ph] += ms * 1e-3; }
+        rep->iterations = it;
+        if (plan->h_flags[1] != ~0ull) {
+            unsigned long long code = plan->h_flags[1];
+            cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+            status = decode_failure(plan, code);
+            break;
+        }
+        double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
+        rep->delta_inf[it - 1] = dv;
+        if (dv < cfg->convergence_tol) { rep->converged = 1; break; }
+    }
+    rep->loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (status != GSE_OK) return status;
+    return gse_objective(plan, va, vm, &rep->objective);
+}
+
+// ---- phase-level entry points ------------------------------------------------------------------
+int gse_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
+    CU(cudaSetDevice(plan->device));
+    enqueue_phase_assemble(plan, va, vm);
+    // reference-layout blocks for component parity (same slot values, second destination map)
+    launch_accumulate(plan->racc_ptr.ptr, plan->racc_a.ptr, plan->racc_b.ptr, plan->g.ptr, plan->gw.ptr, plan->wrg.ptr,
+                      plan->refval.ptr, (int64_t)plan->hp.n_ref_vals, plan->stream);
+    CU(cudaStreamSynchronize(plan->stream));
+    return GSE_OK;
+}
+int gse_phase_condense(gse_plan* plan) {
+    CU(cudaSetDevice(plan->device));
+    enqueue_fwd(plan, 1);
+    return gse_check(plan);
+}
+int gse_phase_boundary(gse_plan* plan) {
+    CU(cudaSetDevice(plan->device));
+    if (!plan->coordinator) return GSE_OK;
+    enqueue_fwd(plan, 2); enqueue_fwd(plan, 3); enqueue_bwd(plan, 3);
+    return gse_check(plan);
+}
+int gse_phase_recover(gse_plan* plan, double* va, double* vm, double* delta_inf) {
+    CU(cudaSetDevice(plan->device));
+    CU(cudaMemsetAsync(plan->flags.ptr, 0, sizeof(unsigned long long), plan->stream));
+    enqueue_bwd(plan, 4);
+    enqueue_update(plan, va, vm);
+    CU(cudaMemcpyAsync(plan->h_flags, plan->flags.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, plan->stream));
+    CU(cudaStreamSynchronize(plan->stream));
+    double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
+    if (delta_inf) *delta_inf = dv;
+    CU(cudaMemcpy(plan->status.ptr, &dv, sizeof dv, cudaMemcpyHostToDevice));
+    return GSE_OK;
+}
+
+// ---- readback ------------------------------------------------------------------------------------
+int gse_area_dims(const gse_plan* plan, int32_t a, int32_t* out) {
+    const HostProgram& hp = plan->hp;
+    if (a < 0 || a >= hp.n_areas) return GSE_E_INVALID;
+    out[0] = hp.area_ni[a]; out[1] = hp.area_nb[a];
+    out[2] = (int)hp.ii_idx[a].size(); out[3] = (int)hp.ib_idx[a].size();
+    int nfr = 0; int64_t lnz = 0;
+    for (auto& f : hp.fronts) if (f.area == a && f.kind == 0) { ++nfr; lnz += (int64_t)(f.p + f.u1 - 1) * f.p; }
+    out[4] = 0; out[5] = 0; out[6] = nfr; out[7] = (int32_t)std::min<int64_t>(lnz, 2147483647);
+    return GSE_OK;
+}
+int gse_area_pattern(const gse_plan* plan, int32_t a, int32_t* ii_ptr, int32_t* ii_idx, int32_t* ib_ptr, int32_t* ib_idx) {
+    const HostProgram& hp = plan->hp;
+    if (a < 0 || a >= hp.n_areas) return GSE_E_INVALID;
+    memcpy(ii_ptr, hp.ii_ptr[a].data(), hp.ii_ptr[a].size() * 4); memcpy(ii_idx, hp.ii_idx[a].data(), hp.ii_idx[a].size() * 4);
+    memcpy(ib_ptr, hp.ib_ptr[a].data(), hp.ib_ptr[a].size() * 4); memcpy(ib_idx, hp.ib_idx[a].data(), hp.ib_idx[a].size() * 4);
+    return GSE_OK;
+}
+int gse_area_blocks(gse_plan* plan, int32_t a, double* data_ii, double* data_ib, double* g_bb, double* b_i, double* b_b) {
+    const HostProgram& hp = plan->hp;
+    if (a < 0 || a >= hp.n_areas || !hp.owned[a]) return fail(plan, GSE_E_INVALID, "area not owned by this plan");
+    CU(cudaSetDevice(plan->device));
+    const size_t nii = hp.ii_idx[a].size(), nib = hp.ib_idx[a].size(), nb = hp.area_nb[a], ni = hp.area_ni[a];
+    const double* base = plan->refval.ptr + hp.ref_off[a];
+    CU(cudaMemcpy(data_ii, base, nii * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(data_ib, base + nii, nib * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(g_bb, base + nii + nib, nb * nb * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(b_i, base + nii + nib + nb * nb, ni * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(b_b, base + nii + nib + nb * nb + ni, nb * 8, cudaMemcpyDeviceToHost));
+    return GSE_OK;
+}
+static int unpack_lower(gse_plan* plan, const Front& f, int n, double* full, double* rhs) {
+    std::vector<double> packed((size_t)f.u1 * (f.u1 + 1) / 2);
+    cudaError_t e = cudaMemcpy(packed.data(), plan->ubuf.ptr + f.u_off, packed.size() * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(plan, GSE_E_CUDA, cudaGetErrorString(e));
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= i; ++j) { double v = packed[(size_t)i * (i + 1) / 2 + j]; full[(size_t)i * n + j] = v; full[(size_t)j * n + i] = v; }
+    for (int j = 0; j < n; ++j) rhs[j] = packed[(size_t)n * (n + 1) / 2 + j];
+    return GSE_OK;
+}
+int gse_area_schur(gse_plan* plan, int32_t a, double* s_b, double* b_hat) {
+    const HostProgram& hp = plan->hp;
+    if (a < 0 || a >= hp.n_areas) return GSE_E_INVALID;
+    CU(cudaSetDevice(plan->device));
+    return unpack_lower(plan, hp.fronts[hp.area_root[a]], hp.area_nb[a], s_b, b_hat);
+}
+int gse_boundary_system(gse_plan* plan, double* s_gamma, double* b_gamma, double* dx_gamma) {
+    const HostProgram& hp = plan->hp;
+    CU(cudaSetDevice(plan->device));
+    if (hp.n_gamma == 0) return GSE_OK;
+    if (hp.gamma_root < 0) return fail(plan, GSE_E_INVALID, "boundary system lives on the coordinator rank");
+    int rc = unpack_lower(plan, hp.fronts[hp.gamma_root], hp.n_gamma, s_gamma, b_gamma);
+    if (rc) return rc;
+    CU(cudaMemcpy(dx_gamma, plan->xsol.ptr + hp.gamma_base, hp.n_gamma * 8, cudaMemcpyDeviceToHost));
+    return GSE_OK;
+}
+int gse_area_delta(gse_plan* plan, int32_t a, double* dx_i) {
+    const HostProgram& hp = plan->hp;
+    if (a < 0 || a >= hp.n_areas || !hp.owned[a]) return fail(plan, GSE_E_INVALID, "area not owned by this plan");
+    CU(cudaSetDevice(plan->device));
+    const int ni = hp.area_ni[a];
+    std::vector<double> x(ni);
+    CU(cudaMemcpy(x.data(), plan->xsol.ptr + hp.area_base[a], ni * 8, cudaMemcpyDeviceToHost));
+    for (int e = 0; e < ni; ++e) dx_i[hp.perm_orig[hp.area_base[a] + e]] = x[e];
+    return GSE_OK;
+}
+int gse_set_boundary_delta(gse_plan* plan, const double* dx_gamma) {
+    CU(cudaSetDevice(plan->device));
+    CU(cudaMemcpy(plan->xsol.ptr + plan->hp.gamma_base, dx_gamma, plan->hp.n_gamma * 8, cudaMemcpyHostToDevice));
+    return GSE_OK;
+}
+
+double* gse_exchange_buffer_dev(gse_plan* plan, int64_t* n) { if (n) *n = plan->hp.xchg_len; return plan->ubuf.ptr + plan->hp.xchg_off; }
+int gse_exchange_offsets(const gse_plan* plan, int64_t* off) {
+    for (size_t i = 0; i < plan->hp.xchg_area_off.size(); ++i) off[i] = plan->hp.xchg_area_off[i];
+    return GSE_OK;
+}
+double* gse_boundary_delta_dev(gse_plan* plan) { return plan->xsol.ptr + plan->hp.gamma_base; }
+double* gse_status_dev(gse_plan* plan) { return plan->status.ptr; }
+
+int gse_plan_stats(const gse_plan* plan, double* s, int32_t n) {
+    const HostProgram& hp = plan->hp;
+    double v[12] = {(double)plan->launches_last, (double)hp.fronts.size(), (double)hp.fwd_levels.size(), (double)plan->tasks.n,
+                    (double)hp.max_front, (double)hp.n_lbuf, (double)hp.n_ubuf, (double)hp.n_pairs, (double)hp.n_slots,
+                    hp.alg_bytes, hp.dense_flops, (double)plan->launches_per_iter};
+    for (int i = 0; i < n && i < 12; ++i) s[i] = v[i];
+    return GSE_OK;
+}
+
+}  // extern "C"

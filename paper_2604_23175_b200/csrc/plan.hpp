@@ -1,0 +1,100 @@
+// plan.hpp -- host-side symbolic structures and the device program layout.
+//
+// One plan = one (network, measurement set, partition) triple analysed once
+// (the reference re-runs build_patterns + symbolic_analyze inside every solve,
+// solver.py:221-229; here both are plan-time).  Everything the GN loop touches
+// lives in flat int32 / float64 device arrays described by DevProgram.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/gridse_b200.h"
+
+namespace gse {
+
+// ---------------------------------------------------------------------------
+// Fronts.  The whole hierarchy -- area interiors (nested dissection), one
+// assembly-only root per area (its update matrix IS the Schur block S_b with
+// b_hat as the extra row), the boundary assembly root (S_Gamma, b_Gamma) and the
+// dense boundary factorisation (a chain of fronts) -- is ONE multifrontal tree.
+// ---------------------------------------------------------------------------
+struct Front {
+    int area = -1;          // owning area, -1 for coordinator fronts
+    int kind = 0;           // 0 interior, 1 area root (S_b), 2 gamma root (S_Gamma), 3 chain
+    int p = 0;              // pivots eliminated here
+    int u1 = 0;             // update rows including the trailing RHS row
+    int parent = -1;
+    int level = 0;
+    int T = 0, nch = 0;     // update-row chunking
+    std::vector<int> rows;  // global positions of [pivots | update rows] (RHS row not listed)
+    std::vector<int> children;
+    std::vector<int> rel;   // as a child: update row i -> local row of the parent
+    int64_t l_off = 0, u_off = 0, gval_off = 0;
+    int n_orig = 0;
+};
+
+struct Task { int front, ci, cj; };
+
+struct HostProgram {
+    // sizes
+    int n_bus = 0, n_rows = 0, n_areas = 0, n_gamma = 0, slack = 0;
+    int64_t n_slots = 0, n_pairs = 0;
+    int n_pos = 0;                       // length of the global solution vector
+    int gamma_base = 0;                  // first position of x_Gamma in it
+    std::vector<int> area_base;          // first interior position of each area
+    std::vector<int> area_ni, area_nb;
+    std::vector<int> owned;              // 1 if this rank assembles / factors the area
+    int rank = 0, world = 1;
+
+    // template evaluation units
+    std::vector<int32_t> vm_bus, vm_row, vm_slot;
+    std::vector<int32_t> fl_branch, fl_from, fl_to, fl_row /*4 per unit*/, fl_slot /*4 per unit*/;
+    std::vector<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq;
+
+    // accumulation: destination-sorted contribution lists (solver layout -> gval)
+    std::vector<int32_t> acc_ptr, acc_a, acc_b;     // b == -1: right-hand-side term wrg[a]
+    // reference layout (component parity): per area CSR patterns + a second program
+    std::vector<std::vector<int32_t>> ii_ptr, ii_idx, ib_ptr, ib_idx;
+    std::vector<int64_t> ref_off;        // per area offset into the ref-layout value array
+    std::vector<int32_t> racc_ptr, racc_a, racc_b;
+    int64_t n_ref_vals = 0;
+    std::vector<int32_t> perm_orig;      // per position: original local variable (error reports)
+
+    // fronts / tasks / levels
+    std::vector<Front> fronts;
+    std::vector<int> area_root;          // front id of each area's root
+    int gamma_root = -1;
+    std::vector<std::vector<Task>> fwd_levels;      // factor tasks per level
+    std::vector<std::vector<int>> bwd_levels;       // fronts per backward level (top-down)
+    std::vector<int> level_phase;        // 1 local_condense, 2 boundary_assemble, 3 boundary_solve
+    std::vector<int> bwd_phase;          // 3 boundary_solve, 4 recovery
+    // original entries per front: (row_local << 16 | col_local), region table
+    std::vector<uint32_t> orig_pos;
+    std::vector<int32_t> reg_ptr;        // flattened per-front region pointers
+    std::vector<int32_t> front_reg_off;  // per front offset into reg_ptr
+    int64_t n_gval = 0, n_lbuf = 0, n_ubuf = 0;
+    // exchange buffer = U storage of the area roots, contiguous in area order
+    int64_t xchg_off = 0, xchg_len = 0;
+    std::vector<int64_t> xchg_area_off;  // n_areas + 1 (relative to xchg_off)
+
+    // state update: one entry per solved variable
+    std::vector<int32_t> upd_bus, upd_quant, upd_pos;
+
+    // stats
+    double alg_bytes = 0, dense_flops = 0;
+    int max_front = 0;
+};
+
+struct BuildOptions {
+    bool dense = false;
+    int leaf_buses = 12;
+    int max_pivots = 64;
+    int rank = 0, world = 1;
+    std::vector<int> area_rank;
+};
+
+// symbolic.cpp
+std::string build_host_program(const gse_problem_desc& d, const BuildOptions& opt, HostProgram& hp);
+
+}  // namespace gse

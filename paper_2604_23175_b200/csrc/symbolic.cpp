@@ -1,0 +1,684 @@
+// symbolic.cpp -- plan-time analysis on the host (runs once per plan).
+//
+// Replaces, for every area at once, the reference's build_patterns /
+// _build_pair_programs (assembly.py:172-400) and SparseCholeskyCache._analyze
+// (linalg.py:156-231):
+//   * template slots in the reference's slot order + SoA evaluation units
+//     (VM rows, one unit per measured branch, one unit per measured bus);
+//   * CSR patterns of G_ii / G_ib in the reference layout (component parity);
+//   * a nested-dissection ordering of each area's interior on the bus graph
+//     (the ordering is free: SPEC.md "ordering is an implementation choice"),
+//     relaxed supernodes ("fronts") of at most max_pivots columns, their update
+//     sets and the assembly tree;
+//   * one assembly-only root front per area (Schur mode: boundary variables are
+//     never eliminated locally), the boundary assembly root and the dense
+//     boundary factorisation as a chain of fronts;
+//   * destination-sorted contribution lists: for every stored entry of every
+//     front (and of the right-hand-side row) the template slot pairs that add
+//     into it, in ascending row order -- the deterministic, atomic-free
+//     replacement of the five bincount scatters (assembly.py:502-520).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "plan.hpp"
+
+namespace gse {
+namespace {
+
+struct AreaSym {
+    int ni = 0, nb = 0;
+    std::vector<int> var_bus;            // interior variable -> index into im_bus
+    std::vector<int> th_var, vm_var;     // per interior bus index: variable ids (-1 none)
+    std::vector<int> epos, order;        // variable -> elimination position and inverse
+    std::vector<int> rows;               // global row ids owned, ascending
+    std::vector<int> slot_ptr, slot_var; // reference template layout
+    int64_t slot_base = 0;
+    // lower-triangular pattern in position space incl. boundary (pos >= ni) and RHS row (pos == ni+nb)
+    std::vector<int> col_ptr, col_row;
+    std::vector<int64_t> col_dest;
+    std::vector<int> front_of_pos;       // interior position -> front id (global)
+    int first_front = 0, n_fronts = 0, root = -1;
+};
+
+// ---- nested dissection on the interior bus graph ---------------------------------
+struct NDGraph {
+    std::vector<int> xadj, adj;
+    std::vector<int> stamp, level;
+    int cur = 0;
+};
+
+void nd_recurse(NDGraph& g, std::vector<int>& verts, int leaf, std::vector<std::vector<int>>& out) {
+    const int n = (int)verts.size();
+    if (n == 0) return;
+    if (n <= leaf) { out.push_back(verts); return; }
+    // connected components of the induced subgraph
+    int tag = ++g.cur;
+    for (int v : verts) g.stamp[v] = tag;
+    std::vector<int> comp_tag_start;
+    {
+        std::vector<std::vector<int>> comps;
+        int seen_tag = ++g.cur;
+        for (int s : verts) {
+            if (g.stamp[s] != tag) continue;
+            std::vector<int> comp{s};
+            g.stamp[s] = seen_tag;
+            for (size_t h = 0; h < comp.size(); ++h) {
+                int u = comp[h];
+                for (int p = g.xadj[u]; p < g.xadj[u + 1]; ++p) {
+                    int w = g.adj[p];
+                    if (g.stamp[w] == tag) { g.stamp[w] = seen_tag; comp.push_back(w); }
+                }
+            }
+            comps.push_back(std::move(comp));
+        }
+        if (comps.size() > 1) {
+            for (auto& c : comps) { std::sort(c.begin(), c.end()); nd_recurse(g, c, leaf, out); }
+            return;
+        }
+    }
+    // level structure from a pseudo-peripheral vertex
+    tag = ++g.cur;
+    for (int v : verts) g.stamp[v] = tag;
+    int start = verts[0];
+    std::vector<int> bfs;
+    int depth = 0;
+    for (int sweep = 0; sweep < 3; ++sweep) {
+        int vis = ++g.cur;
+        bfs.assign(1, start);
+        g.stamp[start] = vis; g.level[start] = 0;
+        for (size_t h = 0; h < bfs.size(); ++h) {
+            int u = bfs[h];
+            for (int p = g.xadj[u]; p < g.xadj[u + 1]; ++p) {
+                int w = g.adj[p];
+                if (g.stamp[w] == tag) { g.stamp[w] = vis; g.level[w] = g.level[u] + 1; bfs.push_back(w); }
+            }
+        }
+        int d = g.level[bfs.back()];
+        // restore membership tag for the next sweep
+        for (int v : verts) g.stamp[v] = tag;
+        if (sweep > 0 && d <= depth) { depth = std::max(depth, d); break; }
+        depth = d;
+        // farthest vertex of smallest degree (ties: lowest id)
+        int best = -1, bdeg = 1 << 30;
+        for (int v : bfs) if (g.level[v] == d) {
+            int deg = g.xadj[v + 1] - g.xadj[v];
+            if (deg < bdeg || (deg == bdeg && v < best)) { best = v; bdeg = deg; }
+        }
+        if (sweep < 2) start = best;
+    }
+    // final BFS from `start` (levels valid for it)
+    {
+        int vis = ++g.cur;
+        bfs.assign(1, start);
+        g.stamp[start] = vis; g.level[start] = 0;
+        for (size_t h = 0; h < bfs.size(); ++h) {
+            int u = bfs[h];
+            for (int p = g.xadj[u]; p < g.xadj[u + 1]; ++p) {
+                int w = g.adj[p];
+                if (g.stamp[w] == tag) { g.stamp[w] = vis; g.level[w] = g.level[u] + 1; bfs.push_back(w); }
+            }
+        }
+        depth = g.level[bfs.back()];
+    }
+    if (depth < 2) { out.push_back(verts); return; }
+    std::vector<int> cnt(depth + 1, 0);
+    for (int v : verts) cnt[g.level[v]]++;
+    int best_j = 1; double best_cost = 1e300; int below = cnt[0];
+    for (int j = 1; j <= depth - 1; ++j) {
+        int above = n - below - cnt[j];
+        double cost = std::abs(below - above) + 2.0 * cnt[j];
+        if (cost < best_cost) { best_cost = cost; best_j = j; }
+        below += cnt[j];
+    }
+    std::vector<int> A, B, S;
+    for (int v : verts) {
+        int l = g.level[v];
+        if (l < best_j) A.push_back(v);
+        else if (l > best_j) B.push_back(v);
+        else {
+            bool touches_b = false;
+            for (int p = g.xadj[v]; p < g.xadj[v + 1] && !touches_b; ++p) {
+                int w = g.adj[p];
+                touches_b = (g.stamp[w] == g.cur) && g.level[w] == best_j + 1;
+            }
+            (touches_b ? S : A).push_back(v);
+        }
+    }
+    std::sort(A.begin(), A.end()); std::sort(B.begin(), B.end()); std::sort(S.begin(), S.end());
+    nd_recurse(g, A, leaf, out);
+    nd_recurse(g, B, leaf, out);
+    out.push_back(S);
+}
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+void choose_chunks(Front& f) {
+    const int TMAX = 96;
+    if (f.u1 <= TMAX) { f.T = f.u1; f.nch = f.u1 > 0 ? 1 : 0; return; }
+    int nch = (f.u1 + TMAX - 1) / TMAX;
+    int T = round_up((f.u1 + nch - 1) / nch, 8);
+    f.T = T; f.nch = (f.u1 + T - 1) / T;
+}
+
+}  // namespace
+
+std::string build_host_program(const gse_problem_desc& d, const BuildOptions& opt, HostProgram& hp) {
+    const int nbus = d.n_bus, K = d.n_areas, m = d.n_rows, ng = d.n_gamma;
+    if (nbus <= 0 || K <= 0 || m < 0) return "empty problem";
+    const int PMAX = opt.max_pivots;
+    hp.n_bus = nbus; hp.n_rows = m; hp.n_areas = K; hp.n_gamma = ng; hp.slack = d.slack;
+    hp.rank = opt.rank; hp.world = opt.world;
+    hp.owned.assign(K, 1);
+    if (!opt.area_rank.empty()) for (int a = 0; a < K; ++a) hp.owned[a] = opt.area_rank[a] == opt.rank;
+    const bool coordinator = opt.rank == 0;
+
+    std::vector<AreaSym> as(K);
+    hp.area_ni.resize(K); hp.area_nb.resize(K); hp.area_base.resize(K);
+    int pos_cursor = 0;
+    for (int a = 0; a < K; ++a) {
+        AreaSym& A = as[a];
+        int n_ia = d.ia_ptr[a + 1] - d.ia_ptr[a], n_im = d.im_ptr[a + 1] - d.im_ptr[a];
+        int n_ba = d.ba_ptr[a + 1] - d.ba_ptr[a], n_bm = d.bm_ptr[a + 1] - d.bm_ptr[a];
+        A.ni = n_ia + n_im; A.nb = n_ba + n_bm;
+        if (d.sel_ptr[a + 1] - d.sel_ptr[a] != A.nb) return "boundary selector length mismatch";
+        for (int j = 1; j < A.nb; ++j)
+            if (d.sel[d.sel_ptr[a] + j] <= d.sel[d.sel_ptr[a] + j - 1]) return "boundary selector must be increasing";
+        hp.area_ni[a] = A.ni; hp.area_nb[a] = A.nb; hp.area_base[a] = pos_cursor;
+        pos_cursor += A.ni;
+    }
+    hp.gamma_base = pos_cursor;
+    hp.n_pos = pos_cursor + ng;
+    hp.perm_orig.assign(hp.n_pos, -1);
+
+    // ---- rows per area -----------------------------------------------------------
+    for (int r = 0; r < m; ++r) {
+        int t = d.m_type[r], tg = d.m_target[r];
+        if (t < 0 || t > 6) return "unknown measurement type";
+        if (tg < 0 || tg >= (t >= 3 ? d.n_branch : nbus)) return "measurement target out of range";
+        int owner = t >= 3 ? d.br_from[tg] : tg;
+        as[d.area_of_bus[owner]].rows.push_back(r);
+    }
+
+    // ---- template slots + evaluation units ------------------------------------------
+    std::vector<int> loc_va(nbus, -1), loc_vm(nbus, -1);
+    std::vector<int> unit_of_branch(d.n_branch, -1), unit_of_bus(nbus, -1);
+    int64_t slot_cursor = 0;
+    hp.ii_ptr.resize(K); hp.ii_idx.resize(K); hp.ib_ptr.resize(K); hp.ib_idx.resize(K);
+    hp.ref_off.assign(K + 1, 0);
+    double nnz_total = 0, rhs_total = 0;
+
+    // reference-layout program pieces are collected per area then concatenated
+    std::vector<int64_t> rdest; std::vector<int32_t> ra, rb;   // (dest, a, b) in program order
+
+    for (int a = 0; a < K; ++a) {
+        AreaSym& A = as[a];
+        const int ni = A.ni, nb = A.nb;
+        const int n_ia = d.ia_ptr[a + 1] - d.ia_ptr[a];
+        const int n_ba = d.ba_ptr[a + 1] - d.ba_ptr[a];
+        // local variable ids of this area (closure: only these buses may be referenced)
+        std::vector<int> touched;
+        auto setv = [&](std::vector<int>& arr, int bus, int v) { arr[bus] = v; touched.push_back(bus); };
+        for (int i = 0; i < n_ia; ++i) setv(loc_va, d.ia_bus[d.ia_ptr[a] + i], i);
+        for (int i = d.im_ptr[a]; i < d.im_ptr[a + 1]; ++i) setv(loc_vm, d.im_bus[i], n_ia + (i - d.im_ptr[a]));
+        for (int i = 0; i < n_ba; ++i) setv(loc_va, d.ba_bus[d.ba_ptr[a] + i], ni + i);
+        for (int i = d.bm_ptr[a]; i < d.bm_ptr[a + 1]; ++i) setv(loc_vm, d.bm_bus[i], ni + n_ba + (i - d.bm_ptr[a]));
+        // interior bus index <-> variables
+        const int nib = d.im_ptr[a + 1] - d.im_ptr[a];
+        A.var_bus.assign(ni, -1); A.th_var.assign(nib, -1); A.vm_var.assign(nib, -1);
+        for (int i = 0; i < nib; ++i) {
+            int bus = d.im_bus[d.im_ptr[a] + i];
+            A.vm_var[i] = n_ia + i; A.var_bus[n_ia + i] = i;
+            if (loc_va[bus] >= 0 && loc_va[bus] < ni) { A.th_var[i] = loc_va[bus]; A.var_bus[loc_va[bus]] = i; }
+        }
+
+        A.slot_base = slot_cursor;
+        A.slot_ptr.assign(A.rows.size() + 1, 0);
+        bool closure_ok = true;
+        auto need = [&](int v) { if (v < 0) closure_ok = false; return v; };
+        for (size_t k = 0; k < A.rows.size(); ++k) {
+            int r = A.rows[k], t = d.m_type[r], tg = d.m_target[r];
+            int32_t gslot = (int32_t)(A.slot_base + A.slot_var.size());
+            if (t == 0) {
+                A.slot_var.push_back(need(loc_vm[tg]));
+                if (hp.owned[a]) { hp.vm_bus.push_back(tg); hp.vm_row.push_back(r); hp.vm_slot.push_back(gslot); }
+            } else if (t <= 2) {
+                for (int p = d.y_ptr[tg]; p < d.y_ptr[tg + 1]; ++p) if (d.y_idx[p] != d.slack) A.slot_var.push_back(need(loc_va[d.y_idx[p]]));
+                for (int p = d.y_ptr[tg]; p < d.y_ptr[tg + 1]; ++p) A.slot_var.push_back(need(loc_vm[d.y_idx[p]]));
+                if (hp.owned[a]) {
+                    int u = unit_of_bus[tg];
+                    if (u < 0) {
+                        u = unit_of_bus[tg] = (int)hp.inj_bus.size();
+                        hp.inj_bus.push_back(tg); hp.inj_rowp.push_back(-1); hp.inj_rowq.push_back(-1);
+                        hp.inj_slotp.push_back(-1); hp.inj_slotq.push_back(-1);
+                    }
+                    if (t == 1) { if (hp.inj_rowp[u] >= 0) return "duplicate injection row"; hp.inj_rowp[u] = r; hp.inj_slotp[u] = gslot; }
+                    else { if (hp.inj_rowq[u] >= 0) return "duplicate injection row"; hp.inj_rowq[u] = r; hp.inj_slotq[u] = gslot; }
+                }
+            } else {
+                int f = d.br_from[tg], tt = d.br_to[tg];
+                if (f != d.slack) A.slot_var.push_back(need(loc_va[f]));
+                if (tt != d.slack) A.slot_var.push_back(need(loc_va[tt]));
+                A.slot_var.push_back(need(loc_vm[f])); A.slot_var.push_back(need(loc_vm[tt]));
+                if (hp.owned[a]) {
+                    int u = unit_of_branch[tg];
+                    if (u < 0) {
+                        u = unit_of_branch[tg] = (int)hp.fl_branch.size();
+                        hp.fl_branch.push_back(tg); hp.fl_from.push_back(f); hp.fl_to.push_back(tt);
+                        for (int q = 0; q < 4; ++q) { hp.fl_row.push_back(-1); hp.fl_slot.push_back(-1); }
+                    }
+                    if (hp.fl_row[4 * u + (t - 3)] >= 0) return "duplicate flow row";
+                    hp.fl_row[4 * u + (t - 3)] = r; hp.fl_slot[4 * u + (t - 3)] = gslot;
+                }
+            }
+            A.slot_ptr[k + 1] = (int)A.slot_var.size();
+        }
+        if (!closure_ok) return "measurement row references a bus outside its area's variable map";
+        slot_cursor += (int64_t)A.slot_var.size();
+
+        // ---- reference-layout CSR patterns of G_ii, G_ib ------------------------------
+        std::vector<int64_t> cii, cib;
+        for (size_t k = 0; k < A.rows.size(); ++k)
+            for (int x = A.slot_ptr[k]; x < A.slot_ptr[k + 1]; ++x) {
+                int va = A.slot_var[x]; if (va >= ni) continue;
+                for (int y = A.slot_ptr[k]; y < A.slot_ptr[k + 1]; ++y) {
+                    int vb = A.slot_var[y];
+                    if (vb < ni) cii.push_back((int64_t)va * ni + vb); else cib.push_back((int64_t)va * std::max(nb, 1) + (vb - ni));
+                }
+            }
+        std::sort(cii.begin(), cii.end()); cii.erase(std::unique(cii.begin(), cii.end()), cii.end());
+        std::sort(cib.begin(), cib.end()); cib.erase(std::unique(cib.begin(), cib.end()), cib.end());
+        hp.ii_ptr[a].assign(ni + 1, 0); hp.ii_idx[a].resize(cii.size());
+        for (size_t i = 0; i < cii.size(); ++i) { hp.ii_ptr[a][cii[i] / std::max(ni, 1) + 1]++; hp.ii_idx[a][i] = (int32_t)(cii[i] % std::max(ni, 1)); }
+        for (int i = 0; i < ni; ++i) hp.ii_ptr[a][i + 1] += hp.ii_ptr[a][i];
+        hp.ib_ptr[a].assign(ni + 1, 0); hp.ib_idx[a].resize(cib.size());
+        for (size_t i = 0; i < cib.size(); ++i) { hp.ib_ptr[a][cib[i] / std::max(nb, 1) + 1]++; hp.ib_idx[a][i] = (int32_t)(cib[i] % std::max(nb, 1)); }
+        for (int i = 0; i < ni; ++i) hp.ib_ptr[a][i + 1] += hp.ib_ptr[a][i];
+        // ref value layout of the area: [data_ii | data_ib | g_bb | b_i | b_b]
+        int64_t base = hp.ref_off[a];
+        int64_t o_ib = base + (int64_t)cii.size(), o_bb = o_ib + (int64_t)cib.size();
+        int64_t o_bi = o_bb + (int64_t)nb * nb, o_bbv = o_bi + ni;
+        hp.ref_off[a + 1] = o_bbv + nb;
+        nnz_total += (double)cii.size() + (double)cib.size() + (double)nb * nb; rhs_total += ni + nb;
+        if (hp.owned[a]) {
+            for (size_t k = 0; k < A.rows.size(); ++k) {
+                int s0 = A.slot_ptr[k], s1 = A.slot_ptr[k + 1];
+                for (int x = s0; x < s1; ++x) {
+                    int va = A.slot_var[x];
+                    for (int y = s0; y < s1; ++y) {
+                        int vb = A.slot_var[y]; int64_t dest;
+                        if (va < ni && vb < ni) dest = base + (std::lower_bound(cii.begin(), cii.end(), (int64_t)va * ni + vb) - cii.begin());
+                        else if (va < ni) dest = o_ib + (std::lower_bound(cib.begin(), cib.end(), (int64_t)va * std::max(nb, 1) + (vb - ni)) - cib.begin());
+                        else if (vb >= ni) dest = o_bb + (int64_t)(va - ni) * nb + (vb - ni);
+                        else continue;
+                        rdest.push_back(dest); ra.push_back((int32_t)(A.slot_base + x)); rb.push_back((int32_t)(A.slot_base + y));
+                    }
+                }
+                for (int x = s0; x < s1; ++x) {
+                    int v = A.slot_var[x];
+                    rdest.push_back(v < ni ? o_bi + v : o_bbv + (v - ni)); ra.push_back((int32_t)(A.slot_base + x)); rb.push_back(-1);
+                }
+            }
+        }
+
+        // ---- ordering of the interior --------------------------------------------------
+        A.epos.assign(ni, -1); A.order.assign(ni, -1);
+        int ep = 0;
+        A.first_front = (int)hp.fronts.size();
+        A.front_of_pos.assign(ni, -1);
+        if (!hp.owned[a]) {
+            for (int v = 0; v < ni; ++v) { A.epos[v] = v; A.order[v] = v; }
+            ep = ni;
+        } else {
+        std::vector<std::vector<int>> nodes;   // each: interior bus indices, in elimination order
+        if (opt.dense || ni <= PMAX) {
+            std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
+            if (nib) nodes.push_back(all);
+        } else {
+            NDGraph g;
+            // bus graph from the G_ii pattern
+            std::vector<int64_t> edges;
+            for (int u = 0; u < ni; ++u)
+                for (int p = hp.ii_ptr[a][u]; p < hp.ii_ptr[a][u + 1]; ++p) {
+                    int bu = A.var_bus[u], bv = A.var_bus[hp.ii_idx[a][p]];
+                    if (bu != bv) edges.push_back((int64_t)bu * nib + bv);
+                }
+            std::sort(edges.begin(), edges.end()); edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+            g.xadj.assign(nib + 1, 0); g.adj.resize(edges.size());
+            for (size_t i = 0; i < edges.size(); ++i) { g.xadj[edges[i] / nib + 1]++; g.adj[i] = (int)(edges[i] % nib); }
+            for (int i = 0; i < nib; ++i) g.xadj[i + 1] += g.xadj[i];
+            g.stamp.assign(nib, 0); g.level.assign(nib, 0);
+            std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
+            nd_recurse(g, all, std::max(1, opt.leaf_buses), nodes);
+        }
+        // nodes -> fronts of at most PMAX pivots
+        for (auto& node : nodes) {
+            std::vector<int> vars;
+            for (int b : node) { if (A.th_var[b] >= 0) vars.push_back(A.th_var[b]); vars.push_back(A.vm_var[b]); }
+            int nv = (int)vars.size();
+            int pieces = (nv + PMAX - 1) / PMAX;
+            for (int q = 0; q < pieces; ++q) {
+                int lo = (int)((int64_t)nv * q / pieces), hi = (int)((int64_t)nv * (q + 1) / pieces);
+                Front f; f.area = a; f.kind = 0; f.p = hi - lo;
+                for (int i = lo; i < hi; ++i) {
+                    A.epos[vars[i]] = ep; A.order[ep] = vars[i];
+                    A.front_of_pos[ep] = (int)hp.fronts.size();
+                    f.rows.push_back(hp.area_base[a] + ep);
+                    hp.perm_orig[hp.area_base[a] + ep] = vars[i];
+                    ++ep;
+                }
+                hp.fronts.push_back(std::move(f));
+            }
+        }
+        }
+        if (ep != ni) return "ordering did not cover the interior";
+        A.n_fronts = (int)hp.fronts.size() - A.first_front;
+
+        // ---- lower-triangular pattern in position space ------------------------------
+        const int nloc = ni + nb;
+        auto lpos = [&](int v) { return v < ni ? A.epos[v] : v; };
+        std::vector<std::vector<int>> colrows(nloc);
+        if (hp.owned[a]) {
+            for (int u = 0; u < ni; ++u) {
+                for (int p = hp.ii_ptr[a][u]; p < hp.ii_ptr[a][u + 1]; ++p) {
+                    int v = hp.ii_idx[a][p];
+                    if (A.epos[u] >= A.epos[v]) colrows[A.epos[v]].push_back(A.epos[u]);
+                }
+                for (int p = hp.ib_ptr[a][u]; p < hp.ib_ptr[a][u + 1]; ++p) colrows[A.epos[u]].push_back(ni + hp.ib_idx[a][p]);
+            }
+            if (opt.dense) for (int c = 0; c < ni; ++c) { colrows[c].clear(); for (int r = c; r < nloc; ++r) colrows[c].push_back(r); }
+            for (int c = ni; c < nloc; ++c) for (int r = c; r < nloc; ++r) colrows[c].push_back(r);
+            A.col_ptr.assign(nloc + 1, 0);
+            for (int c = 0; c < nloc; ++c) {
+                std::sort(colrows[c].begin(), colrows[c].end());
+                colrows[c].push_back(nloc);   // RHS row
+                A.col_ptr[c + 1] = A.col_ptr[c] + (int)colrows[c].size();
+            }
+            A.col_row.reserve(A.col_ptr[nloc]);
+            for (int c = 0; c < nloc; ++c) A.col_row.insert(A.col_row.end(), colrows[c].begin(), colrows[c].end());
+            A.col_dest.assign(A.col_row.size(), -1);
+        }
+        (void)lpos;
+
+        // ---- update sets + assembly tree of the interior fronts ---------------------
+        std::vector<std::vector<int>> structs(A.n_fronts);   // local positions (>= pivots' end), sorted
+        std::vector<int> mark(nloc, -1);
+        // area root
+        Front root; root.area = a; root.kind = 1; root.p = 0; root.u1 = nb + 1;
+        for (int j = 0; j < nb; ++j) root.rows.push_back(hp.gamma_base + d.sel[d.sel_ptr[a] + j]);
+        const int root_id = A.first_front + A.n_fronts;
+        A.root = root_id;
+        std::vector<std::vector<int>> kids(A.n_fronts + 1);
+        int e0 = 0;
+        for (int fi = 0; fi < A.n_fronts; ++fi) {
+            Front& f = hp.fronts[A.first_front + fi];
+            const int e1 = e0 + f.p;
+            std::vector<int>& st = structs[fi];
+            for (int c = e0; c < e1; ++c)
+                for (int q = A.col_ptr[c]; q < A.col_ptr[c + 1] - 1; ++q) {
+                    int r = A.col_row[q];
+                    if (r >= e1 && mark[r] != fi) { mark[r] = fi; st.push_back(r); }
+                }
+            for (int ch : kids[fi])
+                for (int r : structs[ch]) if (r >= e1 && mark[r] != fi) { mark[r] = fi; st.push_back(r); }
+            std::sort(st.begin(), st.end());
+            f.u1 = (int)st.size() + 1;
+            for (int r : st) f.rows.push_back(r < ni ? hp.area_base[a] + r : hp.gamma_base + d.sel[d.sel_ptr[a] + (r - ni)]);
+            int par = A.n_fronts;   // area root by default
+            if (!st.empty() && st[0] < ni) par = A.front_of_pos[st[0]] - A.first_front;
+            kids[par].push_back(fi);
+            f.parent = A.first_front + par;
+            e0 = e1;
+        }
+        if (hp.owned[a]) {
+            // rel maps child -> parent
+            e0 = 0;
+            std::vector<int> e_start(A.n_fronts + 1, 0);
+            for (int fi = 0; fi < A.n_fronts; ++fi) e_start[fi + 1] = e_start[fi] + hp.fronts[A.first_front + fi].p;
+            for (int fi = 0; fi < A.n_fronts; ++fi) {
+                Front& f = hp.fronts[A.first_front + fi];
+                int par = f.parent - A.first_front;
+                const std::vector<int>& st = structs[fi];
+                f.rel.resize(f.u1);
+                if (par == A.n_fronts) {
+                    for (size_t i = 0; i < st.size(); ++i) f.rel[i] = st[i] - ni;
+                    f.rel[f.u1 - 1] = nb;
+                } else {
+                    Front& P = hp.fronts[A.first_front + par];
+                    const std::vector<int>& ps = structs[par];
+                    int pe0 = e_start[par], pe1 = e_start[par + 1];
+                    for (size_t i = 0; i < st.size(); ++i) {
+                        int r = st[i];
+                        if (r < pe1) { if (r < pe0) return "internal: child row precedes parent pivots"; f.rel[i] = r - pe0; }
+                        else {
+                            auto it = std::lower_bound(ps.begin(), ps.end(), r);
+                            if (it == ps.end() || *it != r) return "internal: update row missing in parent front";
+                            f.rel[i] = P.p + (int)(it - ps.begin());
+                        }
+                    }
+                    f.rel[f.u1 - 1] = P.p + P.u1 - 1;
+                }
+            }
+            for (int fi = 0; fi < A.n_fronts; ++fi) {
+                Front& f = hp.fronts[A.first_front + fi];
+                for (int ch : kids[fi]) f.children.push_back(A.first_front + ch);
+            }
+            for (int ch : kids[A.n_fronts]) root.children.push_back(A.first_front + ch);
+        }
+        hp.fronts.push_back(std::move(root));
+        hp.area_root.push_back(root_id);
+
+        // stash structs for the entry layout below
+        if (hp.owned[a]) {
+            // ---- front-major, region-sorted layout of the original entries -------------
+            std::vector<int> e_start(A.n_fronts + 1, 0);
+            for (int fi = 0; fi < A.n_fronts; ++fi) e_start[fi + 1] = e_start[fi] + hp.fronts[A.first_front + fi].p;
+            for (int fi = 0; fi <= A.n_fronts; ++fi) {
+                Front& f = hp.fronts[A.first_front + fi];
+                choose_chunks(f);
+                const bool is_root = fi == A.n_fronts;
+                const int c0 = is_root ? ni : e_start[fi], c1 = is_root ? nloc : e_start[fi + 1];
+                const std::vector<int>* st = is_root ? nullptr : &structs[fi];
+                auto local_row = [&](int r) -> int {
+                    if (r == nloc) return f.p + f.u1 - 1;
+                    if (is_root) return r - ni;
+                    if (r < c1) return r - c0;
+                    return f.p + (int)(std::lower_bound(st->begin(), st->end(), r) - st->begin());
+                };
+                auto chunk_of = [&](int lr) { return lr < f.p ? 0 : 1 + (lr - f.p) / f.T; };
+                struct Ent { int reg; uint32_t pos; int q; };
+                std::vector<Ent> ents;
+                for (int c = c0; c < c1; ++c)
+                    for (int q = A.col_ptr[c]; q < A.col_ptr[c + 1]; ++q) {
+                        int lr = local_row(A.col_row[q]), lc = is_root ? c - ni : c - c0;
+                        int rc = chunk_of(lr), cc = is_root ? 1 + lc / f.T : 0;
+                        if (is_root && rc < cc) return "internal: upper entry in root";
+                        ents.push_back({rc * (rc + 1) / 2 + cc, ((uint32_t)lr << 16) | (uint32_t)lc, q});
+                    }
+                std::stable_sort(ents.begin(), ents.end(), [](const Ent& x, const Ent& y) { return x.reg < y.reg; });
+                const int nreg = (f.nch + 1) * (f.nch + 2) / 2;
+                hp.front_reg_off.resize(hp.fronts.size(), 0);
+                hp.front_reg_off[A.first_front + fi] = (int32_t)hp.reg_ptr.size();
+                f.gval_off = hp.n_gval; f.n_orig = (int)ents.size();
+                std::vector<int32_t> rp(nreg + 1, 0);
+                for (auto& e : ents) rp[e.reg + 1]++;
+                for (int i = 0; i < nreg; ++i) rp[i + 1] += rp[i];
+                hp.reg_ptr.insert(hp.reg_ptr.end(), rp.begin(), rp.end());
+                for (size_t i = 0; i < ents.size(); ++i) { hp.orig_pos.push_back(ents[i].pos); A.col_dest[ents[i].q] = hp.n_gval + (int64_t)i; }
+                hp.n_gval += (int64_t)ents.size();
+            }
+        } else {
+            choose_chunks(hp.fronts[root_id]);
+        }
+        for (int b : touched) { loc_va[b] = -1; loc_vm[b] = -1; }
+    }
+    hp.n_slots = slot_cursor;
+
+    // ---- coordinator fronts: boundary assembly root + dense factorisation chain -----
+    const int first_coord = (int)hp.fronts.size();
+    if (ng > 0) {
+        for (int a = 0; a < K; ++a) {
+            Front& r = hp.fronts[hp.area_root[a]];
+            r.parent = first_coord;
+            r.rel.resize(r.u1);
+            for (int j = 0; j < as[a].nb; ++j) r.rel[j] = d.sel[d.sel_ptr[a] + j];
+            r.rel[r.u1 - 1] = ng;
+        }
+        if (coordinator) {
+            Front g; g.kind = 2; g.p = 0; g.u1 = ng + 1;
+            for (int s = 0; s < ng; ++s) g.rows.push_back(hp.gamma_base + s);
+            for (int a = 0; a < K; ++a) g.children.push_back(hp.area_root[a]);
+            g.parent = first_coord + 1;
+            g.rel.resize(g.u1); std::iota(g.rel.begin(), g.rel.end(), 0);
+            choose_chunks(g);
+            hp.gamma_root = first_coord;
+            hp.fronts.push_back(std::move(g));
+            int nchain = (ng + PMAX - 1) / PMAX;
+            for (int k = 0; k < nchain; ++k) {
+                int lo = (int)((int64_t)ng * k / nchain), hi = (int)((int64_t)ng * (k + 1) / nchain);
+                Front c; c.kind = 3; c.p = hi - lo; c.u1 = ng - hi + 1;
+                for (int s = lo; s < ng; ++s) c.rows.push_back(hp.gamma_base + s);
+                c.children.push_back((int)hp.fronts.size() - 1);
+                c.parent = k + 1 < nchain ? (int)hp.fronts.size() + 1 : -1;
+                c.rel.resize(c.u1); std::iota(c.rel.begin(), c.rel.end(), 0);
+                choose_chunks(c);
+                hp.fronts.push_back(std::move(c));
+            }
+        } else {
+            for (int a = 0; a < K; ++a) hp.fronts[hp.area_root[a]].parent = -1;
+        }
+    }
+    for (int s = 0; s < ng; ++s) hp.perm_orig[hp.gamma_base + s] = s;
+    hp.front_reg_off.resize(hp.fronts.size(), 0);
+    for (size_t f = 0; f < hp.fronts.size(); ++f)
+        if (hp.fronts[f].kind >= 2) {   // no original entries: an all-empty region table
+            hp.front_reg_off[f] = (int32_t)hp.reg_ptr.size();
+            int nreg = (hp.fronts[f].nch + 1) * (hp.fronts[f].nch + 2) / 2;
+            hp.reg_ptr.insert(hp.reg_ptr.end(), nreg + 1, 0);
+        }
+
+    // ---- storage offsets ----------------------------------------------------------------
+    // update matrices: area roots first, contiguous in area order (the exchange buffer)
+    hp.xchg_off = 0; hp.xchg_area_off.assign(K + 1, 0);
+    int64_t ucur = 0;
+    for (int a = 0; a < K; ++a) {
+        Front& r = hp.fronts[hp.area_root[a]];
+        r.u_off = ucur; hp.xchg_area_off[a] = ucur;
+        ucur += (int64_t)r.u1 * (r.u1 + 1) / 2;
+    }
+    hp.xchg_area_off[K] = ucur; hp.xchg_len = ucur;
+    int64_t lcur = 0;
+    for (auto& f : hp.fronts) {
+        if (f.kind != 1) { f.u_off = ucur; ucur += (int64_t)f.u1 * (f.u1 + 1) / 2; }
+        f.l_off = lcur; lcur += (int64_t)(f.p + f.u1) * f.p;
+        hp.max_front = std::max(hp.max_front, f.p + f.u1);
+        double p = f.p, u = f.u1;
+        hp.dense_flops += p * p * p / 3.0 + p * p * u + p * u * u;
+    }
+    hp.n_ubuf = ucur; hp.n_lbuf = lcur;
+
+    // ---- levels + tasks -------------------------------------------------------------------
+    int max_interior = -1;
+    for (auto& f : hp.fronts) if (f.kind == 0) {
+        int lv = 0;
+        for (int c : f.children) lv = std::max(lv, hp.fronts[c].level + 1);
+        f.level = lv; max_interior = std::max(max_interior, lv);
+    }
+    const int root_level = max_interior + 1;
+    int n_levels = root_level + 1;
+    for (auto& f : hp.fronts) {
+        if (f.kind == 1) f.level = root_level;
+        else if (f.kind == 2) { f.level = root_level + 1; n_levels = std::max(n_levels, f.level + 1); }
+    }
+    { int k = 0; for (auto& f : hp.fronts) if (f.kind == 3) { f.level = root_level + 2 + k++; n_levels = std::max(n_levels, f.level + 1); } }
+    hp.fwd_levels.assign(n_levels, {}); hp.level_phase.assign(n_levels, 1);
+    for (size_t fi = 0; fi < hp.fronts.size(); ++fi) {
+        Front& f = hp.fronts[fi];
+        if (f.area >= 0 && !hp.owned[f.area]) continue;
+        for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj});
+        hp.level_phase[f.level] = f.kind <= 1 ? 1 : f.kind;
+    }
+    for (auto& lv : hp.fwd_levels)
+        std::stable_sort(lv.begin(), lv.end(), [&](const Task& x, const Task& y) {
+            const Front& a = hp.fronts[x.front]; const Front& b = hp.fronts[y.front];
+            return (int64_t)a.p * (a.p + a.u1) > (int64_t)b.p * (b.p + b.u1); });
+    for (int lv = n_levels - 1; lv >= 0; --lv) {
+        std::vector<int> fs; int phase = 4;
+        for (size_t fi = 0; fi < hp.fronts.size(); ++fi) {
+            const Front& f = hp.fronts[fi];
+            if (f.level != lv || f.p == 0) continue;
+            if (f.area >= 0 && !hp.owned[f.area]) continue;
+            fs.push_back((int)fi); if (f.kind == 3) phase = 3;
+        }
+        if (!fs.empty()) { hp.bwd_levels.push_back(fs); hp.bwd_phase.push_back(phase); }
+    }
+
+    // ---- solver-layout accumulation program ---------------------------------------------
+    {
+        std::vector<int64_t> dest; std::vector<int32_t> pa, pb;
+        for (int a = 0; a < K; ++a) {
+            if (!hp.owned[a]) continue;
+            AreaSym& A = as[a];
+            const int ni = A.ni, nloc = A.ni + A.nb;
+            auto lp = [&](int v) { return v < ni ? A.epos[v] : v; };
+            auto find = [&](int c, int r) -> int64_t {
+                auto b = A.col_row.begin() + A.col_ptr[c], e = A.col_row.begin() + A.col_ptr[c + 1];
+                auto it = std::lower_bound(b, e, r);
+                return (it == e || *it != r) ? -1 : A.col_dest[it - A.col_row.begin()];
+            };
+            for (size_t k = 0; k < A.rows.size(); ++k) {
+                int s0 = A.slot_ptr[k], s1 = A.slot_ptr[k + 1];
+                for (int x = s0; x < s1; ++x) {
+                    int ra_ = lp(A.slot_var[x]);
+                    for (int y = s0; y < s1; ++y) {
+                        int cb = lp(A.slot_var[y]);
+                        if (ra_ < cb) continue;
+                        int64_t dd = find(cb, ra_);
+                        if (dd < 0) return "internal: pair without a destination";
+                        dest.push_back(dd); pa.push_back((int32_t)(A.slot_base + x)); pb.push_back((int32_t)(A.slot_base + y));
+                    }
+                }
+                for (int x = s0; x < s1; ++x) {
+                    int64_t dd = find(lp(A.slot_var[x]), nloc);
+                    dest.push_back(dd); pa.push_back((int32_t)(A.slot_base + x)); pb.push_back(-1);
+                }
+            }
+        }
+        hp.n_pairs = (int64_t)dest.size();
+        // stable counting sort by destination keeps ascending-row order per slot
+        hp.acc_ptr.assign(hp.n_gval + 1, 0);
+        for (int64_t dd : dest) hp.acc_ptr[dd + 1]++;
+        for (int64_t i = 0; i < hp.n_gval; ++i) hp.acc_ptr[i + 1] += hp.acc_ptr[i];
+        hp.acc_a.resize(dest.size()); hp.acc_b.resize(dest.size());
+        std::vector<int32_t> cur(hp.acc_ptr.begin(), hp.acc_ptr.end() - 1);
+        for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = pa[i]; hp.acc_b[q] = pb[i]; }
+    }
+    // ---- reference-layout program (component parity) ---------------------------------------
+    {
+        hp.n_ref_vals = hp.ref_off[K];
+        hp.racc_ptr.assign(hp.n_ref_vals + 1, 0);
+        for (int64_t dd : rdest) hp.racc_ptr[dd + 1]++;
+        for (int64_t i = 0; i < hp.n_ref_vals; ++i) hp.racc_ptr[i + 1] += hp.racc_ptr[i];
+        hp.racc_a.resize(rdest.size()); hp.racc_b.resize(rdest.size());
+        std::vector<int32_t> cur(hp.racc_ptr.begin(), hp.racc_ptr.end() - 1);
+        for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = ra[i]; hp.racc_b[q] = rb[i]; }
+    }
+
+    // ---- state update list ----------------------------------------------------------------
+    for (int a = 0; a < K; ++a) {
+        if (!hp.owned[a]) continue;
+        AreaSym& A = as[a];
+        int n_ia = d.ia_ptr[a + 1] - d.ia_ptr[a];
+        for (int v = 0; v < A.ni; ++v) {
+            int bus = v < n_ia ? d.ia_bus[d.ia_ptr[a] + v] : d.im_bus[d.im_ptr[a] + (v - n_ia)];
+            hp.upd_bus.push_back(bus); hp.upd_quant.push_back(v < n_ia ? 0 : 1); hp.upd_pos.push_back(hp.area_base[a] + A.epos[v]);
+        }
+    }
+    for (int s = 0; s < ng; ++s) { hp.upd_bus.push_back(d.gamma_bus[s]); hp.upd_quant.push_back(d.gamma_quant[s]); hp.upd_pos.push_back(hp.gamma_base + s); }
+
+    hp.alg_bytes = 16.0 * m + 32.0 * nbus + 96.0 * d.n_branch + 8.0 * nnz_total + 8.0 * rhs_total;
+    return "";
+}
+
+}  // namespace gse
