@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""bench.py -- GN iterations/s and time-to-converge of the multi-area state estimator.
+
+    python bench.py --gpus N --steps K --warmup W            # B200 arm (this repo's CUDA path)
+    python bench.py --impl reference --gpus N --steps K ...  # the reference algorithm on host cores
+
+A "step" is one full flat-start Gauss-Newton solve (to convergence) of the workload
+BASELINE.json's metric is quoted on: the PEGASE-9241-shaped grid split into 16 areas
+(configs[2]; 91,919 measurement rows, n_Gamma = 716), synthetic measurements.
+
+One JSON line on stdout (rank 0).  `value` = GN iterations per second with inputs resident in
+HBM (device-timed solve loop); `e2e` = the same metric through the public API with HOST
+buffers (measurement values + weights host->device, flat start host->device, estimate
+device->host inside the timed region); `roofline` = the dominant kernel group against the
+measured peaks; `cpu_baseline` = the C oracle port (oracle/) on this box's host cores.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {"pegase2869_k8": "pegase2869", "pegase9241_k16": "pegase9241", "activsg10k_k32": "activsg10k"}
+
+
+def build_workload(name):
+    import paper_2604_23175_b200 as G
+    from paper_2604_23175_b200 import synth
+    shape = WORKLOADS[name]
+    net = synth.shaped_network(shape)
+    ms = G.generate_measurements(net, G.MeasurementConfig(seed=0))
+    part = G.load_partition(net, synth.golden_partition(shape))
+    return net, ms, part
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:6]) if v.lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference(net, ms, part, threads, budget_s=20.0, min_runs=2):
+    """Time the C oracle port (the reference's algorithm) on this host: solves/s, iterations."""
+    from oracle.mase_oracle import Oracle
+    t0 = time.perf_counter()
+    orc = Oracle(net, ms, part.area_of_bus)
+    setup = time.perf_counter() - t0
+    res = orc.solve(threads=threads)        # warm-up
+    times = []
+    while len(times) < min_runs or (sum(times) < budget_s and len(times) < 50):
+        t0 = time.perf_counter()
+        res = orc.solve(threads=threads)
+        times.append(time.perf_counter() - t0)
+    return res, float(np.mean(times)), setup, len(times)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import mase_oracle
+    net, ms, part = build_workload(args.workload)
+    threads = min(mase_oracle.max_threads(), part.k, os.cpu_count() or 1)
+    res, sec, setup, runs = cpu_reference(net, ms, part, threads, budget_s=max(5.0, 2.0 * args.steps))
+    value = res["iterations"] / sec
+    line = {
+        "impl": "reference", "metric": "GN iterations/s (PEGASE-9241-shape MASE, 16 areas)", "value": value,
+        "unit": "GN iterations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "areas": part.k, "n_bus": net.n_bus, "rows": ms.m,
+                   "iterations_per_solve": res["iterations"]},
+        "cpu_baseline": {"value": value, "unit": "GN iterations/s", "cores": threads, "kind": "port",
+                         "sample": f"{runs} full flat-start solves of {args.workload} (C restatement of the reference "
+                                   f"algorithm, oracle/mase_oracle.c; analysis {setup:.2f}s excluded)"},
+        "e2e": {"value": value, "unit": "GN iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "time_to_converge_ms": sec * 1e3, "objective": res["objective"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def dgemm_peak(torch, dev):
+    """Measured FP64 GEMM throughput on this box (MEASURED_PEAKS.json has no FP64 figure)."""
+    n = 4096
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize(dev)
+    best = 1e9
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1))
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def run_gpu(args):
+    import torch
+    import paper_2604_23175_b200 as G
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        from paper_2604_23175_b200.distributed import DistributedEstimator
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    net, ms, part = build_workload(args.workload)
+
+    t0 = time.perf_counter()
+    if world > 1:
+        est = DistributedEstimator(net, ms, part, device=local)
+    else:
+        est = G.MultiAreaEstimator(net, ms, part, device=local)
+    plan_s = time.perf_counter() - t0
+
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def one_step(e2e=False):
+        """One flat-start solve; returns (device seconds, wall seconds, iterations)."""
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        if e2e:
+            est.update_measurements(ms)           # host z, w -> device
+        state, rep = est.estimate()               # flat start h2d, GN loop, state d2h
+        wall = time.perf_counter() - t
+        return est.last_gpu_s, wall, rep
+
+    for _ in range(max(args.warmup, 3)):
+        one_step()
+    barrier()
+    dev_s, e2e_s, iters = [], [], 0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            g, w, rep = one_step()
+            dev_s.append(g)
+            iters += rep.iterations
+        barrier()
+        for _ in range(args.steps):
+            g, w, rep_e = one_step(e2e=True)
+            e2e_s.append(w)
+    barrier()
+    tot_dev, tot_e2e = float(np.sum(dev_s)), float(np.sum(e2e_s))
+    if world > 1:
+        t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_dev, tot_e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    it_per_solve = rep.iterations
+    value = iters / tot_dev
+    e2e_value = it_per_solve * args.steps / tot_e2e
+
+    # ---- per-phase device times (CUDA events on the plan's stream, ungraphed pass) ----------------
+    peaks, peak_src = measured_peaks()
+    roof, phases, stats = None, None, {}
+    if world == 1:
+        prof = G.MultiAreaEstimator(net, ms, part, config=G.SolverConfig(profile_phases=True), device=local)
+        for _ in range(3):
+            prof.estimate()
+        acc = np.zeros(5)
+        reps = 5
+        for _ in range(reps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            _, r = prof.estimate()
+            acc += np.array([r.timings[p] for p in G.solver.PHASES])
+        per_iter = acc / (reps * it_per_solve)           # seconds per GN iteration per phase
+        stats = prof.plan.stats()
+        phases = dict(zip(G.solver.PHASES, (float(x) for x in per_iter)))
+        fp64_peak = dgemm_peak(torch, dev)
+        t_asm = phases["assembly"]
+        t_dense = phases["local_condense"] + phases["boundary_assemble"] + phases["boundary_solve"]
+        hbm = {"kernel": "eval_templates_kernel+accumulate_kernel", "bound": "hbm",
+               "achieved": stats["alg_bytes"] / t_asm / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+               "frac": stats["alg_bytes"] / t_asm / 1e9 / peaks["hbm_gbs"], "traffic": None,
+               "peak_source": f"MEASURED_PEAKS.json ({peak_src})", "bytes_per_launch": stats["alg_bytes"]}
+        dense = {"kernel": "front_task_kernel", "bound": "tensor", "achieved": stats["dense_flops"] / t_dense / 1e12,
+                 "peak": fp64_peak, "unit": "TFLOP/s", "frac": stats["dense_flops"] / t_dense / 1e12 / fp64_peak,
+                 "traffic": None, "peak_source": "cuBLAS FP64 DGEMM 4096^3 measured in this run",
+                 "flops_per_iteration": stats["dense_flops"]}
+        roof = dense if t_dense >= t_asm else hbm
+        roof["other"] = hbm if roof is dense else dense
+        prof.close()
+
+    # ---- CPU baseline: the oracle port, bounded sample ---------------------------------------------
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        res1, sec1, setup1, runs1 = cpu_reference(net, ms, part, 1, budget_s=10.0)
+        cpu = {"value": res1["iterations"] / sec1, "unit": "GN iterations/s", "cores": 1, "kind": "port",
+               "sample": f"{runs1} full flat-start solves of {args.workload}, oracle/mase_oracle.c single thread; "
+                         f"host has {os.cpu_count()} cores; analysis {setup1:.2f}s excluded",
+               "time_to_converge_ms": sec1 * 1e3, "iterations": res1["iterations"],
+               "objective_rel_diff": abs(res1["objective"] - rep.objective) / res1["objective"]}
+
+    m, nb = ms.m, net.n_bus
+    line = {
+        "metric": "GN iterations/s (PEGASE-9241-shape MASE, 16 areas)", "value": value, "unit": "GN iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": tot_dev / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "areas": part.k, "n_bus": nb, "rows": m, "n_gamma": est.n_gamma,
+                   "iterations_per_solve": it_per_solve, "converged": bool(rep.converged),
+                   "l2": "flushed between steps (256 MB write)", "parallelism": f"areas sharded over {world} GPU(s)"},
+        "time_to_converge_ms": {"warm_device": tot_dev / args.steps * 1e3, "warm_e2e": tot_e2e / args.steps * 1e3,
+                                "plan_build_s": plan_s},
+        "objective": rep.objective,
+        "e2e": {"value": e2e_value, "unit": "GN iterations/s", "h2d_bytes_per_step": 16 * m + 16 * nb,
+                "d2h_bytes_per_step": 16 * nb + 16 * it_per_solve},
+        "gpu_launches": int(est.launches_per_solve * args.steps * 2),
+        "clocks": clocks.summary(),
+    }
+    if roof:
+        line["roofline"] = roof
+        line["phase_s_per_iteration"] = phases
+        line["plan"] = {k: stats[k] for k in ("fronts", "levels", "tasks", "max_front", "launches_per_iter")}
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    est.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="pegase9241_k16", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,7 +85,8 @@ typedef struct {
     /* seconds: assembly, local_condense, boundary_assemble, boundary_solve, recovery
      * (solver.py:36), then the whole GN loop */
     double phase_s[5];
-    double loop_s;
+    double loop_s;                 /* host wall clock around the loop                   */
+    double gpu_s;                  /* CUDA-event time on the plan's stream, same region */
 } gse_report;
 
 typedef struct {
@@ -172,6 +173,8 @@ double *gse_status_dev(gse_plan *plan);
  * iteration (SURVEY.md section 8(d) A_min), [10]=dense flops per iteration (fronts),
  * [11]=launches per iteration. */
 int gse_plan_stats(const gse_plan *plan, double *stats, int32_t n);
+/* The CUDA stream (cudaStream_t) every kernel of the plan is launched on. */
+void *gse_stream(gse_plan *plan);
 const char *gse_version(void);
 
 #ifdef __cplusplus

@@ -57,7 +57,8 @@ class Config(C.Structure):
 
 class Report(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("objective", C.c_double),
-                ("delta_inf", C.c_double * 64), ("phase_s", C.c_double * 5), ("loop_s", C.c_double)]
+                ("delta_inf", C.c_double * 64), ("phase_s", C.c_double * 5), ("loop_s", C.c_double),
+                ("gpu_s", C.c_double)]
 
 
 class Error(C.Structure):
@@ -120,6 +121,8 @@ def lib():
     L.gse_status_dev.argtypes = [vp]
     L.gse_status_dev.restype = vp
     L.gse_plan_stats.argtypes = [vp, f64p, C.c_int32]
+    L.gse_stream.argtypes = [vp]
+    L.gse_stream.restype = vp
     _LIB = L
     return L
 
@@ -131,7 +134,7 @@ EXPORTED = [
     "gse_area_dims", "gse_area_pattern", "gse_area_blocks", "gse_area_schur", "gse_area_delta",
     "gse_boundary_system", "gse_set_boundary_delta", "gse_exchange_buffer_dev",
     "gse_exchange_offsets", "gse_boundary_delta_dev", "gse_status_dev", "gse_plan_stats",
-    "gse_version",
+    "gse_version", "gse_stream",
 ]
 
 

@@ -391,6 +391,7 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
     if (!timed) { int rc = ensure_graph(plan, va, vm); if (rc) return rc; }
     plan->launches_last = 0;
     auto t0 = std::chrono::steady_clock::now();
+    cudaEventRecord(plan->ev[6], plan->stream);
     int status = GSE_OK;
     for (int it = 1; it <= max_it; ++it) {
         if (timed) plan->launches_last += enqueue_iteration(plan, va, vm, true);
@@ -409,7 +410,10 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
         rep->delta_inf[it - 1] = dv;
         if (dv < cfg->convergence_tol) { rep->converged = 1; break; }
     }
+    cudaEventRecord(plan->ev[7], plan->stream);
+    cudaEventSynchronize(plan->ev[7]);
     rep->loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    { float ms = 0; cudaEventElapsedTime(&ms, plan->ev[6], plan->ev[7]); rep->gpu_s = ms * 1e-3; }
     if (status != GSE_OK) return status;
     return gse_objective(plan, va, vm, &rep->objective);
 }
@@ -527,6 +531,8 @@ int gse_exchange_offsets(const gse_plan* plan, int64_t* off) {
 }
 double* gse_boundary_delta_dev(gse_plan* plan) { return plan->xsol.ptr + plan->hp.gamma_base; }
 double* gse_status_dev(gse_plan* plan) { return plan->status.ptr; }
+
+void* gse_stream(gse_plan* plan) { return (void*)plan->stream; }
 
 int gse_plan_stats(const gse_plan* plan, double* s, int32_t n) {
     const HostProgram& hp = plan->hp;

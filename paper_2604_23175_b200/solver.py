@@ -1,0 +1,250 @@
+"""WLS Gauss-Newton solvers on the device.
+
+API mirror of the reference's ``gridse.solver`` (reference
+``pkg/src/gridse/solver.py:36-346``): ``SolverConfig``, ``SolveReport``,
+``BoundarySystem``, ``SolverError``, ``objective``, ``assemble_boundary``,
+``solve_multiarea``, ``solve_centralized`` keep their signatures, defaults,
+result fields and error texts; the work happens in ``libgridse_b200.so``.
+
+``MultiAreaEstimator`` is the warm path the reference lacks: the plan
+(templates, slot map, ordering, fronts, CUDA graph) is built once and reused
+across solves -- new measurement values or masks are weight / value refreshes
+(reference ``PAPER.md:203,226``: "template indices, mapping arrays, working
+buffers allocated once").  PyTorch only owns the device state vectors.
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .linalg import NotPositiveDefiniteError
+from .measurement import MeasurementSet, StateVector
+from .partition import build_variable_maps, partition_network
+
+PHASES = ("assembly", "local_condense", "boundary_assemble", "boundary_solve", "recovery")
+
+
+class SolverError(RuntimeError):
+    pass
+
+
+@dataclass
+class SolverConfig:
+    max_outer_iterations: int = 10
+    inner_gn_steps: int = 1
+    convergence_tol: float = 1e-6
+    deterministic: bool = True      # the device path is always bit-stable; kept for API parity
+    backend: str = "sparse"         # "dense": chain of dense fronts per area instead of nested dissection
+    dense_threshold: int = 64       # kept for API parity (fronts are dense blocks at every size)
+    iterative_refinement: bool = False
+    profile_phases: bool = False    # extension: fill per-phase timings from CUDA events (no graph)
+
+    def __post_init__(self):
+        if self.max_outer_iterations < 1:
+            raise ValueError("max_outer_iterations must be >= 1")
+        if self.convergence_tol <= 0:
+            raise ValueError("convergence_tol must be positive")
+        if self.backend not in ("dense", "sparse"):
+            raise ValueError(f"unknown backend {self.backend!r}")
+        if self.inner_gn_steps != 1:
+            raise NotImplementedError(
+                "inner_gn_steps > 1 is not implemented on the device path yet "
+                "(SURVEY.md section 8 row f2)")
+
+    @property
+    def effective_dense_threshold(self):
+        return 10**9 if self.backend == "dense" else self.dense_threshold
+
+
+@dataclass
+class SolveReport:
+    method: str
+    iterations: int
+    converged: bool
+    objective: float
+    weighted_residual_norm: float
+    n_gamma: int
+    timings: dict
+
+    def to_dict(self):
+        return {
+            "method": self.method, "iterations": self.iterations, "converged": self.converged,
+            "objective": self.objective, "weighted_residual_norm": self.weighted_residual_norm,
+            "n_gamma": self.n_gamma, "timings": dict(self.timings),
+        }
+
+    def to_json(self):
+        return json.dumps(self.to_dict(), indent=1)
+
+
+@dataclass
+class BoundarySystem:
+    s_gamma: np.ndarray
+    b_gamma: np.ndarray
+    delta_x_gamma: np.ndarray = None
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise _native.NoDeviceError(
+            _native.GSE_E_NO_DEVICE, -1, -1,
+            "no CUDA device visible: gridse-b200 has no CPU fallback")
+    return torch
+
+
+class MultiAreaEstimator:
+    """Plan once, estimate many times (device-resident Gauss-Newton loop)."""
+
+    def __init__(self, net, ms: MeasurementSet, part, maps=None, config: SolverConfig = None,
+                 device=0, method="multiarea", rank=0, world=1, area_rank=None):
+        self.cfg = config or SolverConfig()
+        self.net, self.part, self.method = net, part, method
+        self.bord, self.maps = maps if maps is not None else build_variable_maps(net, part)
+        t0 = time.perf_counter()
+        torch = _torch()
+        self.torch = torch
+        self.device = torch.device("cuda", device)
+        self.plan = _native.Plan(net, ms, part, self.bord, self.maps, device=device,
+                                 dense=self.cfg.backend == "dense", rank=rank, world=world,
+                                 area_rank=area_rank)
+        self.ms = ms
+        self.n_gamma = self.bord.n_gamma
+        self._flat = np.stack([StateVector.flat_start(net).va, np.ones(net.n_bus)])
+        self._host = torch.empty((2, net.n_bus), dtype=torch.float64).pin_memory()
+        self._state = torch.empty((2, net.n_bus), dtype=torch.float64, device=self.device)
+        self.setup_s = time.perf_counter() - t0
+
+    # -- inputs ----------------------------------------------------------------------
+    def update_measurements(self, ms: MeasurementSet):
+        """New values / masks on the same rows: refresh z and w, no re-analysis."""
+        if ms.m != self.ms.m or not (np.array_equal(ms.mtype, self.ms.mtype)
+                                     and np.array_equal(ms.target, self.ms.target)):
+            raise ValueError("measurement rows differ from the analysed template set")
+        self.plan.set_measurements(ms.z)
+        self.plan.set_weights(ms.weight)
+        self.ms = ms
+
+    def _ptrs(self):
+        return self._state[0].data_ptr(), self._state[1].data_ptr()
+
+    def _load_flat_start(self):
+        self._host.copy_(self.torch.from_numpy(self._flat))
+        self._state.copy_(self._host, non_blocking=True)
+
+    def _read_state(self):
+        self._host.copy_(self._state)
+        arr = self._host.numpy()
+        return StateVector(va=arr[0].copy(), vm=arr[1].copy())
+
+    def _raise(self, exc):
+        if exc.code == _native.GSE_E_NOT_SPD_AREA:
+            ctx = f"area {exc.area} interior block"
+            inner = NotPositiveDefiniteError(exc.pivot, ctx)
+            if self.method == "centralized":
+                raise SolverError(
+                    f"gain matrix {inner}: system unobservable or ill-conditioned") from inner
+            raise SolverError(f"{inner}; area {exc.area} is likely locally unobservable") from inner
+        if exc.code == _native.GSE_E_NOT_SPD_BOUNDARY:
+            inner = NotPositiveDefiniteError(exc.pivot, "boundary system")
+            bus, quant = self.bord.entries[exc.pivot]
+            raise SolverError(
+                f"boundary system not positive definite at pivot {exc.pivot} "
+                f"(bus {self.net.buses[bus].id}, {quant})") from inner
+        raise exc
+
+    # -- the solve -----------------------------------------------------------------------
+    def estimate(self, on_iteration=None, t_start=None):
+        """Flat-start GN solve; returns (StateVector, SolveReport)."""
+        cfg = self.cfg
+        t_start = time.perf_counter() if t_start is None else t_start
+        timings = {p: 0.0 for p in PHASES}
+        self._load_flat_start()
+        va_ptr, vm_ptr = self._ptrs()
+        self.torch.cuda.current_stream(self.device).synchronize()
+        try:
+            if on_iteration is None:
+                rep = self.plan.solve(va_ptr, vm_ptr, cfg.max_outer_iterations,
+                                      cfg.convergence_tol, cfg.profile_phases)
+                iterations, converged, j = rep.iterations, bool(rep.converged), rep.objective
+                self.last_deltas = [rep.delta_inf[i] for i in range(iterations)]
+                self.last_loop_s, self.last_gpu_s = rep.loop_s, rep.gpu_s
+                self.launches_per_solve = int(self.plan.stats()["launches_last"])
+                if cfg.profile_phases:
+                    for p, v in zip(PHASES, rep.phase_s):
+                        timings[p] = float(v)
+            else:
+                iterations, converged = 0, False
+                self.last_deltas = []
+                t0 = time.perf_counter()
+                for it in range(1, cfg.max_outer_iterations + 1):
+                    delta = self.plan.iterate(va_ptr, vm_ptr)
+                    iterations = it
+                    self.last_deltas.append(delta)
+                    on_iteration(it, self._read_state(), delta)
+                    if delta < cfg.convergence_tol:
+                        converged = True
+                        break
+                self.last_loop_s = time.perf_counter() - t0
+                j = self.plan.objective(va_ptr, vm_ptr)
+        except _native.NativeError as exc:
+            self._raise(exc)
+        state = self._read_state()
+        timings["total"] = time.perf_counter() - t_start
+        report = SolveReport(
+            method=self.method, iterations=iterations, converged=converged, objective=float(j),
+            weighted_residual_norm=float(np.sqrt(j)), n_gamma=self.n_gamma if self.method == "multiarea" else 0,
+            timings=timings)
+        return state, report
+
+    def objective(self, state: StateVector) -> float:
+        self._host.copy_(self.torch.from_numpy(np.stack([state.va, state.vm])))
+        self._state.copy_(self._host)
+        return self.plan.objective(*self._ptrs())
+
+    def close(self):
+        self.plan.close()
+
+
+def objective(ms: MeasurementSet, state: StateVector) -> float:
+    """WLS objective sum w (z - h(x))^2 on the device (reference solver.py:100-103)."""
+    net = ms.net
+    part = partition_network(net, 1)
+    est = MultiAreaEstimator(net, ms, part)
+    try:
+        return est.objective(state)
+    finally:
+        est.close()
+
+
+def solve_multiarea(net, ms: MeasurementSet, part, maps=None, config: SolverConfig = None,
+                    on_iteration=None):
+    """Boundary-condensed multi-area WLS-GN; returns (estimate, report).
+
+    Same contract as the reference (solver.py:204-346).  Setup (plan build) is
+    inside ``timings['total']`` as it is there; use ``MultiAreaEstimator`` to
+    amortise it.
+    """
+    t_start = time.perf_counter()
+    est = MultiAreaEstimator(net, ms, part, maps=maps, config=config)
+    try:
+        return est.estimate(on_iteration=on_iteration, t_start=t_start)
+    finally:
+        est.close()
+
+
+def solve_centralized(net, ms: MeasurementSet, config: SolverConfig = None, on_iteration=None):
+    """Single-area GN on the device: the k = 1 path of the same plan (one area,
+    empty boundary), i.e. the paper's "centralized GPU" baseline."""
+    t_start = time.perf_counter()
+    est = MultiAreaEstimator(net, ms, partition_network(net, 1), config=config,
+                             method="centralized")
+    try:
+        return est.estimate(on_iteration=on_iteration, t_start=t_start)
+    finally:
+        est.close()
