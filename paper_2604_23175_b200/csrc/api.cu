@@ -308,7 +308,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 ++L.count;
             }
             if (L.count) {
-                if (L.smem > 227 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
+                if (L.smem > 226 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
                 plan->fwd.push_back(L);
             }
         }

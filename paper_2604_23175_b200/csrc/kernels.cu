@@ -504,7 +504,7 @@ void launch_objective(const EvalProg& ep, const int32_t* m_type, const int32_t* 
 }
 
 cudaError_t configure_kernels() {
-    const int maxsm = 227 * 1024;
+    const int maxsm = 226 * 1024;   // static + dynamic must stay within the 227 KB opt-in limit
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(front_task_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
     if ((e = cudaFuncSetAttribute(front_task_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
