@@ -37,7 +37,7 @@ struct DevBuf {
 };
 
 struct LevelLaunch { int pclass; int first, count; size_t smem; int phase; };
-struct BwdLaunch { int first, count, max_u, phase; };
+struct BwdLaunch { int first, count, phase; };
 
 }  // namespace
 
@@ -60,7 +60,9 @@ struct gse_plan {
     DevBuf<double> gval, refval;
     // fronts
     DevBuf<int32_t> f_p, f_u1, f_T, f_nchild, f_child_ptr, f_children, f_rel_off, f_rel, f_reg_off, f_reg_ptr;
-    DevBuf<int32_t> f_rows_off, f_rows;
+    DevBuf<int32_t> f_rows_off, f_rows, f_cb_off, f_cbounds, bcnt;
+    DevBuf<BwdTask> btasks;
+    DevBuf<double> bpart;
     DevBuf<uint32_t> orig_pos;
     DevBuf<int64_t> f_gval_off, f_l_off, f_u_off;
     DevBuf<TaskRec> tasks;
@@ -120,7 +122,8 @@ int enqueue_bwd(gse_plan* plan, int phase) {
     int n = 0;
     for (auto& B : plan->bwd) {
         if (B.phase != phase) continue;
-        launch_backward(plan->ft, plan->bwd_fronts.ptr + B.first, B.count, B.max_u, plan->lbuf.ptr, plan->xsol.ptr, plan->stream);
+        launch_backward(plan->ft, plan->btasks.ptr + B.first, B.count, plan->lbuf.ptr, plan->xsol.ptr, plan->bpart.ptr, plan->bcnt.ptr,
+                        plan->stream);
         ++n;
     }
     return n;
@@ -191,11 +194,12 @@ gse_plan::~gse_plan() {
     DevBuf<int32_t>* ib[] = {&y_ptr, &y_idx, &br_from, &br_to, &m_type, &m_target, &vm_bus, &vm_row, &vm_slot, &fl_branch,
                              &fl_from, &fl_to, &fl_row, &fl_slot, &inj_bus, &inj_rowp, &inj_rowq, &inj_slotp, &inj_slotq,
                              &acc_ptr, &acc_a, &acc_b, &racc_ptr, &racc_a, &racc_b, &f_p, &f_u1, &f_T, &f_nchild,
-                             &f_child_ptr, &f_children, &f_rel_off, &f_rel, &f_reg_off, &f_reg_ptr, &f_rows_off, &f_rows,
+                             &f_child_ptr, &f_children, &f_rel_off, &f_rel, &f_reg_off, &f_reg_ptr, &f_rows_off, &f_rows, &f_cb_off, &f_cbounds, &bcnt,
                              &bwd_fronts, &upd_bus, &upd_quant, &upd_pos};
     for (auto* b : ib) b->release();
     DevBuf<double>* db[] = {&y_g, &y_b, &br_y, &z, &w, &g, &gw, &wrg, &gval, &refval, &lbuf, &ubuf, &xsol, &obj_partial, &status};
     for (auto* b : db) b->release();
+    btasks.release(); bpart.release();
     orig_pos.release(); f_gval_off.release(); f_l_off.release(); f_u_off.release(); tasks.release(); flags.release();
 }
 
@@ -280,6 +284,19 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         frows_off[i] = (int)rows.size(); rows.insert(rows.end(), f.rows.begin(), f.rows.end());
         fg[i] = f.gval_off; fl[i] = f.l_off; fuo[i] = f.u_off;
     }
+    // lower bounds of every child's rel map at the parent's pivot edge and chunk edges
+    std::vector<int32_t> cb_off(children.size(), 0), cbounds;
+    for (size_t i = 0; i < nf; ++i) {
+        const Front& f = hp.fronts[i];
+        for (size_t c = 0; c < f.children.size(); ++c) {
+            const std::vector<int>& rel_c = hp.fronts[f.children[c]].rel;
+            auto lb = [&](int key) { return (int32_t)(std::lower_bound(rel_c.begin(), rel_c.end(), key) - rel_c.begin()); };
+            cb_off[fcp[i] + c] = (int32_t)cbounds.size();
+            cbounds.push_back(lb(f.p));
+            for (int q = 0; q <= f.nch; ++q) cbounds.push_back(lb(f.p + q * std::max(f.T, 1)));
+        }
+    }
+    CU(plan->f_cb_off.upload(cb_off)); CU(plan->f_cbounds.upload(cbounds));
     CU(plan->f_p.upload(fp)); CU(plan->f_u1.upload(fu)); CU(plan->f_T.upload(fT)); CU(plan->f_nchild.upload(fnc));
     CU(plan->f_child_ptr.upload(fcp)); CU(plan->f_children.upload(children)); CU(plan->f_rel_off.upload(frel_off));
     CU(plan->f_rel.upload(rel)); CU(plan->f_reg_off.upload(hp.front_reg_off)); CU(plan->f_reg_ptr.upload(hp.reg_ptr));
@@ -289,6 +306,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     FrontTab& ft = plan->ft;
     ft.p = plan->f_p.ptr; ft.u1 = plan->f_u1.ptr; ft.T = plan->f_T.ptr; ft.nchild = plan->f_nchild.ptr;
     ft.child_ptr = plan->f_child_ptr.ptr; ft.children = plan->f_children.ptr; ft.rel_off = plan->f_rel_off.ptr;
+    ft.cb_off = plan->f_cb_off.ptr; ft.cbounds = plan->f_cbounds.ptr;
     ft.rel = plan->f_rel.ptr; ft.reg_off = plan->f_reg_off.ptr; ft.reg_ptr = plan->f_reg_ptr.ptr;
     ft.orig_pos = plan->orig_pos.ptr; ft.gval_off = plan->f_gval_off.ptr; ft.l_off = plan->f_l_off.ptr;
     ft.u_off = plan->f_u_off.ptr; ft.rows_off = plan->f_rows_off.ptr; ft.rows = plan->f_rows.ptr;
@@ -296,11 +314,11 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     // ---- level launches: tasks grouped by (level, pivot class) ----
     std::vector<TaskRec> trecs;
     for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
-        for (int pclass : {64, 32, 0}) {
+        for (int pclass : {1, 0}) {
             LevelLaunch L{pclass, (int)trecs.size(), 0, 0, hp.level_phase[lv]};
             for (const Task& t : hp.fwd_levels[lv]) {
                 const Front& f = hp.fronts[t.front];
-                const int cls = f.p == 0 ? 0 : f.p <= 32 ? 32 : 64;
+                const int cls = f.p == 0 ? 0 : 1;
                 if (cls != pclass) continue;
                 const int ni = std::min(f.T, f.u1 - t.ci * f.T), nj = std::min(f.T, f.u1 - t.cj * f.T);
                 L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, t.ci == t.cj));
@@ -308,20 +326,27 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 ++L.count;
             }
             if (L.count) {
-                if (L.smem > 226 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
+                if (L.smem > 222 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
                 plan->fwd.push_back(L);
             }
         }
     }
     CU(plan->tasks.upload(trecs));
-    std::vector<int32_t> bfronts;
+    std::vector<BwdTask> btasks;
+    int pbase = 0;
     for (size_t i = 0; i < hp.bwd_levels.size(); ++i) {
-        BwdLaunch B{(int)bfronts.size(), (int)hp.bwd_levels[i].size(), 0, hp.bwd_phase[i]};
-        for (int f : hp.bwd_levels[i]) { B.max_u = std::max(B.max_u, hp.fronts[f].u1); bfronts.push_back(f); }
-        if (B.max_u > 15000) return fail(plan, GSE_E_INVALID, "update set too large for the backward kernel");
+        BwdLaunch B{(int)btasks.size(), 0, hp.bwd_phase[i]};
+        for (int f : hp.bwd_levels[i]) {
+            const int u = hp.fronts[f].u1 - 1;
+            const int ns = std::max(1, (u + 63) / 64);
+            for (int sp = 0; sp < ns; ++sp) btasks.push_back({f, sp, ns, pbase});
+            pbase += ns; B.count += ns;
+        }
         plan->bwd.push_back(B);
     }
-    CU(plan->bwd_fronts.upload(bfronts));
+    CU(plan->btasks.upload(btasks));
+    CU(plan->bpart.alloc((size_t)pbase * 64 + 64));
+    CU(plan->bcnt.alloc(nf + 1));
     CU(plan->upd_bus.upload(hp.upd_bus)); CU(plan->upd_quant.upload(hp.upd_quant)); CU(plan->upd_pos.upload(hp.upd_pos));
     CU(plan->obj_partial.alloc(objective_blocks(d->n_rows) + 1));
     CU(plan->status.alloc(2));

@@ -4,12 +4,7 @@
 //                          residual + analytic partials per template slot   [assembly.py:427-483]
 //  accumulate_kernel       atomic-free, order-preserving gather-reduction of w*g_a*g_b and
 //                          (w*r)*g_a into precomputed destination slots      [assembly.py:486-524]
-//  front_task_kernel<P>    one (front, row-chunk, col-chunk) task of the multifrontal Schur-mode
-//                          factorisation: extend-add assembly, register-resident panel Cholesky,
-//                          FP64 tensor-core (DMMA m8n8k4) trailing / Schur update
-//                                                      [linalg.py:292-332,410-424; solver.py:106-119;
-//                                                       linalg.py:46-61 for the boundary chain]
-//  backward_kernel         per-front back-substitution (top-down)          [linalg.py:366-383,427-434]
+//  (front_task_kernel / backward_kernel: front_kernels.cu)
 //  update_state_kernel     va/vm += dx, stacked infinity norm               [partition.py:59-62,113-116;
 //                                                                            solver.py:328-333]
 //  objective_kernel        J(x) = sum w (z - h(x))^2                        [solver.py:100-103]
@@ -161,255 +156,6 @@ void launch_accumulate(const int32_t* ptr, const int32_t* a, const int32_t* b, c
 }
 
 // ---------------------------------------------------------------------------------------------
-// Front tasks
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ int lower_bound_dev(const int32_t* __restrict__ a, int n, int key) {
-    int lo = 0, hi = n;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if (a[mid] < key) lo = mid + 1; else hi = mid; }
-    return lo;
-}
-
-__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
-}
-
-// child update block rows [r0,r1) x cols [c0,c1) (lower part only) -> dst[(rel[i]-rs)*ld + rel[j]-cs]
-__device__ __forceinline__ void add_child_block(const double* __restrict__ U, const int32_t* __restrict__ rel,
-                                                int r0, int r1, int c0, int c1, double* dst, int ld,
-                                                int rs, int cs, int tid, int nth) {
-    const int w = c1 - c0, h = r1 - r0;
-    if (w <= 0 || h <= 0) return;
-    for (int t = tid; t < w * h; t += nth) {
-        const int i = r0 + t / w, j = c0 + t % w;
-        if (j <= i) dst[(rel[i] - rs) * ld + (rel[j] - cs)] += U[(size_t)i * (i + 1) / 2 + j];
-    }
-}
-
-template <int P>
-__global__ void __launch_bounds__(kFrontThreads, P == 64 ? 1 : 2)
-front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* __restrict__ gval,
-                  double* __restrict__ lbuf, double* __restrict__ ubuf, unsigned long long* err) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ int sb[8];
-    const TaskRec tk = tasks[blockIdx.x];
-    const int f = tk.front, ci = tk.ci, cj = tk.cj;
-    const int p = P ? ft.p[f] : 0;
-    const int u1 = ft.u1[f], T = ft.T[f];
-    const int i0 = ci * T, ni = min(T, u1 - i0), j0 = cj * T, nj = min(T, u1 - j0);
-    const bool diag = ci == cj;
-    const int ld = pad_ld(p);
-    const int rp = p ? round8(p) : 0, ri = p ? round8(ni) : 0, rj = (p && !diag) ? round8(nj) : 0;
-    const int ldt = round8(nj) | 1;
-    double* pan = sm;
-    double* tile = sm + (size_t)(rp + ri + rj) * ld;
-    const int tid = threadIdx.x, nth = blockDim.x;
-
-    {
-        const int total = (rp + ri + rj) * ld + round8(ni) * ldt;
-        for (int t = tid; t < total; t += nth) sm[t] = 0.0;
-    }
-    __syncthreads();
-
-    // ---- original entries (written by accumulate_kernel into gval) --------------------------
-    {
-        const int32_t* rptr = ft.reg_ptr + ft.reg_off[f];
-        const int64_t goff = ft.gval_off[f];
-        const uint32_t* opos = ft.orig_pos + goff;
-        const double* gv = gval + goff;
-        if (p) {
-            for (int e = rptr[0] + tid; e < rptr[1]; e += nth) {       // region (0,0): pivot block
-                const uint32_t q = opos[e];
-                pan[(q >> 16) * ld + (q & 0xffffu)] = gv[e];
-            }
-            const int ridI = (ci + 1) * (ci + 2) / 2;
-            for (int e = rptr[ridI] + tid; e < rptr[ridI + 1]; e += nth) {
-                const uint32_t q = opos[e];
-                pan[(rp + (int)(q >> 16) - p - i0) * ld + (q & 0xffffu)] = gv[e];
-            }
-            if (!diag) {
-                const int ridJ = (cj + 1) * (cj + 2) / 2;
-                for (int e = rptr[ridJ] + tid; e < rptr[ridJ + 1]; e += nth) {
-                    const uint32_t q = opos[e];
-                    pan[(rp + ri + (int)(q >> 16) - p - j0) * ld + (q & 0xffffu)] = gv[e];
-                }
-            }
-        }
-        const int ridT = (ci + 1) * (ci + 2) / 2 + cj + 1;
-        for (int e = rptr[ridT] + tid; e < rptr[ridT + 1]; e += nth) {
-            const uint32_t q = opos[e];
-            tile[((int)(q >> 16) - p - i0) * ldt + ((int)(q & 0xffffu) - p - j0)] = gv[e];
-        }
-    }
-    __syncthreads();
-
-    // ---- extend-add of the children's update matrices, fixed child order --------------------
-    {
-        const int nchild = ft.nchild[f], cptr = ft.child_ptr[f];
-        for (int c = 0; c < nchild; ++c) {
-            const int ch = ft.children[cptr + c];
-            const int cu1 = ft.u1[ch];
-            const int32_t* rel = ft.rel + ft.rel_off[ch];
-            const double* U = ubuf + ft.u_off[ch];
-            if (tid < 5) {
-                const int key = tid == 0 ? p : tid == 1 ? p + i0 : tid == 2 ? p + i0 + ni : tid == 3 ? p + j0 : p + j0 + nj;
-                sb[tid] = lower_bound_dev(rel, cu1, key);
-            }
-            __syncthreads();
-            const int eP = sb[0], bI = sb[1], eI = sb[2], bJ = sb[3], eJ = sb[4];
-            if (p) {
-                add_child_block(U, rel, 0, eP, 0, eP, pan, ld, 0, 0, tid, nth);
-                add_child_block(U, rel, bI, eI, 0, eP, pan + (size_t)rp * ld, ld, p + i0, 0, tid, nth);
-                if (!diag) add_child_block(U, rel, bJ, eJ, 0, eP, pan + (size_t)(rp + ri) * ld, ld, p + j0, 0, tid, nth);
-            }
-            add_child_block(U, rel, bI, eI, bJ, eJ, tile, ldt, p + i0, p + j0, tid, nth);
-            __syncthreads();
-        }
-    }
-
-    // ---- panel Cholesky: one thread per row, row in registers, one barrier per pivot --------
-    if (P && p) {
-        const int R = p + ni + (diag ? 0 : nj);
-        const bool active = tid < R;
-        const int prow = tid < p ? tid : tid < p + ni ? rp + (tid - p) : rp + ri + (tid - p - ni);
-        double* myrow = pan + (size_t)(active ? prow : 0) * ld;
-        double x[P ? P : 1];
-#pragma unroll
-        for (int k = 0; k < P; ++k) x[k] = (active && k < p) ? myrow[k] : 0.0;
-        double ss = 0.0;
-        if (tid == 0) {
-            const double d = x[0];
-            if (!(d > 0.0)) atomicMin(err, ((unsigned long long)f << 32) | 0ull);
-            x[0] = sqrt(d);
-            myrow[0] = x[0];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            if (k < p) {
-                if (active && tid > k) {
-                    const double* lk = pan + (size_t)k * ld;
-                    double a0 = x[k], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-                    for (int j = 0; j < k; ++j) {
-                        const double l = lk[j];
-                        if ((j & 3) == 0) a0 = fma(-x[j], l, a0);
-                        else if ((j & 3) == 1) a1 = fma(-x[j], l, a1);
-                        else if ((j & 3) == 2) a2 = fma(-x[j], l, a2);
-                        else a3 = fma(-x[j], l, a3);
-                    }
-                    x[k] = ((a0 + a1) + (a2 + a3)) / lk[k];
-                    myrow[k] = x[k];
-                    if (tid < p) {
-                        ss = fma(x[k], x[k], ss);
-                        if (k + 1 < P && tid == k + 1) {
-                            const double d = x[k + 1 < P ? k + 1 : 0] - ss;
-                            if (!(d > 0.0)) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(k + 1));
-                            x[k + 1 < P ? k + 1 : 0] = sqrt(d);
-                            myrow[k + 1] = x[k + 1 < P ? k + 1 : 0];
-                        }
-                    }
-                }
-                __syncthreads();
-            }
-        }
-    }
-
-    // ---- trailing update on the FP64 tensor pipe: U_IJ = F_IJ - L_I L_J^T -------------------
-    {
-        const double* Pi = pan + (size_t)rp * ld;
-        const double* Pj = diag ? Pi : pan + (size_t)(rp + ri) * ld;
-        const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
-        const int nbi = round8(ni) >> 3, nbj = round8(nj) >> 3;
-        const int kend = (p + 3) & ~3;
-        double* U = ubuf + ft.u_off[f];
-        for (int blk = warp; blk < nbi * nbj; blk += nwarps) {
-            const int bi = blk / nbj, bj = blk % nbj;
-            if (diag && bj > bi) continue;
-            double c0 = 0.0, c1 = 0.0;
-            if (p) {
-                const double* ap = Pi + (size_t)(bi * 8 + (lane >> 2)) * ld + (lane & 3);
-                const double* bp = Pj + (size_t)(bj * 8 + (lane >> 2)) * ld + (lane & 3);
-#pragma unroll 4
-                for (int kk = 0; kk < kend; kk += 4) dmma_m8n8k4(c0, c1, ap[kk], bp[kk]);
-            }
-            const int row = bi * 8 + (lane >> 2), col = bj * 8 + 2 * (lane & 3);
-            if (row < ni) {
-                const int I = i0 + row, J = j0 + col;
-                double* urow = U + (size_t)I * (I + 1) / 2;
-                if (col < nj && J <= I) urow[J] = tile[row * ldt + col] - c0;
-                if (col + 1 < nj && J + 1 <= I) urow[J + 1] = tile[row * ldt + col + 1] - c1;
-            }
-        }
-        // ---- factor panel to global (diagonal tasks own their row chunk) ----------------------
-        if (p && diag) {
-            double* L = lbuf + ft.l_off[f];
-            if (ci == 0)
-                for (int t = tid; t < p * p; t += nth) L[t] = pan[(t / p) * ld + (t % p)];
-            double* Li = L + (size_t)(p + i0) * p;
-            for (int t = tid; t < ni * p; t += nth) Li[t] = Pi[(t / p) * ld + (t % p)];
-        }
-    }
-}
-
-void launch_front_tasks(int pclass, const FrontTab& ft, const TaskRec* tasks, int ntasks,
-                        size_t smem_bytes, const double* gval, double* lbuf, double* ubuf,
-                        unsigned long long* err, cudaStream_t s) {
-    if (ntasks == 0) return;
-    if (pclass == 0) front_task_kernel<0><<<ntasks, kFrontThreads, smem_bytes, s>>>(ft, tasks, gval, lbuf, ubuf, err);
-    else if (pclass == 32) front_task_kernel<32><<<ntasks, kFrontThreads, smem_bytes, s>>>(ft, tasks, gval, lbuf, ubuf, err);
-    else front_task_kernel<64><<<ntasks, kFrontThreads, smem_bytes, s>>>(ft, tasks, gval, lbuf, ubuf, err);
-}
-
-// ---------------------------------------------------------------------------------------------
-// Backward substitution: x_P = L11^{-T} (y_P - L21^T x_U), one CTA per front
-// ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) backward_kernel(FrontTab ft, const int32_t* __restrict__ fronts,
-                                                       const double* __restrict__ lbuf, double* __restrict__ xsol) {
-    __shared__ double l11[64 * 65];
-    __shared__ double part[4][64];
-    __shared__ double tv[64];
-    extern __shared__ double xu[];
-    const int f = fronts[blockIdx.x];
-    const int p = ft.p[f], u = ft.u1[f] - 1;
-    const double* L = lbuf + ft.l_off[f];
-    const int32_t* rows = ft.rows + ft.rows_off[f];
-    const int tid = threadIdx.x;
-    for (int i = tid; i < u; i += blockDim.x) xu[i] = xsol[rows[p + i]];
-    for (int t = tid; t < p * p; t += blockDim.x) l11[(t / p) * 65 + (t % p)] = L[t];
-    __syncthreads();
-    const int k = tid & 63, grp = tid >> 6;
-    {
-        const int per = (u + 3) / 4, lo = grp * per, hi = min(u, lo + per);
-        double s0 = 0.0, s1 = 0.0;
-        if (k < p) {
-            const double* col = L + (size_t)p * p + k;
-            int i = lo;
-            for (; i + 1 < hi; i += 2) { s0 = fma(col[(size_t)i * p], xu[i], s0); s1 = fma(col[(size_t)(i + 1) * p], xu[i + 1], s1); }
-            if (i < hi) s0 = fma(col[(size_t)i * p], xu[i], s0);
-        }
-        part[grp][k] = s0 + s1;
-    }
-    __syncthreads();
-    if (tid < p) tv[tid] = L[(size_t)(p + u) * p + tid] - ((part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]));
-    __syncthreads();
-    // warp 0+1 run the triangular solve with L11^T
-    for (int c = p - 1; c >= 0; --c) {
-        if (tid == c) tv[c] = tv[c] / l11[c * 65 + c];
-        __syncthreads();
-        if (tid < c) tv[tid] = fma(-l11[c * 65 + tid], tv[c], tv[tid]);
-        __syncthreads();
-    }
-    if (tid < p) xsol[rows[tid]] = tv[tid];
-}
-
-void launch_backward(const FrontTab& ft, const int32_t* fronts, int nfronts, int max_u, const double* lbuf,
-                     double* xsol, cudaStream_t s) {
-    if (nfronts == 0) return;
-    backward_kernel<<<nfronts, 256, sizeof(double) * (size_t)(max_u + 8), s>>>(ft, fronts, lbuf, xsol);
-}
-
-// ---------------------------------------------------------------------------------------------
 // State update + stacked infinity norm (max is order independent -> deterministic)
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) update_state_kernel(const int32_t* __restrict__ bus, const int32_t* __restrict__ quant,
@@ -502,16 +248,5 @@ void launch_objective(const EvalProg& ep, const int32_t* m_type, const int32_t* 
     if (nb) objective_kernel<<<nb, 256, 0, s>>>(ep, m_type, m_target, br_from, br_to, n_rows, va, vm, partial);
     objective_final_kernel<<<1, 256, 0, s>>>(partial, nb, out);
 }
-
-cudaError_t configure_kernels() {
-    const int maxsm = 226 * 1024;   // static + dynamic must stay within the 227 KB opt-in limit
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(front_task_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    if ((e = cudaFuncSetAttribute(front_task_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    if ((e = cudaFuncSetAttribute(front_task_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    if ((e = cudaFuncSetAttribute(backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024))) return e;
-    return cudaSuccess;
-}
-
 
 }  // namespace gse

@@ -24,6 +24,7 @@ struct EvalProg {
 struct FrontTab {
     const int32_t *p, *u1, *T, *nchild, *child_ptr, *children;
     const int32_t *rel_off, *rel;          // rel of a front as a child: update row -> parent local row
+    const int32_t *cb_off, *cbounds;       // per (front, child): lower bounds of rel at p and at every chunk edge
     const int32_t *reg_off, *reg_ptr;      // original-entry region table
     const uint32_t *orig_pos;              // (local row << 16) | local col, aligned with gval
     const int64_t *gval_off, *l_off, *u_off;
@@ -31,11 +32,12 @@ struct FrontTab {
 };
 
 struct TaskRec { int32_t front, ci, cj, pad; };
+struct BwdTask { int32_t front, split, nsplit, pbase; };
 
 constexpr int kFrontThreads = 256;
 constexpr int kMaxTile = 96;
 
-inline __host__ __device__ int pad_ld(int p) { return ((p + 11) / 16) * 16 + 4; }   // == 4 mod 16, >= p
+inline __host__ __device__ int pad_ld(int p) { return ((((p + 7) & ~7) + 11) / 16) * 16 + 4; }   // == 4 mod 16, >= round8(p)
 inline __host__ __device__ int round8(int x) { return (x + 7) & ~7; }
 
 // shared-memory doubles needed by one front task
@@ -53,8 +55,8 @@ void launch_accumulate(const int32_t* ptr, const int32_t* a, const int32_t* b, c
 void launch_front_tasks(int pclass, const FrontTab& ft, const TaskRec* tasks, int ntasks,
                         size_t smem_bytes, const double* gval, double* lbuf, double* ubuf,
                         unsigned long long* err, cudaStream_t s);
-void launch_backward(const FrontTab& ft, const int32_t* fronts, int nfronts, int max_u, const double* lbuf,
-                     double* xsol, cudaStream_t s);
+void launch_backward(const FrontTab& ft, const BwdTask* tasks, int ntasks, const double* lbuf,
+                     double* xsol, double* bpart, int32_t* bcnt, cudaStream_t s);
 void launch_update(const int32_t* bus, const int32_t* quant, const int32_t* pos, int n,
                    const double* xsol, double* va, double* vm, unsigned long long* delta_bits,
                    cudaStream_t s);
