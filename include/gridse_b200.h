@@ -70,6 +70,7 @@ typedef struct {
     int32_t rank, world;     /* area sharding: this process / number of processes           */
     const int32_t *area_rank;/* [n_areas] owner rank per area, NULL = all on rank 0          */
     int32_t persistent;      /* reserved (dataflow scheduler)                               */
+    int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default 48) */
 } gse_options;
 
 typedef struct {

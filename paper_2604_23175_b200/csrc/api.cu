@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -63,9 +64,11 @@ struct gse_plan {
     DevBuf<int32_t> f_rows_off, f_rows, f_cb_off, f_cbounds, bcnt;
     DevBuf<BwdTask> btasks;
     DevBuf<double> bpart;
+    DevBuf<long long> tbuf;
     DevBuf<uint32_t> orig_pos;
     DevBuf<int64_t> f_gval_off, f_l_off, f_u_off;
     DevBuf<TaskRec> tasks;
+    DevBuf<ChildRec> crecs;
     DevBuf<int32_t> bwd_fronts;
     DevBuf<double> lbuf, ubuf, xsol;
     DevBuf<int32_t> upd_bus, upd_quant, upd_pos;
@@ -199,7 +202,7 @@ gse_plan::~gse_plan() {
     for (auto* b : ib) b->release();
     DevBuf<double>* db[] = {&y_g, &y_b, &br_y, &z, &w, &g, &gw, &wrg, &gval, &refval, &lbuf, &ubuf, &xsol, &obj_partial, &status};
     for (auto* b : db) b->release();
-    btasks.release(); bpart.release();
+    btasks.release(); bpart.release(); tbuf.release(); crecs.release();
     orig_pos.release(); f_gval_off.release(); f_l_off.release(); f_u_off.release(); tasks.release(); flags.release();
 }
 
@@ -223,9 +226,12 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         bo.dense = opt->backend_dense != 0;
         if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
         if (opt->max_pivots == 32 || opt->max_pivots == 64) bo.max_pivots = opt->max_pivots;
+        if (opt->tile_rows >= 8 && opt->tile_rows <= kMaxTile) bo.tile_rows = opt->tile_rows / 8 * 8;
         bo.rank = opt->rank; bo.world = std::max(1, opt->world);
         if (opt->area_rank) bo.area_rank.assign(opt->area_rank, opt->area_rank + d->n_areas);
     }
+    if (const char* e = getenv("GSE_TILE_ROWS")) { int v = atoi(e); if (v >= 8 && v <= kMaxTile) bo.tile_rows = v / 8 * 8; }
+    if (const char* e = getenv("GSE_LEAF_BUSES")) { int v = atoi(e); if (v >= 1) bo.leaf_buses = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;
     std::string msg = build_host_program(*d, bo, hp);
@@ -313,6 +319,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
 
     // ---- level launches: tasks grouped by (level, pivot class) ----
     std::vector<TaskRec> trecs;
+    std::vector<ChildRec> crecs;
     for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
         for (int pclass : {1, 0}) {
             LevelLaunch L{pclass, (int)trecs.size(), 0, 0, hp.level_phase[lv]};
@@ -320,18 +327,52 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 const Front& f = hp.fronts[t.front];
                 const int cls = f.p == 0 ? 0 : 1;
                 if (cls != pclass) continue;
-                const int ni = std::min(f.T, f.u1 - t.ci * f.T), nj = std::min(f.T, f.u1 - t.cj * f.T);
-                L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, t.ci == t.cj));
-                trecs.push_back({t.front, t.ci, t.cj, 0});
+                const int T = std::max(f.T, 1);
+                const int ni = std::min(T, f.u1 - t.ci * T), nj = std::min(T, f.u1 - t.cj * T);
+                const bool diag = t.ci == t.cj;
+                // chain fronts: single child, identity map, no original entries -> tile read in place
+                bool direct = f.kind == 3 && f.children.size() == 1 && f.n_orig == 0;
+                if (direct) {
+                    const std::vector<int>& rel_c = hp.fronts[f.children[0]].rel;
+                    for (size_t q = 0; q < rel_c.size() && direct; ++q) direct = rel_c[q] == (int)q;
+                }
+                L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, diag, direct));
+                TaskRec r{};
+                r.front = t.front; r.ci = t.ci; r.cj = t.cj; r.p = f.p; r.u1 = f.u1; r.T = T;
+                r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = direct ? 1 : 0;
+                const int32_t* rp = &hp.reg_ptr[hp.front_reg_off[t.front]];
+                const int ridI = (t.ci + 1) * (t.ci + 2) / 2, ridJ = (t.cj + 1) * (t.cj + 2) / 2;
+                r.reg[0] = rp[0]; r.reg[1] = rp[1];
+                r.reg[2] = rp[ridI]; r.reg[3] = rp[ridI + 1];
+                r.reg[4] = rp[ridJ]; r.reg[5] = rp[ridJ + 1];
+                r.reg[6] = rp[ridI + t.cj + 1]; r.reg[7] = rp[ridI + t.cj + 2];
+                r.child_off = (int32_t)crecs.size();
+                for (int ch : f.children) {
+                    const Front& c = hp.fronts[ch];
+                    auto lb = [&](int key) { return (int32_t)(std::lower_bound(c.rel.begin(), c.rel.end(), key) - c.rel.begin()); };
+                    ChildRec cr{};
+                    cr.u_off = c.u_off; cr.rel_off = frel_off[ch];
+                    cr.eP = f.p ? lb(f.p) : 0;
+                    cr.bI = lb(f.p + t.ci * T); cr.eI = lb(f.p + t.ci * T + ni);
+                    cr.bJ = lb(f.p + t.cj * T); cr.eJ = lb(f.p + t.cj * T + nj);
+                    const bool hits_panel = f.p && cr.eP > 0;
+                    const bool hits_tile = !direct && cr.eI > cr.bI && cr.eJ > cr.bJ;
+                    if (!hits_panel && !hits_tile && !direct) continue;   // pruned (order of the rest is kept)
+                    crecs.push_back(cr);
+                    ++r.nchild;
+                }
+                trecs.push_back(r);
                 ++L.count;
             }
             if (L.count) {
-                if (L.smem > 222 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
+                if (L.smem > 220 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
                 plan->fwd.push_back(L);
             }
         }
     }
     CU(plan->tasks.upload(trecs));
+    CU(plan->crecs.upload(crecs));
+    plan->ft.task0 = plan->tasks.ptr; plan->ft.tbuf = nullptr; plan->ft.crecs = plan->crecs.ptr;
     std::vector<BwdTask> btasks;
     int pbase = 0;
     for (size_t i = 0; i < hp.bwd_levels.size(); ++i) {
@@ -339,7 +380,8 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         for (int f : hp.bwd_levels[i]) {
             const int u = hp.fronts[f].u1 - 1;
             const int ns = std::max(1, (u + 63) / 64);
-            for (int sp = 0; sp < ns; ++sp) btasks.push_back({f, sp, ns, pbase});
+            const Front& fr = hp.fronts[f];
+            for (int sp = 0; sp < ns; ++sp) btasks.push_back({f, sp, ns, pbase, fr.p, u, frows_off[f], 0, fr.l_off, 0});
             pbase += ns; B.count += ns;
         }
         plan->bwd.push_back(B);
@@ -558,6 +600,59 @@ double* gse_boundary_delta_dev(gse_plan* plan) { return plan->xsol.ptr + plan->h
 double* gse_status_dev(gse_plan* plan) { return plan->status.ptr; }
 
 void* gse_stream(gse_plan* plan) { return (void*)plan->stream; }
+
+// Debug: per-task phase clocks of the front kernel (8 clock64 stamps per task) of the next launches.
+int gse_debug_task_clocks(gse_plan* plan, int enable, long long* out, int64_t max_n) {
+    CU(cudaSetDevice(plan->device));
+    if (enable) {
+        if (!plan->tbuf.ptr) CU(plan->tbuf.alloc(plan->tasks.n * 8 + 8));
+        plan->ft.tbuf = plan->tbuf.ptr;
+        if (plan->graph) { cudaGraphExecDestroy(plan->graph); plan->graph = nullptr; }
+        return (int)plan->tasks.n;
+    }
+    if (out && plan->tbuf.ptr) CU(cudaMemcpy(out, plan->tbuf.ptr, sizeof(long long) * std::min<int64_t>(max_n, plan->tasks.n * 8), cudaMemcpyDeviceToHost));
+    plan->ft.tbuf = nullptr;
+    if (plan->graph) { cudaGraphExecDestroy(plan->graph); plan->graph = nullptr; }
+    return (int)plan->tasks.n;
+}
+
+// One outer iteration with a CUDA event around every launch (warm, ungraphed): per-launch device
+// time in microseconds.  kind: 0 eval, 1 accumulate, 2 front tasks, 3 backward, 4 state update.
+int gse_profile_iteration(gse_plan* plan, double* va, double* vm, int32_t max_n, int32_t* kind, int32_t* phase,
+                          int32_t* ctas, double* usec) {
+    CU(cudaSetDevice(plan->device));
+    std::vector<cudaEvent_t> evs;
+    std::vector<int> k, ph, ct;
+    auto mark = [&]() { cudaEvent_t e; cudaEventCreate(&e); cudaEventRecord(e, plan->stream); evs.push_back(e); };
+    cudaMemsetAsync(plan->flags.ptr, 0, sizeof(unsigned long long), plan->stream);
+    mark();
+    launch_eval(plan->ep, va, vm, plan->stream); mark(); k.push_back(0); ph.push_back(0); ct.push_back((plan->ep.n_vm + plan->ep.n_fl + plan->ep.n_inj + 127) / 128);
+    launch_accumulate(plan->acc_ptr.ptr, plan->acc_a.ptr, plan->acc_b.ptr, plan->g.ptr, plan->gw.ptr, plan->wrg.ptr, plan->gval.ptr,
+                      (int64_t)plan->hp.n_gval, plan->stream);
+    mark(); k.push_back(1); ph.push_back(0); ct.push_back((int)((plan->hp.n_gval + 255) / 256));
+    for (int phs : {1, 2, 3})
+        for (auto& L : plan->fwd) {
+            if (L.phase != phs) continue;
+            launch_front_tasks(L.pclass, plan->ft, plan->tasks.ptr + L.first, L.count, L.smem, plan->gval.ptr, plan->lbuf.ptr, plan->ubuf.ptr,
+                               plan->flags.ptr + 1, plan->stream);
+            mark(); k.push_back(2); ph.push_back(phs); ct.push_back(L.count);
+        }
+    for (int phs : {3, 4})
+        for (auto& B : plan->bwd) {
+            if (B.phase != phs) continue;
+            launch_backward(plan->ft, plan->btasks.ptr + B.first, B.count, plan->lbuf.ptr, plan->xsol.ptr, plan->bpart.ptr, plan->bcnt.ptr, plan->stream);
+            mark(); k.push_back(3); ph.push_back(phs); ct.push_back(B.count);
+        }
+    enqueue_update(plan, va, vm); mark(); k.push_back(4); ph.push_back(4); ct.push_back((int)(plan->upd_bus.n + 255) / 256);
+    CU(cudaStreamSynchronize(plan->stream));
+    int n = (int)k.size();
+    for (int i = 0; i < n && i < max_n; ++i) {
+        float ms = 0; cudaEventElapsedTime(&ms, evs[i], evs[i + 1]);
+        kind[i] = k[i]; phase[i] = ph[i]; ctas[i] = ct[i]; usec[i] = ms * 1e3;
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+    return n;
+}
 
 int gse_plan_stats(const gse_plan* plan, double* s, int32_t n) {
     const HostProgram& hp = plan->hp;

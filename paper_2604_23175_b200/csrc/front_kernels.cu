@@ -1,12 +1,15 @@
 // front_kernels.cu -- the multifrontal Schur-mode factorisation and its back-substitution.
 //
 // front_task_kernel<HAS_PIVOTS>: one CTA = one (front, row-chunk I, col-chunk J) task.
+//   0. one coalesced read brings the task header and its (pruned) child records into shared memory,
+//      so no phase starts with a chain of dependent global loads;
 //   1. assemble in shared memory: original entries (written by accumulate_kernel) + extend-add of
 //      the children's packed update matrices in fixed child order (deterministic, no atomics);
 //   2. factor the pivot block and solve the two row chunks against it: left-looking in blocks of
 //      8 columns -- the rank-k update of each block column runs on the FP64 tensor pipe
-//      (mma.sync m8n8k4 f64 from shared memory), the 8x8 diagonal block is factored redundantly
-//      in registers by every row thread (no communication), two barriers per 8 pivots;
+//      (mma.sync m8n8k4 f64 from shared memory); warp 0 updates and factors the 8x8 diagonal
+//      block while the other warps update the remaining rows (look-ahead), then every row thread
+//      solves its row against the published block;
 //   3. trailing / Schur update U_IJ = F_IJ - L_I L_J^T on the tensor pipe, written packed-lower;
 //   4. diagonal tasks store their slice of the factor panel for the backward pass.
 // Every task of a front recomputes the (small) pivot-block factor instead of exchanging it:
@@ -23,129 +26,200 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// child update block rows [r0,r1) x cols [c0,c1) (lower part) -> dst[(srel[i-ro]-rs)*ld + srel[j-co]-cs]
-// srow / scol: the child's rel map for these ranges, staged in shared memory.
+// child update block rows [r0,r1) x cols [c0,c1) (lower part) -> dst[(srow[i-r0]-rs)*ld + scol[j-c0]-cs]
+// srow / scol: the child's rel map for these ranges, staged in shared memory.  One warp per child
+// row (packed rows are contiguous -> coalesced), eight rows in flight per warp: the loop is L2-
+// latency bound, so memory-level parallelism is what matters.
 __device__ __forceinline__ void add_child_block(const double* __restrict__ U, const int* __restrict__ srow,
                                                 const int* __restrict__ scol, int r0, int r1, int c0, int c1,
                                                 double* dst, int ld, int rs, int cs, int warp, int lane, int nwarps) {
     if (c1 <= c0 || r1 <= r0) return;
-    for (int ib = r0 + warp; ib < r1; ib += 4 * nwarps) {
+    constexpr int kRows = 8;
+    for (int ib = r0 + warp; ib < r1; ib += kRows * nwarps) {
         for (int jb = c0; jb < c1; jb += 32) {
             const int j = jb + lane;
-            double v[4];
-            bool ok[4];
+            double v[kRows];
+            bool ok[kRows];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < kRows; ++q) {
                 const int i = ib + q * nwarps;
                 ok[q] = i < r1 && j < c1 && j <= i;
                 v[q] = ok[q] ? __ldg(U + (size_t)i * (i + 1) / 2 + j) : 0.0;
             }
             const int tc = j < c1 ? scol[j - c0] - cs : 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < kRows; ++q)
                 if (ok[q]) dst[(srow[ib + q * nwarps - r0] - rs) * ld + tc] += v[q];
         }
     }
 }
 
-constexpr int kStage = kFrontThreads + 2 * kMaxTile + 16;   // staged rel entries: pivots + I + J ranges
+constexpr int kStage = 64 + 2 * kMaxTile + 16;   // staged rel entries of one child: pivots + I + J ranges
+constexpr int kChildBatch = 32;
 
 template <int HAS_PIVOTS>
 __global__ void __launch_bounds__(kFrontThreads, HAS_PIVOTS ? 1 : 2)
 front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* __restrict__ gval,
                   double* __restrict__ lbuf, double* __restrict__ ubuf, unsigned long long* err) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ int s_rel[kStage];
-    const TaskRec tk = tasks[blockIdx.x];
-    const int f = tk.front, ci = tk.ci, cj = tk.cj;
-    const int p = HAS_PIVOTS ? ft.p[f] : 0;
-    const int u1 = ft.u1[f], T = ft.T[f];
+    __shared__ __align__(16) TaskRec hdr;
+    __shared__ __align__(16) ChildRec crec[kChildBatch];
+    __shared__ int s_rel[2][kStage];
+    __shared__ double s_ld[48];           // published 8x8 diagonal factor (36) + reciprocal pivots (8)
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+    long long* tb = ft.tbuf ? ft.tbuf + 8 * ((&tasks[blockIdx.x]) - (const TaskRec*)ft.task0) : nullptr;
+#define GSE_TICK(k) do { if (tb && tid == 0) tb[k] = clock64(); } while (0)
+    GSE_TICK(0);
+    if (tid < (int)(sizeof(TaskRec) / 16))
+        reinterpret_cast<int4*>(&hdr)[tid] = reinterpret_cast<const int4*>(&tasks[blockIdx.x])[tid];
+    __syncthreads();
+    const int f = hdr.front, ci = hdr.ci, cj = hdr.cj;
+    const int p = HAS_PIVOTS ? hdr.p : 0;
+    const int u1 = hdr.u1, T = hdr.T;
     const int i0 = ci * T, ni = min(T, u1 - i0), j0 = cj * T, nj = min(T, u1 - j0);
     const bool diag = ci == cj;
+    const bool direct = (hdr.flags & 1) != 0;      // tile comes straight from the single child's U
     const int ld = pad_ld(p);
     const int rp = p ? round8(p) : 0, ri = p ? round8(ni) : 0, rj = (p && !diag) ? round8(nj) : 0;
     const int ldt = round8(nj) | 1;
     double* pan = sm;
     double* tile = sm + (size_t)(rp + ri + rj) * ld;
-    const int tid = threadIdx.x, nth = blockDim.x;
-    const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+    // first batch of child records: issue now, consume after the zero fill
+    const int nchild = hdr.nchild;
+    if (tid < 2 * min(nchild, kChildBatch))
+        reinterpret_cast<int4*>(crec)[tid] = reinterpret_cast<const int4*>(ft.crecs + hdr.child_off)[tid];
 
     {
-        const int total = ((rp + ri + rj) * ld + round8(ni) * ldt + 1) >> 1;
+        const int total = ((rp + ri + rj) * ld + (direct ? 0 : round8(ni) * ldt) + 1) >> 1;
         double2* z2 = reinterpret_cast<double2*>(sm);
         for (int t = tid; t < total; t += nth) z2[t] = make_double2(0.0, 0.0);
     }
     __syncthreads();
     if (HAS_PIVOTS && tid < rp - p) pan[(p + tid) * ld + p + tid] = 1.0;   // identity on padded pivots
+    GSE_TICK(1);
 
-    // ---- original entries (written by accumulate_kernel into gval) --------------------------
+    // ---- original entries (written by accumulate_kernel into gval), four loads in flight ------
     {
-        const int32_t* rptr = ft.reg_ptr + ft.reg_off[f];
-        const int64_t goff = ft.gval_off[f];
-        const uint32_t* opos = ft.orig_pos + goff;
-        const double* gv = gval + goff;
-        if (p) {
-            for (int e = rptr[0] + tid; e < rptr[1]; e += nth) {       // region (0,0): pivot block
-                const uint32_t q = opos[e];
-                pan[(q >> 16) * ld + (q & 0xffffu)] = gv[e];
-            }
-            const int ridI = (ci + 1) * (ci + 2) / 2;
-            for (int e = rptr[ridI] + tid; e < rptr[ridI + 1]; e += nth) {
-                const uint32_t q = opos[e];
-                pan[(rp + (int)(q >> 16) - p - i0) * ld + (q & 0xffffu)] = gv[e];
-            }
-            if (!diag) {
-                const int ridJ = (cj + 1) * (cj + 2) / 2;
-                for (int e = rptr[ridJ] + tid; e < rptr[ridJ + 1]; e += nth) {
-                    const uint32_t q = opos[e];
-                    pan[(rp + ri + (int)(q >> 16) - p - j0) * ld + (q & 0xffffu)] = gv[e];
+        const uint32_t* opos = ft.orig_pos + hdr.gval_off;
+        const double* gv = gval + hdr.gval_off;
+        auto scatter = [&](int b, int e, double* dst, int ldd, int rsub, int csub) {
+            for (int e0 = b + tid; e0 < e; e0 += 4 * nth) {
+                uint32_t q[4];
+                double v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int ee = e0 + k * nth;
+                    q[k] = ee < e ? opos[ee] : 0u;
+                    v[k] = ee < e ? gv[ee] : 0.0;
                 }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (e0 + k * nth < e) dst[((int)(q[k] >> 16) - rsub) * ldd + ((int)(q[k] & 0xffffu) - csub)] = v[k];
             }
+        };
+        if (p) {
+            scatter(hdr.reg[0], hdr.reg[1], pan, ld, 0, 0);
+            scatter(hdr.reg[2], hdr.reg[3], pan + (size_t)rp * ld, ld, p + i0, 0);
+            if (!diag) scatter(hdr.reg[4], hdr.reg[5], pan + (size_t)(rp + ri) * ld, ld, p + j0, 0);
         }
-        const int ridT = (ci + 1) * (ci + 2) / 2 + cj + 1;
-        for (int e = rptr[ridT] + tid; e < rptr[ridT + 1]; e += nth) {
-            const uint32_t q = opos[e];
-            tile[((int)(q >> 16) - p - i0) * ldt + ((int)(q & 0xffffu) - p - j0)] = gv[e];
-        }
+        scatter(hdr.reg[6], hdr.reg[7], tile, ldt, p + i0, p + j0);
     }
     __syncthreads();
+    GSE_TICK(2);
 
     // ---- extend-add of the children's update matrices, fixed child order --------------------
-    {
-        const int nchild = ft.nchild[f], cptr = ft.child_ptr[f];
-        for (int c = 0; c < nchild; ++c) {
-            const int ch = ft.children[cptr + c];
-            const int32_t* rel = ft.rel + ft.rel_off[ch];
-            const double* U = ubuf + ft.u_off[ch];
-            const int32_t* cb = ft.cbounds + ft.cb_off[cptr + c];   // precomputed lower bounds of rel
-            const int eP = cb[0], bI = cb[1 + ci], eI = cb[2 + ci], bJ = cb[1 + cj], eJ = cb[2 + cj];
-            const int nI = eI - bI, nJ = eJ - bJ;
-            if ((eP <= 0 || !p) && (nI <= 0 || nJ <= 0)) continue;   // nothing lands in this task (uniform)
-            // stage the needed slices of rel: [0,eP) | [bI,eI) | [bJ,eJ)
-            int* sP = s_rel; int* sI = s_rel + eP; int* sJ = sI + nI;
-            for (int t = tid; t < eP + nI + nJ; t += nth)
-                s_rel[t] = t < eP ? rel[t] : t < eP + nI ? rel[bI + t - eP] : rel[bJ + t - eP - nI];
+    // (the child list of a task is pruned on the host to the children that reach its regions)
+    for (int cb0 = 0; cb0 < nchild; cb0 += kChildBatch) {
+        const int nb = min(kChildBatch, nchild - cb0);
+        if (cb0) {
             __syncthreads();
+            if (tid < 2 * nb) reinterpret_cast<int4*>(crec)[tid] = reinterpret_cast<const int4*>(ft.crecs + hdr.child_off + cb0)[tid];
+            __syncthreads();
+        }
+        auto stage = [&](int c, int buf) {   // rel slices [0,eP) | [bI,eI) | [bJ,eJ) of child c
+            const ChildRec& cr = crec[c];
+            const int32_t* rel = ft.rel + cr.rel_off;
+            const int eP = cr.eP, nI = cr.eI - cr.bI, nJ = cr.eJ - cr.bJ;
+            for (int t = tid; t < eP + nI + nJ; t += nth)
+                s_rel[buf][t] = t < eP ? rel[t] : t < eP + nI ? rel[cr.bI + t - eP] : rel[cr.bJ + t - eP - nI];
+        };
+        stage(0, 0);
+        __syncthreads();
+        for (int c = 0; c < nb; ++c) {
+            const ChildRec cr = crec[c];
+            const int buf = c & 1;
+            if (c + 1 < nb) stage(c + 1, buf ^ 1);          // overlaps with this child's loads
+            const double* U = ubuf + cr.u_off;
+            const int eP = cr.eP, bI = cr.bI, eI = cr.eI, bJ = cr.bJ, eJ = cr.eJ;
+            const int* sP = s_rel[buf]; const int* sI = sP + eP; const int* sJ = sI + (eI - bI);
             if (p) {
                 add_child_block(U, sP, sP, 0, eP, 0, eP, pan, ld, 0, 0, warp, lane, nwarps);
                 add_child_block(U, sI, sP, bI, eI, 0, eP, pan + (size_t)rp * ld, ld, p + i0, 0, warp, lane, nwarps);
                 if (!diag) add_child_block(U, sJ, sP, bJ, eJ, 0, eP, pan + (size_t)(rp + ri) * ld, ld, p + j0, 0, warp, lane, nwarps);
             }
-            add_child_block(U, sI, sJ, bI, eI, bJ, eJ, tile, ldt, p + i0, p + j0, warp, lane, nwarps);
+            if (!direct) add_child_block(U, sI, sJ, bI, eI, bJ, eJ, tile, ldt, p + i0, p + j0, warp, lane, nwarps);
             __syncthreads();
         }
     }
+    GSE_TICK(3);
 
     // ---- blocked panel factorisation (block = 8 columns) ---------------------------------------
     if (HAS_PIVOTS && p) {
         const int R = rp + ri + rj;                 // padded rows: [pivots | chunk I | chunk J]
         const int ntile = R >> 3;
         for (int kb = 0; kb < rp; kb += 8) {
-            // A. rows >= kb: block column kb -= A[rows, 0:kb] * A[kb:kb+8, 0:kb]^T   (tensor pipe)
-            if (kb) {
-                const int t0 = kb >> 3;
-                for (int tb = t0 + warp; tb < ntile; tb += 2 * nwarps) {
-                    const int ta = tb, tc2 = tb + nwarps;
+            const int t0 = kb >> 3;
+            if (warp == 0) {
+                // diagonal tile first: update (tensor pipe), then factor in registers and publish
+                if (kb) {
+                    const double* ap = pan + (size_t)(kb + (lane >> 2)) * ld + (lane & 3);
+                    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+                    int kk = 0;
+                    for (; kk + 4 < kb; kk += 8) {           // two independent chains
+                        dmma_m8n8k4(c0, c1, ap[kk], ap[kk]);
+                        dmma_m8n8k4(e0, e1, ap[kk + 4], ap[kk + 4]);
+                    }
+                    if (kk < kb) dmma_m8n8k4(c0, c1, ap[kk], ap[kk]);
+                    double* o = pan + (size_t)(kb + (lane >> 2)) * ld + kb + 2 * (lane & 3);
+                    o[0] -= c0 + e0; o[1] -= c1 + e1;
+                    __syncwarp();
+                }
+                double d[36];   // lower triangle, row-major: d[i*(i+1)/2 + j]
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j <= i; ++j) d[i * (i + 1) / 2 + j] = pan[(kb + i) * ld + kb + j];
+                double rinv[8];
+                int badk = -1;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double dk = d[k * (k + 1) / 2 + k];
+                    if (!(dk > 0.0) && badk < 0) badk = k;
+                    const double r = rsqrt(dk);
+                    rinv[k] = r;
+                    d[k * (k + 1) / 2 + k] = dk * r;
+#pragma unroll
+                    for (int i = k + 1; i < 8; ++i) d[i * (i + 1) / 2 + k] *= r;
+#pragma unroll
+                    for (int j = k + 1; j < 8; ++j)
+#pragma unroll
+                        for (int i = j; i < 8; ++i)
+                            d[i * (i + 1) / 2 + j] = fma(-d[i * (i + 1) / 2 + k], d[j * (j + 1) / 2 + k], d[i * (i + 1) / 2 + j]);
+                }
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < 36; ++i) s_ld[i] = d[i];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) s_ld[36 + k] = rinv[k];
+                    if (badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
+                }
+            } else if (kb) {
+                // rows below the diagonal tile: block column kb -= A[rows, 0:kb] * A[kb:kb+8, 0:kb]^T
+                const int nw = nwarps - 1;
+                for (int tb2 = t0 + 1 + (warp - 1); tb2 < ntile; tb2 += 2 * nw) {
+                    const int ta = tb2, tc2 = tb2 + nw;
                     const bool two = tc2 < ntile;
                     const double* a0p = pan + (size_t)(ta * 8 + (lane >> 2)) * ld + (lane & 3);
                     const double* a1p = pan + (size_t)((two ? tc2 : ta) * 8 + (lane >> 2)) * ld + (lane & 3);
@@ -164,49 +238,15 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
                         o1[0] -= c10; o1[1] -= c11;
                     }
                 }
-                __syncthreads();
             }
-            // B. every row thread factors the 8x8 diagonal block in registers (redundantly) and
-            //    solves its own row against it
-            const bool act = tid >= kb && tid < R;
-            double d[36];   // lower triangle, row-major: d[i*(i+1)/2 + j]
-            if (act) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j <= i; ++j) d[i * (i + 1) / 2 + j] = pan[(kb + i) * ld + kb + j];
-            }
-            __syncthreads();   // everyone holds the block before its owner rows overwrite it
-            if (act) {
-                double rinv[8];
-                bool bad = false;
-                int badk = 0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double dk = d[k * (k + 1) / 2 + k];
-                    if (!(dk > 0.0) && !bad) { bad = true; badk = k; }
-                    const double r = rsqrt(dk);
-                    rinv[k] = r;
-                    d[k * (k + 1) / 2 + k] = dk * r;
-#pragma unroll
-                    for (int i = k + 1; i < 8; ++i) d[i * (i + 1) / 2 + k] *= r;
-#pragma unroll
-                    for (int j = k + 1; j < 8; ++j)
-#pragma unroll
-                        for (int i = j; i < 8; ++i)
-                            d[i * (i + 1) / 2 + j] = fma(-d[i * (i + 1) / 2 + k], d[j * (j + 1) / 2 + k], d[i * (i + 1) / 2 + j]);
-                }
+            __syncthreads();
+            // every row at or below the block solves against the published 8x8 factor
+            if (tid >= kb && tid < R) {
                 double* myrow = pan + (size_t)tid * ld + kb;
                 if (tid < kb + 8) {
-                    if (tid == kb && bad && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
                     const int i = tid - kb;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        double v = 0.0;
-#pragma unroll
-                        for (int ii = 0; ii < 8; ++ii) if (ii == i && j <= ii) v = d[ii * (ii + 1) / 2 + j];
-                        myrow[j] = v;
-                    }
+                    for (int j = 0; j < 8; ++j) myrow[j] = j <= i ? s_ld[i * (i + 1) / 2 + j] : 0.0;
                 } else {
                     double y[8];
 #pragma unroll
@@ -215,8 +255,8 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
                     for (int k = 0; k < 8; ++k) {
                         double acc = y[k];
 #pragma unroll
-                        for (int j = 0; j < k; ++j) acc = fma(-y[j], d[k * (k + 1) / 2 + j], acc);
-                        y[k] = acc * rinv[k];
+                        for (int j = 0; j < k; ++j) acc = fma(-y[j], s_ld[k * (k + 1) / 2 + j], acc);
+                        y[k] = acc * s_ld[36 + k];
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) myrow[j] = y[j];
@@ -225,6 +265,7 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
             __syncthreads();
         }
     }
+    GSE_TICK(4);
 
     // ---- trailing update on the FP64 tensor pipe: U_IJ = F_IJ - L_I L_J^T -------------------
     {
@@ -233,10 +274,25 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
         const int nbi = round8(ni) >> 3, nbj = round8(nj) >> 3;
         const int ngj = (nbj + 3) >> 2;                 // groups of four 8-wide column blocks
         const int kend = (p + 3) & ~3;
-        double* U = ubuf + ft.u_off[f];
+        double* U = ubuf + hdr.u_off;
+        const double* Uc = direct ? ubuf + crec[0].u_off : nullptr;   // chain: F_IJ lives in the child's U
         for (int w = warp; w < nbi * ngj; w += nwarps) {
             const int bi = w / ngj, gj = w % ngj;
             if (diag && gj * 4 > bi) continue;
+            const int row = bi * 8 + (lane >> 2);
+            const int I = i0 + row;
+            double fv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) fv[q] = 0.0;
+            if (direct && row < ni) {
+                const double* crow = Uc + (size_t)(p + I) * (p + I + 1) / 2 + p;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int col = (gj * 4 + q) * 8 + 2 * (lane & 3), J = j0 + col;
+                    if (col < nj && J <= I) fv[2 * q] = __ldg(crow + J);
+                    if (col + 1 < nj && J + 1 <= I) fv[2 * q + 1] = __ldg(crow + J + 1);
+                }
+            }
             double c[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             if (p) {
                 const double* ap = Pi + (size_t)(bi * 8 + (lane >> 2)) * ld + (lane & 3);
@@ -253,23 +309,22 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
                     for (int q = 0; q < 4; ++q) dmma_m8n8k4(c[2 * q], c[2 * q + 1], a, bp[q][kk]);
                 }
             }
-            const int row = bi * 8 + (lane >> 2);
             if (row < ni) {
-                const int I = i0 + row;
                 double* urow = U + (size_t)I * (I + 1) / 2;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int bj = gj * 4 + q;
                     if (bj >= nbj) break;
                     const int col = bj * 8 + 2 * (lane & 3), J = j0 + col;
-                    if (col < nj && J <= I) urow[J] = tile[row * ldt + col] - c[2 * q];
-                    if (col + 1 < nj && J + 1 <= I) urow[J + 1] = tile[row * ldt + col + 1] - c[2 * q + 1];
+                    if (col < nj && J <= I) urow[J] = (direct ? fv[2 * q] : tile[row * ldt + col]) - c[2 * q];
+                    if (col + 1 < nj && J + 1 <= I) urow[J + 1] = (direct ? fv[2 * q + 1] : tile[row * ldt + col + 1]) - c[2 * q + 1];
                 }
             }
         }
+        GSE_TICK(5);
         // ---- factor panel to global (diagonal tasks own their row chunk) ----------------------
         if (HAS_PIVOTS && p && diag) {
-            double* L = lbuf + ft.l_off[f];
+            double* L = lbuf + hdr.l_off;
             if (ci == 0)
                 for (int r = warp; r < p; r += nwarps)
                     for (int k = lane; k < p; k += 32) L[(size_t)r * p + k] = pan[r * ld + k];
@@ -277,7 +332,9 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
             for (int r = warp; r < ni; r += nwarps)
                 for (int k = lane; k < p; k += 32) Li[(size_t)r * p + k] = Pi[r * ld + k];
         }
+        GSE_TICK(6);
     }
+#undef GSE_TICK
 }
 
 void launch_front_tasks(int pclass, const FrontTab& ft, const TaskRec* tasks, int ntasks,
@@ -306,13 +363,21 @@ __global__ void __launch_bounds__(128) backward_kernel(FrontTab ft, const BwdTas
     __shared__ int s_last;
     const BwdTask tk = tasks[blockIdx.x];
     const int f = tk.front;
-    const int p = ft.p[f], u = ft.u1[f] - 1;
-    const double* L = lbuf + ft.l_off[f];
-    const int32_t* rows = ft.rows + ft.rows_off[f];
+    const int p = tk.p, u = tk.u;
+    const double* L = lbuf + tk.l_off;
+    const int32_t* rows = ft.rows + tk.rows_off;
     const int tid = threadIdx.x, k = tid & 63, h = tid >> 6;
     const int lo = tk.split * kBwdRows, n = min(kBwdRows, u - lo);
+    // L11 is needed only by the CTA that finishes last; every CTA prefetches it asynchronously so
+    // the copy overlaps the matrix-vector part instead of following the atomic hand-off
+    for (int t = tid; t < p * p; t += 128) {
+        const int r = t / p, c = t - r * p;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&l11[r * 65 + c]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(L + t));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    const double yk = (tid < p) ? __ldg(L + (size_t)(p + u) * p + tid) : 0.0;
     if (tid < kBwdRows) xs[tid] = tid < n ? xsol[rows[p + lo + tid]] : 0.0;
-    // the last split also prefetches L11 (needed only by whichever CTA finishes last, usually this one)
     __syncthreads();
     {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -339,22 +404,26 @@ __global__ void __launch_bounds__(128) backward_kernel(FrontTab ft, const BwdTas
         __syncthreads();
         if (tid == 0) s_last = atomicAdd(&bcnt[f], 1) == tk.nsplit - 1;
         __syncthreads();
-        if (!s_last) return;
+        if (!s_last) { asm volatile("cp.async.wait_group 0;\n" ::); return; }
         __threadfence();
     }
-    // ---- last CTA of the front: combine, then solve L11^T x = t in warp 0 --------------------
-    for (int r = tid >> 5; r < p; r += 4)
-        for (int c = tid & 31; c < p; c += 32) l11[r * 65 + c] = L[(size_t)r * p + c];
+    // ---- last CTA of the front: combine (split order), then solve L11^T x = t in warp 0 ------
     if (tid < 64) {
         double acc = 0.0;
         if (tid < p) {
             const volatile double* bp = bpart + (size_t)tk.pbase * 64 + tid;
-            for (int s = 0; s < tk.nsplit; ++s) acc += bp[(size_t)s * 64];
-            acc = L[(size_t)(p + u) * p + tid] - acc;
+            int s = 0;
+            for (; s + 3 < tk.nsplit; s += 4) {
+                const double b0 = bp[(size_t)s * 64], b1 = bp[(size_t)(s + 1) * 64], b2 = bp[(size_t)(s + 2) * 64], b3 = bp[(size_t)(s + 3) * 64];
+                acc = (((acc + b0) + b1) + b2) + b3;
+            }
+            for (; s < tk.nsplit; ++s) acc += bp[(size_t)s * 64];
+            acc = yk - acc;
         }
         tv[tid] = acc;
     }
     if (tid == 0 && tk.nsplit > 1) bcnt[f] = 0;
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
     if (tid < 32) {
         double t0 = tv[tid], t1 = tv[tid + 32];
@@ -377,7 +446,7 @@ void launch_backward(const FrontTab& ft, const BwdTask* tasks, int ntasks, const
 }
 
 cudaError_t configure_kernels() {
-    const int maxsm = 222 * 1024;   // static + dynamic must stay within the 227 KB opt-in limit
+    const int maxsm = 220 * 1024;   // static + dynamic must stay within the 227 KB opt-in limit
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(front_task_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
     if ((e = cudaFuncSetAttribute(front_task_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;

@@ -20,6 +20,18 @@ struct EvalProg {
     double *g, *gw, *wrg;
 };
 
+// One (front, row-chunk, col-chunk) task: everything the CTA needs, read with one coalesced load.
+struct TaskRec {                                      // 128 bytes
+    int32_t front, ci, cj, p, u1, T, nchild, child_off;
+    int32_t reg[8];                                   // original-entry ranges (relative to gval_off): PP, IP, JP, tile
+    int64_t gval_off, l_off, u_off;
+    int32_t flags, pad[9];                            // flags bit 0: tile read directly from the single child's U
+};
+// One child of a task (children that do not reach the task's regions are pruned on the host).
+struct ChildRec { int64_t u_off; int32_t rel_off, eP, bI, eI, bJ, eJ; };   // 32 bytes
+struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, pad; int64_t l_off, pad2; };   // 48 bytes
+
+
 // Front tables (SoA over fronts).
 struct FrontTab {
     const int32_t *p, *u1, *T, *nchild, *child_ptr, *children;
@@ -29,10 +41,10 @@ struct FrontTab {
     const uint32_t *orig_pos;              // (local row << 16) | local col, aligned with gval
     const int64_t *gval_off, *l_off, *u_off;
     const int32_t *rows_off, *rows;        // global positions of [pivots | update rows]
+    const ChildRec* crecs;          // per-task child records
+    long long* tbuf;                       // optional per-task phase clocks (debug), 8 per task
+    const void* task0;                     // base of the task array (indexes tbuf)
 };
-
-struct TaskRec { int32_t front, ci, cj, pad; };
-struct BwdTask { int32_t front, split, nsplit, pbase; };
 
 constexpr int kFrontThreads = 256;
 constexpr int kMaxTile = 96;
@@ -41,11 +53,11 @@ inline __host__ __device__ int pad_ld(int p) { return ((((p + 7) & ~7) + 11) / 1
 inline __host__ __device__ int round8(int x) { return (x + 7) & ~7; }
 
 // shared-memory doubles needed by one front task
-inline __host__ __device__ size_t task_smem_doubles(int p, int ni, int nj, bool diag) {
+inline __host__ __device__ size_t task_smem_doubles(int p, int ni, int nj, bool diag, bool direct = false) {
     size_t ld = pad_ld(p);
     size_t rows = (p ? round8(p) : 0) + (p ? round8(ni) : 0) + ((p && !diag) ? round8(nj) : 0);
     size_t ldt = (size_t)(round8(nj) | 1);
-    return rows * ld + (size_t)round8(ni) * ldt + 16;
+    return rows * ld + (direct ? 0 : (size_t)round8(ni) * ldt) + 16;
 }
 
 void launch_eval(const EvalProg& ep, const double* va, const double* vm, cudaStream_t s);

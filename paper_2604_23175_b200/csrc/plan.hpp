@@ -90,6 +90,7 @@ struct BuildOptions {
     bool dense = false;
     int leaf_buses = 12;
     int max_pivots = 64;
+    int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;
 };

@@ -154,8 +154,7 @@ void nd_recurse(NDGraph& g, std::vector<int>& verts, int leaf, std::vector<std::
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-void choose_chunks(Front& f) {
-    const int TMAX = 96;
+void choose_chunks(Front& f, int TMAX) {
     if (f.u1 <= TMAX) { f.T = f.u1; f.nch = f.u1 > 0 ? 1 : 0; return; }
     int nch = (f.u1 + TMAX - 1) / TMAX;
     int T = round_up((f.u1 + nch - 1) / nch, 8);
@@ -476,7 +475,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             for (int fi = 0; fi < A.n_fronts; ++fi) e_start[fi + 1] = e_start[fi] + hp.fronts[A.first_front + fi].p;
             for (int fi = 0; fi <= A.n_fronts; ++fi) {
                 Front& f = hp.fronts[A.first_front + fi];
-                choose_chunks(f);
+                choose_chunks(f, opt.tile_rows);
                 const bool is_root = fi == A.n_fronts;
                 const int c0 = is_root ? ni : e_start[fi], c1 = is_root ? nloc : e_start[fi + 1];
                 const std::vector<int>* st = is_root ? nullptr : &structs[fi];
@@ -509,7 +508,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 hp.n_gval += (int64_t)ents.size();
             }
         } else {
-            choose_chunks(hp.fronts[root_id]);
+            choose_chunks(hp.fronts[root_id], opt.tile_rows);
         }
         for (int b : touched) { loc_va[b] = -1; loc_vm[b] = -1; }
     }
@@ -531,7 +530,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             for (int a = 0; a < K; ++a) g.children.push_back(hp.area_root[a]);
             g.parent = first_coord + 1;
             g.rel.resize(g.u1); std::iota(g.rel.begin(), g.rel.end(), 0);
-            choose_chunks(g);
+            choose_chunks(g, opt.tile_rows);
             hp.gamma_root = first_coord;
             hp.fronts.push_back(std::move(g));
             int nchain = (ng + PMAX - 1) / PMAX;
@@ -542,7 +541,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 c.children.push_back((int)hp.fronts.size() - 1);
                 c.parent = k + 1 < nchain ? (int)hp.fronts.size() + 1 : -1;
                 c.rel.resize(c.u1); std::iota(c.rel.begin(), c.rel.end(), 0);
-                choose_chunks(c);
+                choose_chunks(c, opt.tile_rows);
                 hp.fronts.push_back(std::move(c));
             }
         } else {
