@@ -628,3 +628,39 @@ int orc_max_threads(void) {
     return 1;
 #endif
 }
+
+/* ---- area-sharded variants (the multi-process driver tests shard areas over ranks) ---- */
+int orc_local_masked(orc_t *o, const double *va, const double *vm, const int32_t *mine) {
+    int K = o->d.n_areas;
+    for (int a = 0; a < K; a++) {
+        if (!mine[a]) continue;
+        area_t *A = &o->areas[a];
+        eval_rows(o, A, va, vm); accumulate(o, A);
+        A->fail_pivot = chol_refactor(&A->ch, A->data_ii);
+        if (A->fail_pivot < 0) condense(A);
+        else { o->err_kind = 1; o->err_area = a; o->err_pivot = A->fail_pivot; return -1; }
+    }
+    return 0;
+}
+void orc_get_schur(const orc_t *o, int a, double *s_b, double *b_hat) { const area_t *A = &o->areas[a];
+    memcpy(s_b, A->s_b, sizeof(double) * (size_t)A->n_b * A->n_b); memcpy(b_hat, A->b_hat, sizeof(double) * A->n_b); }
+void orc_set_schur(orc_t *o, int a, const double *s_b, const double *b_hat) { area_t *A = &o->areas[a];
+    memcpy(A->s_b, s_b, sizeof(double) * (size_t)A->n_b * A->n_b); memcpy(A->b_hat, b_hat, sizeof(double) * A->n_b); }
+void orc_set_dx_gamma(orc_t *o, const double *dx) { memcpy(o->dx_gamma, dx, sizeof(double) * o->n_gamma); }
+/* recovery of the owned areas + every rank's replica of the boundary state */
+double orc_recover_masked(orc_t *o, double *va, double *vm, const int32_t *mine) {
+    int K = o->d.n_areas; double dmax = 0.0;
+    for (int a = 0; a < K; a++) { if (!mine[a]) continue; area_t *A = &o->areas[a];
+        recover(A, o->dx_gamma);
+        for (int i = 0; i < A->n_ia; i++) va[A->ia_bus[i]] += A->dxi[i];
+        for (int i = 0; i < A->n_int_bus; i++) vm[A->int_bus[i]] += A->dxi[A->n_ia + i];
+        for (int i = 0; i < A->n_i; i++) if (fabs(A->dxi[i]) > dmax) dmax = fabs(A->dxi[i]); }
+    for (int s = 0; s < o->n_gamma; s++) { int b = o->gamma_bus[s]; if (s < o->n_ga) va[b] += o->dx_gamma[s]; else vm[b] += o->dx_gamma[s]; if (fabs(o->dx_gamma[s]) > dmax) dmax = fabs(o->dx_gamma[s]); }
+    return dmax;
+}
+/* buses whose state this rank owns: interiors of its areas (boundary buses are replicated) */
+void orc_owned_interior_mask(const orc_t *o, const int32_t *mine, int32_t *bus_mask) {
+    for (int b = 0; b < o->d.n_bus; b++) bus_mask[b] = 0;
+    for (int a = 0; a < o->d.n_areas; a++) { if (!mine[a]) continue; const area_t *A = &o->areas[a];
+        for (int i = 0; i < A->n_int_bus; i++) bus_mask[A->int_bus[i]] = 1; }
+}

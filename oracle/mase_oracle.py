@@ -203,6 +203,35 @@ class Oracle:
         assert va.dtype == np.float64 and vm.dtype == np.float64
         return float(_lib().orc_recover(self._h, _p(va, _f64p), _p(vm, _f64p), threads))
 
+    # -- area-sharded variants (multi-process driver tests) -----------------------------------
+    def local_masked(self, va, vm, mine):
+        lib = _lib()
+        lib.orc_local_masked.argtypes = [C.c_void_p, _f64p, _f64p, _i32p]
+        mine = np.ascontiguousarray(mine, dtype=np.int32)
+        if lib.orc_local_masked(self._h, _p(np.ascontiguousarray(va), _f64p),
+                                _p(np.ascontiguousarray(vm), _f64p), _p(mine, _i32p)):
+            self._raise()
+
+    def set_schur(self, a, s_b, b_hat):
+        lib = _lib()
+        lib.orc_set_schur.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p]
+        s_b = np.ascontiguousarray(s_b, dtype=np.float64)
+        b_hat = np.ascontiguousarray(b_hat, dtype=np.float64)
+        lib.orc_set_schur(self._h, a, _p(s_b, _f64p), _p(b_hat, _f64p))
+
+    def set_dx_gamma(self, dx):
+        lib = _lib()
+        lib.orc_set_dx_gamma.argtypes = [C.c_void_p, _f64p]
+        dx = np.ascontiguousarray(dx, dtype=np.float64)
+        lib.orc_set_dx_gamma(self._h, _p(dx, _f64p))
+
+    def recover_masked(self, va, vm, mine):
+        lib = _lib()
+        lib.orc_recover_masked.restype = C.c_double
+        lib.orc_recover_masked.argtypes = [C.c_void_p, _f64p, _f64p, _i32p]
+        mine = np.ascontiguousarray(mine, dtype=np.int32)
+        return float(lib.orc_recover_masked(self._h, _p(va, _f64p), _p(vm, _f64p), _p(mine, _i32p)))
+
     def objective(self, va, vm):
         va = np.ascontiguousarray(va, dtype=np.float64)
         vm = np.ascontiguousarray(vm, dtype=np.float64)

@@ -1,0 +1,252 @@
+"""Area-sharded multi-GPU solve: one process per GPU, ``torch.distributed`` for the plumbing.
+
+SURVEY.md section 8(e): areas are independent between the two coordinator exchanges
+(reference ``solver.py:277-298,318-326``), so each rank owns a contiguous block of areas
+(balanced by estimated factor work), condenses them locally and
+
+  1. sends its packed ``(S_b | b_hat)`` blocks to the coordinator rank (variable-size
+     gather = grouped send/recv; NCCL over NVLink on GPUs),
+  2. the coordinator scatters them into ``S_Gamma`` **in area order** -- so the bits do not
+     depend on the number of ranks -- and runs the dense boundary solve,
+  3. ``delta_x_Gamma`` is broadcast back, every rank recovers its interiors and updates its
+     replica of the boundary state,
+  4. one MAX all-reduce carries the convergence scalar (and the failure flag).
+
+The driver is engine-agnostic: the product engine (``CudaEngine``) wraps the C-ABI plan;
+the CPU tests inject an oracle-backed engine and run the same code under ``gloo``.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from .measurement import StateVector
+from .partition import build_variable_maps
+from .solver import PHASES, SolveReport, SolverConfig, SolverError
+
+
+def area_work_estimate(maps):
+    """Relative factor + condensation work per area (interior^2 bandwidth-like + Schur)."""
+    return np.array([m.n_interior * 40.0 + m.n_interior * m.n_boundary + m.n_boundary ** 2.0 + 1.0
+                     for m in maps])
+
+
+def assign_areas(work, world):
+    """Contiguous blocks of areas per rank, greedy linear partition of ``work``.
+
+    Returns ``area_rank`` (owner per area).  Every rank gets at least one area when
+    ``len(work) >= world``; surplus ranks own nothing otherwise.
+    """
+    work = np.asarray(work, dtype=float)
+    k = len(work)
+    area_rank = np.zeros(k, dtype=np.int32)
+    if world <= 1 or k == 0:
+        return area_rank
+    target = work.sum() / min(world, k)
+    rank, acc = 0, 0.0
+    for a in range(k):
+        remaining_areas, remaining_ranks = k - a, min(world, k) - rank
+        if rank < min(world, k) - 1 and acc > 0 and (
+                acc + 0.5 * work[a] > target or remaining_areas <= remaining_ranks - 1):
+            rank, acc = rank + 1, 0.0
+        area_rank[a] = rank
+        acc += work[a]
+    return area_rank
+
+
+class CudaEngine:
+    """Phase engine over the C-ABI plan (``libgridse_b200.so``)."""
+
+    def __init__(self, net, ms, part, bord, maps, cfg, rank, world, area_rank, device):
+        import torch
+        from . import _native
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+        self.plan = _native.Plan(net, ms, part, bord, maps, device=device,
+                                 dense=cfg.backend == "dense", rank=rank, world=world,
+                                 area_rank=area_rank)
+        self.n_bus, self.n_gamma = net.n_bus, bord.n_gamma
+        self.state = torch.empty((2, net.n_bus), dtype=torch.float64, device=self.dev)
+        ptr, n, off = self.plan.exchange_buffer()
+        self.offsets = off
+        self.exchange = self._view(ptr, n)
+        self.delta = self._view(self.plan.boundary_delta_ptr(), max(self.n_gamma, 1))[: self.n_gamma]
+        owned = np.zeros(net.n_bus, dtype=bool)
+        for a, m in enumerate(maps):
+            if area_rank[a] == rank:
+                owned[m.internal_buses] = True
+        self.owned_mask = torch.from_numpy(owned).to(self.dev)
+
+    def _view(self, ptr, n):
+        class _Dev:
+            pass
+        holder = _Dev()
+        holder.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8",
+                                           "data": (int(ptr), False), "version": 3}
+        return self.torch.as_tensor(holder, device=self.dev)
+
+    def load_state(self, va, vm):
+        self.state.copy_(self.torch.from_numpy(np.stack([va, vm])))
+        self.torch.cuda.synchronize(self.dev)
+
+    def phase_local(self):
+        va, vm = self.state[0].data_ptr(), self.state[1].data_ptr()
+        self.plan.phase_assemble(va, vm)
+        self.plan.phase_condense()
+
+    def phase_boundary(self):
+        self.plan.phase_boundary()
+
+    def phase_recover(self):
+        return self.plan.phase_recover(self.state[0].data_ptr(), self.state[1].data_ptr())
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.dev)
+
+    def objective(self):
+        return self.plan.objective(self.state[0].data_ptr(), self.state[1].data_ptr())
+
+    def close(self):
+        self.plan.close()
+
+
+class DistributedEstimator:
+    """Multi-rank counterpart of ``MultiAreaEstimator`` (same ``estimate`` contract)."""
+
+    def __init__(self, net, ms, part, maps=None, config: SolverConfig = None, device=0,
+                 engine_factory=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.cfg = config or SolverConfig()
+        self.net, self.ms, self.part = net, ms, part
+        self.bord, self.maps = maps if maps is not None else build_variable_maps(net, part)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.area_rank = assign_areas(area_work_estimate(self.maps), self.world)
+        self.n_gamma = self.bord.n_gamma
+        t0 = time.perf_counter()
+        factory = engine_factory or CudaEngine
+        self.engine = factory(net, ms, part, self.bord, self.maps, self.cfg, self.rank, self.world,
+                              self.area_rank, device)
+        self.setup_s = time.perf_counter() - t0
+        # contiguous exchange segment of every rank: [off[first area], off[last area + 1])
+        off = self.engine.offsets
+        self.segments = []
+        for r in range(self.world):
+            mine = np.flatnonzero(self.area_rank == r)
+            self.segments.append((int(off[mine[0]]), int(off[mine[-1] + 1])) if mine.size else (0, 0))
+        self.launches_per_solve = 0
+        self.last_gpu_s = 0.0
+
+    # -- collectives ---------------------------------------------------------------------------
+    def _gather_blocks(self):
+        if self.world == 1:
+            return
+        dist, buf = self.dist, self.engine.exchange
+        ops = []
+        if self.rank == 0:
+            for r in range(1, self.world):
+                lo, hi = self.segments[r]
+                if hi > lo:
+                    ops.append(dist.P2POp(dist.irecv, buf[lo:hi], r, group=self.group))
+        else:
+            lo, hi = self.segments[self.rank]
+            if hi > lo:
+                ops.append(dist.P2POp(dist.isend, buf[lo:hi], 0, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def _allreduce_max(self, values):
+        t = self.torch.tensor(values, dtype=self.torch.float64, device=self.engine.exchange.device)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return [float(v) for v in t.cpu()]
+
+    # -- the solve -------------------------------------------------------------------------------
+    def update_measurements(self, ms):
+        self.engine.plan.set_measurements(ms.z)
+        self.engine.plan.set_weights(ms.weight)
+        self.ms = ms
+
+    def estimate(self, on_iteration=None):
+        cfg, eng = self.cfg, self.engine
+        t_start = time.perf_counter()
+        flat = StateVector.flat_start(self.net)
+        eng.load_state(flat.va, flat.vm)
+        iterations, converged, deltas = 0, False, []
+        t_loop = time.perf_counter()
+        for it in range(1, cfg.max_outer_iterations + 1):
+            failure = None
+            try:
+                eng.phase_local()
+            except Exception as exc:       # reported consistently on every rank below
+                failure = exc
+            flag = self._allreduce_max([1.0 if failure is not None else 0.0])[0]
+            if flag:
+                raise failure if failure is not None else SolverError(
+                    "an area interior block on another rank is not positive definite; "
+                    "that area is likely locally unobservable")
+            eng.sync()
+            self._gather_blocks()
+            failure = None
+            if self.rank == 0 and self.n_gamma:
+                try:
+                    eng.phase_boundary()
+                except Exception as exc:
+                    failure = exc
+            flag = self._allreduce_max([1.0 if failure is not None else 0.0])[0]
+            if flag:
+                raise failure if failure is not None else SolverError(
+                    "boundary system not positive definite (reported by the coordinator rank)")
+            if self.world > 1 and self.n_gamma:
+                eng.sync()
+                self.dist.broadcast(eng.delta, src=0, group=self.group)
+            local_delta = eng.phase_recover()
+            delta = self._allreduce_max([local_delta])[0]
+            iterations = it
+            deltas.append(delta)
+            if on_iteration is not None:
+                on_iteration(it, self._full_state(), delta)
+            if delta < cfg.convergence_tol:
+                converged = True
+                break
+        self.last_gpu_s = time.perf_counter() - t_loop
+        state = self._full_state(load_back=True)
+        j = eng.objective()
+        self.last_deltas = deltas
+        timings = {p: 0.0 for p in PHASES}
+        timings["total"] = time.perf_counter() - t_start
+        report = SolveReport(method="multiarea", iterations=iterations, converged=converged,
+                             objective=float(j), weighted_residual_norm=float(np.sqrt(j)),
+                             n_gamma=self.n_gamma, timings=timings)
+        return state, report
+
+    def _full_state(self, load_back=False):
+        """Every rank's interior slice merged (SUM all-reduce of disjoint masks); the boundary
+        replica and the pinned slack come from the coordinator's copy."""
+        eng, torch = self.engine, self.torch
+        st = eng.state.clone()
+        if self.world > 1:
+            keep = eng.owned_mask if self.rank else torch.ones_like(eng.owned_mask)
+            if self.rank == 0:
+                # rank 0 contributes its interiors + everything that is not an interior of another rank
+                other = torch.zeros_like(eng.owned_mask)
+                other[torch.from_numpy(self._foreign_interiors()).to(other.device)] = True
+                keep = ~other
+            st = st * keep.to(st.dtype)
+            self.dist.all_reduce(st, op=self.dist.ReduceOp.SUM, group=self.group)
+            if load_back:
+                eng.state.copy_(st)
+        arr = st.cpu().numpy()
+        return StateVector(va=arr[0].copy(), vm=arr[1].copy())
+
+    def _foreign_interiors(self):
+        idx = [m.internal_buses for a, m in enumerate(self.maps) if self.area_rank[a] != 0]
+        return np.concatenate(idx).astype(np.int64) if idx else np.zeros(0, dtype=np.int64)
+
+    def close(self):
+        self.engine.close()

@@ -109,12 +109,6 @@ def tile_partition(base_area_of_bus, copies):
     return np.concatenate([base + c * k for c in range(copies)])
 
 
-def interval_partition(n_bus, k):
-    """Contiguous index intervals (valid for ``random_network`` grids, whose
-    spanning tree links every bus to one of its four predecessors)."""
-    return (np.arange(n_bus) * k) // n_bus
-
-
 def golden_partition(name):
     """Committed ``area_of_bus`` produced once by the reference partitioner
     (``tests/golden/make_golden.py``); None when no fixture exists."""
