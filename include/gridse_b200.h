@@ -65,7 +65,7 @@ typedef struct {
 typedef struct {
     int32_t device;          /* CUDA device ordinal                                        */
     int32_t backend_dense;   /* 1: SolverConfig.backend == "dense" (solver.py:49,61-63)    */
-    int32_t leaf_buses;      /* nested-dissection leaf size in buses (0 = default 12)       */
+    int32_t leaf_buses;      /* nested-dissection leaf size in buses (0 = default 48)       */
     int32_t max_pivots;      /* front pivot-block width, 32 or 64 (0 = default 64)          */
     int32_t rank, world;     /* area sharding: this process / number of processes           */
     const int32_t *area_rank;/* [n_areas] owner rank per area, NULL = all on rank 0          */

@@ -605,12 +605,12 @@ void* gse_stream(gse_plan* plan) { return (void*)plan->stream; }
 int gse_debug_task_clocks(gse_plan* plan, int enable, long long* out, int64_t max_n) {
     CU(cudaSetDevice(plan->device));
     if (enable) {
-        if (!plan->tbuf.ptr) CU(plan->tbuf.alloc(plan->tasks.n * 8 + 8));
+        if (!plan->tbuf.ptr) CU(plan->tbuf.alloc(plan->tasks.n * 32 + 32));
         plan->ft.tbuf = plan->tbuf.ptr;
         if (plan->graph) { cudaGraphExecDestroy(plan->graph); plan->graph = nullptr; }
         return (int)plan->tasks.n;
     }
-    if (out && plan->tbuf.ptr) CU(cudaMemcpy(out, plan->tbuf.ptr, sizeof(long long) * std::min<int64_t>(max_n, plan->tasks.n * 8), cudaMemcpyDeviceToHost));
+    if (out && plan->tbuf.ptr) CU(cudaMemcpy(out, plan->tbuf.ptr, sizeof(long long) * std::min<int64_t>(max_n, plan->tasks.n * 32), cudaMemcpyDeviceToHost));
     plan->ft.tbuf = nullptr;
     if (plan->graph) { cudaGraphExecDestroy(plan->graph); plan->graph = nullptr; }
     return (int)plan->tasks.n;

@@ -26,35 +26,106 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// child update block rows [r0,r1) x cols [c0,c1) (lower part) -> dst[(srow[i-r0]-rs)*ld + scol[j-c0]-cs]
-// srow / scol: the child's rel map for these ranges, staged in shared memory.  One warp per child
-// row (packed rows are contiguous -> coalesced), eight rows in flight per warp: the loop is L2-
-// latency bound, so memory-level parallelism is what matters.
-__device__ __forceinline__ void add_child_block(const double* __restrict__ U, const int* __restrict__ srow,
-                                                const int* __restrict__ scol, int r0, int r1, int c0, int c1,
-                                                double* dst, int ld, int rs, int cs, int warp, int lane, int nwarps) {
-    if (c1 <= c0 || r1 <= r0) return;
-    constexpr int kRows = 8;
-    for (int ib = r0 + warp; ib < r1; ib += kRows * nwarps) {
-        for (int jb = c0; jb < c1; jb += 32) {
-            const int j = jb + lane;
-            double v[kRows];
-            bool ok[kRows];
+// Extend-add as a GATHER: every destination entry of the task's shared-memory panels / tile is
+// owned by one thread, which adds the contributions of the children in child order.  No barrier
+// between children, no read-modify-write chains, and the loads of all children of a batch are in
+// flight together -- the phase costs a few L2 latencies instead of several per child.
+// inv[c][panel row] = row of child c that maps there (or -1), built from the child's rel map.
+constexpr int kInvRows = 64 + 2 * kMaxTile;
+constexpr int kGatherBatch = 4;
+
+struct GatherArgs {
+    double* pan; double* tile; const int* inv; const double* ubuf;
+    int p, ld, ldt, rp, Rp, ni, nj, diag, direct, warp, lane, nwarps;
+};
+
+// NB children of one batch, compile-time so that empty child slots cost no instructions
+template <int NB>
+__device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec* __restrict__ crec) {
+    const int p = a.p, ld = a.ld, ldt = a.ldt, rp = a.rp, Rp = a.Rp, ni = a.ni, nj = a.nj;
+    const int warp = a.warp, lane = a.lane, nwarps = a.nwarps;
+    const double* Ub[NB];
 #pragma unroll
-            for (int q = 0; q < kRows; ++q) {
-                const int i = ib + q * nwarps;
-                ok[q] = i < r1 && j < c1 && j <= i;
-                v[q] = ok[q] ? __ldg(U + (size_t)i * (i + 1) / 2 + j) : 0.0;
+    for (int c = 0; c < NB; ++c) Ub[c] = a.ubuf + crec[c].u_off;
+    // panel rows [pivots | I | J] x pivot columns
+    if (p) {
+        for (int Rb = warp; Rb < Rp; Rb += 4 * nwarps) {
+            double v[NB][8];
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+                const int* inv = a.inv + c * kInvRows;
+                int ic[2];
+#pragma unroll
+                for (int cp = 0; cp < 2; ++cp) { const int C = lane + 32 * cp; ic[cp] = C < p ? inv[C] : -1; }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int R = Rb + g * nwarps;
+                    const int ir = R < Rp ? inv[R] : -1;
+                    const int irc = ir > 0 ? ir : 0;
+                    const double* row = Ub[c] + (size_t)irc * (irc + 1) / 2;
+#pragma unroll
+                    for (int cp = 0; cp < 2; ++cp)
+                        v[c][2 * g + cp] = (ir >= 0 && ic[cp] >= 0 && ic[cp] <= ir) ? __ldg(row + ic[cp]) : 0.0;
+                }
             }
-            const int tc = j < c1 ? scol[j - c0] - cs : 0;
 #pragma unroll
-            for (int q = 0; q < kRows; ++q)
-                if (ok[q]) dst[(srow[ib + q * nwarps - r0] - rs) * ld + tc] += v[q];
+            for (int g = 0; g < 4; ++g) {
+                const int R = Rb + g * nwarps;
+#pragma unroll
+                for (int cp = 0; cp < 2; ++cp) {
+                    const int C = lane + 32 * cp;
+                    if (R < Rp && C < p) {
+                        double acc = a.pan[R * ld + C];
+#pragma unroll
+                        for (int c = 0; c < NB; ++c) acc += v[c][2 * g + cp];
+                        a.pan[R * ld + C] = acc;
+                    }
+                }
+            }
+        }
+    }
+    // tile: rows of chunk I x rows of chunk J
+    if (!a.direct) {
+        const int irow0 = rp, jrow0 = a.diag ? rp : rp + round8(ni);   // index of tile row / column 0 in inv
+        for (int Cb = 0; Cb < nj; Cb += 64) {
+            for (int Rb = warp; Rb < ni; Rb += 4 * nwarps) {
+                double v[NB][8];
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    const int* inv = a.inv + c * kInvRows;
+                    int ic[2];
+#pragma unroll
+                    for (int cp = 0; cp < 2; ++cp) { const int C = Cb + lane + 32 * cp; ic[cp] = C < nj ? inv[jrow0 + C] : -1; }
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const int R = Rb + g * nwarps;
+                        const int ir = R < ni ? inv[irow0 + R] : -1;
+                        const int irc = ir > 0 ? ir : 0;
+                        const double* row = Ub[c] + (size_t)irc * (irc + 1) / 2;
+#pragma unroll
+                        for (int cp = 0; cp < 2; ++cp)
+                            v[c][2 * g + cp] = (ir >= 0 && ic[cp] >= 0 && ic[cp] <= ir) ? __ldg(row + ic[cp]) : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int R = Rb + g * nwarps;
+#pragma unroll
+                    for (int cp = 0; cp < 2; ++cp) {
+                        const int C = Cb + lane + 32 * cp;
+                        if (R < ni && C < nj) {
+                            double acc = a.tile[R * ldt + C];
+#pragma unroll
+                            for (int c = 0; c < NB; ++c) acc += v[c][2 * g + cp];
+                            a.tile[R * ldt + C] = acc;
+                        }
+                    }
+                }
+            }
         }
     }
 }
 
-constexpr int kStage = 64 + 2 * kMaxTile + 16;   // staged rel entries of one child: pivots + I + J ranges
 constexpr int kChildBatch = 32;
 
 template <int HAS_PIVOTS>
@@ -64,11 +135,11 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(16) TaskRec hdr;
     __shared__ __align__(16) ChildRec crec[kChildBatch];
-    __shared__ int s_rel[2][kStage];
+    __shared__ int s_inv[kGatherBatch][kInvRows];
     __shared__ double s_ld[48];           // published 8x8 diagonal factor (36) + reciprocal pivots (8)
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
-    long long* tb = ft.tbuf ? ft.tbuf + 8 * ((&tasks[blockIdx.x]) - (const TaskRec*)ft.task0) : nullptr;
+    long long* tb = ft.tbuf ? ft.tbuf + 32 * ((&tasks[blockIdx.x]) - (const TaskRec*)ft.task0) : nullptr;
 #define GSE_TICK(k) do { if (tb && tid == 0) tb[k] = clock64(); } while (0)
     GSE_TICK(0);
     if (tid < (int)(sizeof(TaskRec) / 16))
@@ -128,40 +199,42 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
     __syncthreads();
     GSE_TICK(2);
 
-    // ---- extend-add of the children's update matrices, fixed child order --------------------
+    // ---- extend-add of the children's update matrices, fixed child order (gather form) -------
     // (the child list of a task is pruned on the host to the children that reach its regions)
-    for (int cb0 = 0; cb0 < nchild; cb0 += kChildBatch) {
-        const int nb = min(kChildBatch, nchild - cb0);
-        if (cb0) {
+    for (int cb0 = 0; cb0 < nchild; cb0 += kGatherBatch) {
+        const int nb = min(kGatherBatch, nchild - cb0);
+        const int Rp = rp + ri + rj;
+        if (cb0 && (cb0 % kChildBatch) == 0) {          // next page of child records
             __syncthreads();
-            if (tid < 2 * nb) reinterpret_cast<int4*>(crec)[tid] = reinterpret_cast<const int4*>(ft.crecs + hdr.child_off + cb0)[tid];
-            __syncthreads();
+            if (tid < 2 * min(kChildBatch, nchild - cb0))
+                reinterpret_cast<int4*>(crec)[tid] = reinterpret_cast<const int4*>(ft.crecs + hdr.child_off + cb0)[tid];
         }
-        auto stage = [&](int c, int buf) {   // rel slices [0,eP) | [bI,eI) | [bJ,eJ) of child c
-            const ChildRec& cr = crec[c];
-            const int32_t* rel = ft.rel + cr.rel_off;
-            const int eP = cr.eP, nI = cr.eI - cr.bI, nJ = cr.eJ - cr.bJ;
-            for (int t = tid; t < eP + nI + nJ; t += nth)
-                s_rel[buf][t] = t < eP ? rel[t] : t < eP + nI ? rel[cr.bI + t - eP] : rel[cr.bJ + t - eP - nI];
-        };
-        stage(0, 0);
         __syncthreads();
+        for (int t = tid; t < kGatherBatch * kInvRows; t += nth) (&s_inv[0][0])[t] = -1;
+        __syncthreads();
+        const int cbase = cb0 % kChildBatch;
         for (int c = 0; c < nb; ++c) {
-            const ChildRec cr = crec[c];
-            const int buf = c & 1;
-            if (c + 1 < nb) stage(c + 1, buf ^ 1);          // overlaps with this child's loads
-            const double* U = ubuf + cr.u_off;
-            const int eP = cr.eP, bI = cr.bI, eI = cr.eI, bJ = cr.bJ, eJ = cr.eJ;
-            const int* sP = s_rel[buf]; const int* sI = sP + eP; const int* sJ = sI + (eI - bI);
-            if (p) {
-                add_child_block(U, sP, sP, 0, eP, 0, eP, pan, ld, 0, 0, warp, lane, nwarps);
-                add_child_block(U, sI, sP, bI, eI, 0, eP, pan + (size_t)rp * ld, ld, p + i0, 0, warp, lane, nwarps);
-                if (!diag) add_child_block(U, sJ, sP, bJ, eJ, 0, eP, pan + (size_t)(rp + ri) * ld, ld, p + j0, 0, warp, lane, nwarps);
+            const ChildRec& cr = crec[cbase + c];
+            const int32_t* rel = ft.rel + cr.rel_off;
+            const int eP = p ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = diag ? 0 : cr.eJ - cr.bJ;
+            for (int t = tid; t < eP + nI + nJ; t += nth) {
+                if (t < eP) s_inv[c][rel[t]] = t;
+                else if (t < eP + nI) { const int i = cr.bI + t - eP; s_inv[c][rp + rel[i] - p - i0] = i; }
+                else { const int i = cr.bJ + t - eP - nI; s_inv[c][rp + round8(ni) + rel[i] - p - j0] = i; }
             }
-            if (!direct) add_child_block(U, sI, sJ, bI, eI, bJ, eJ, tile, ldt, p + i0, p + j0, warp, lane, nwarps);
-            __syncthreads();
+        }
+        __syncthreads();
+        if (cb0 == 0) GSE_TICK(7);
+        GatherArgs ga{pan, tile, &s_inv[0][0], ubuf, p, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, direct ? 1 : 0, warp, lane, nwarps};
+        const ChildRec* cb = crec + cbase;
+        switch (nb) {
+            case 1: gather_batch<1>(ga, cb); break;
+            case 2: gather_batch<2>(ga, cb); break;
+            case 3: gather_batch<3>(ga, cb); break;
+            default: gather_batch<4>(ga, cb); break;
         }
     }
+    __syncthreads();
     GSE_TICK(3);
 
     // ---- blocked panel factorisation (block = 8 columns) ---------------------------------------

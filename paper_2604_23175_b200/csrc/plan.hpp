@@ -88,7 +88,7 @@ struct HostProgram {
 
 struct BuildOptions {
     bool dense = false;
-    int leaf_buses = 12;
+    int leaf_buses = 48;   // measured best on the PEGASE-9241 shape (tools/gpu_leaf.sh: 12 -> 4.2 ms, 48 -> 3.25 ms per solve)
     int max_pivots = 64;
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;

@@ -36,9 +36,9 @@ L.gse_debug_task_clocks.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
 nt = L.gse_debug_task_clocks(est.plan._h, 1, None, 0)
 est._load_flat_start(); est.torch.cuda.synchronize()
 L.gse_profile_iteration(est.plan._h, va, vm, N, kind.ctypes.data_as(_native.i32p), ph.ctypes.data_as(_native.i32p), ct.ctypes.data_as(_native.i32p), us.ctypes.data_as(_native.f64p))
-clk = np.zeros(nt * 8, dtype=np.int64)
-L.gse_debug_task_clocks(est.plan._h, 0, clk.ctypes.data_as(C.c_void_p), nt * 8)
-clk = clk.reshape(nt, 8)
+clk = np.zeros(nt * 32, dtype=np.int64)
+L.gse_debug_task_clocks(est.plan._h, 0, clk.ctypes.data_as(C.c_void_p), nt * 32)
+clk = clk.reshape(nt, 32)
 d = np.diff(clk[:, :7], axis=1)   # zero, orig, children, panel, dmma, store
 labels = ["zero", "orig", "extend-add", "panel", "dmma", "Lstore"]
 # tasks are laid out launch by launch in the same order as the front launches above
@@ -51,4 +51,8 @@ for i in range(n):
     tot = blk.sum(axis=1)
     w = int(np.argmax(tot))
     print(f"launch {i:2d} ctas {ct[i]:4d} slowest {tot[w]:7d} cyc: " + " ".join(f"{l}={v}" for l, v in zip(labels, blk[w])) + f" | median total {int(np.median(tot))}")
+    if ct[i] <= 8 or i in (3, 17):
+        row = clk[pos + w]
+        ch = [(int(row[8 + 2 * c] - (row[7] if c == 0 else row[7 + 2 * c])), int(row[9 + 2 * c] - row[8 + 2 * c])) for c in range(12) if row[8 + 2 * c] > 0 and row[9 + 2 * c] >= row[8 + 2 * c]]
+        print(f"      stage0={int(row[7] - row[2])} children (add, wait+sync): {ch}")
     pos += ct[i]
