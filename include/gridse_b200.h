@@ -71,6 +71,7 @@ typedef struct {
     const int32_t *area_rank;/* [n_areas] owner rank per area, NULL = all on rank 0          */
     int32_t persistent;      /* reserved (dataflow scheduler)                               */
     int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default 48) */
+    int32_t boundary_mode;   /* boundary factorisation: 0 auto, 1 dense chain (dense_cholesky_solve), 2 block-sparse tree */
 } gse_options;
 
 typedef struct {

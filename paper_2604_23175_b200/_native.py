@@ -47,6 +47,7 @@ class Options(C.Structure):
         ("device", C.c_int32), ("backend_dense", C.c_int32), ("leaf_buses", C.c_int32),
         ("max_pivots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("area_rank", i32p), ("persistent", C.c_int32), ("tile_rows", C.c_int32),
+        ("boundary_mode", C.c_int32),
     ]
 
 
@@ -215,7 +216,7 @@ class Plan:
     """Owner of one ``gse_plan`` (analysis + device program of one problem)."""
 
     def __init__(self, net, ms, part, bord, maps, *, device=0, dense=False, leaf_buses=0,
-                 max_pivots=0, rank=0, world=1, area_rank=None, tile_rows=0):
+                 max_pivots=0, rank=0, world=1, area_rank=None, tile_rows=0, boundary_mode=0):
         L = lib()
         self._desc, self._keep = make_desc(net, ms, part, bord, maps)
         opt = Options()
@@ -223,6 +224,7 @@ class Plan:
         opt.leaf_buses, opt.max_pivots = int(leaf_buses), int(max_pivots)
         opt.rank, opt.world = int(rank), int(world)
         opt.tile_rows = int(tile_rows)
+        opt.boundary_mode = int(boundary_mode)
         if area_rank is not None:
             self._keep["area_rank"] = np.ascontiguousarray(area_rank, dtype=np.int32)
             opt.area_rank = _ip(self._keep["area_rank"])

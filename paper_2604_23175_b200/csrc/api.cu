@@ -227,10 +227,13 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
         if (opt->max_pivots == 32 || opt->max_pivots == 64) bo.max_pivots = opt->max_pivots;
         if (opt->tile_rows >= 8 && opt->tile_rows <= kMaxTile) bo.tile_rows = opt->tile_rows / 8 * 8;
+        if (opt->boundary_mode >= 0 && opt->boundary_mode <= 2) bo.boundary_mode = opt->boundary_mode;
         bo.rank = opt->rank; bo.world = std::max(1, opt->world);
         if (opt->area_rank) bo.area_rank.assign(opt->area_rank, opt->area_rank + d->n_areas);
     }
     if (const char* e = getenv("GSE_TILE_ROWS")) { int v = atoi(e); if (v >= 8 && v <= kMaxTile) bo.tile_rows = v / 8 * 8; }
+    if (const char* e = getenv("GSE_BOUNDARY")) { int v = atoi(e); if (v >= 0 && v <= 2) bo.boundary_mode = v; }
+    if (const char* e = getenv("GSE_GAMMA_LEAF")) { int v = atoi(e); if (v >= 1) bo.gamma_leaf_buses = v; }
     if (const char* e = getenv("GSE_LEAF_BUSES")) { int v = atoi(e); if (v >= 1) bo.leaf_buses = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;
@@ -290,18 +293,9 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         frows_off[i] = (int)rows.size(); rows.insert(rows.end(), f.rows.begin(), f.rows.end());
         fg[i] = f.gval_off; fl[i] = f.l_off; fuo[i] = f.u_off;
     }
-    // lower bounds of every child's rel map at the parent's pivot edge and chunk edges
-    std::vector<int32_t> cb_off(children.size(), 0), cbounds;
-    for (size_t i = 0; i < nf; ++i) {
-        const Front& f = hp.fronts[i];
-        for (size_t c = 0; c < f.children.size(); ++c) {
-            const std::vector<int>& rel_c = hp.fronts[f.children[c]].rel;
-            auto lb = [&](int key) { return (int32_t)(std::lower_bound(rel_c.begin(), rel_c.end(), key) - rel_c.begin()); };
-            cb_off[fcp[i] + c] = (int32_t)cbounds.size();
-            cbounds.push_back(lb(f.p));
-            for (int q = 0; q <= f.nch; ++q) cbounds.push_back(lb(f.p + q * std::max(f.T, 1)));
-        }
-    }
+    std::vector<int32_t> extra_rel_off(hp.extra_rel.size(), 0);
+    for (size_t i = 0; i < hp.extra_rel.size(); ++i) { extra_rel_off[i] = (int32_t)rel.size(); rel.insert(rel.end(), hp.extra_rel[i].begin(), hp.extra_rel[i].end()); }
+    std::vector<int32_t> cb_off(1, 0), cbounds(1, 0);   // (kept for the table layout; bounds now live in ChildRec)
     CU(plan->f_cb_off.upload(cb_off)); CU(plan->f_cbounds.upload(cbounds));
     CU(plan->f_p.upload(fp)); CU(plan->f_u1.upload(fu)); CU(plan->f_T.upload(fT)); CU(plan->f_nchild.upload(fnc));
     CU(plan->f_child_ptr.upload(fcp)); CU(plan->f_children.upload(children)); CU(plan->f_rel_off.upload(frel_off));
@@ -321,12 +315,13 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     std::vector<TaskRec> trecs;
     std::vector<ChildRec> crecs;
     for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
-        for (int pclass : {1, 0}) {
-            LevelLaunch L{pclass, (int)trecs.size(), 0, 0, hp.level_phase[lv]};
+        for (int key : {11, 10, 21, 20, 31, 30, 51, 50}) {      // (phase, pivot class)
+            const int phase = key / 10, pclass = key % 10;
+            LevelLaunch L{pclass, (int)trecs.size(), 0, 0, phase};
             for (const Task& t : hp.fwd_levels[lv]) {
                 const Front& f = hp.fronts[t.front];
                 const int cls = f.p == 0 ? 0 : 1;
-                if (cls != pclass) continue;
+                if (cls != pclass || t.phase != phase) continue;
                 const int T = std::max(f.T, 1);
                 const int ni = std::min(T, f.u1 - t.ci * T), nj = std::min(T, f.u1 - t.cj * T);
                 const bool diag = t.ci == t.cj;
@@ -347,11 +342,14 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 r.reg[4] = rp[ridJ]; r.reg[5] = rp[ridJ + 1];
                 r.reg[6] = rp[ridI + t.cj + 1]; r.reg[7] = rp[ridI + t.cj + 2];
                 r.child_off = (int32_t)crecs.size();
-                for (int ch : f.children) {
+                for (size_t cx = 0; cx < f.children.size(); ++cx) {
+                    const int ch = f.children[cx];
                     const Front& c = hp.fronts[ch];
-                    auto lb = [&](int key) { return (int32_t)(std::lower_bound(c.rel.begin(), c.rel.end(), key) - c.rel.begin()); };
+                    const bool over = cx < f.child_rel.size() && f.child_rel[cx] >= 0;
+                    const std::vector<int>& relv = over ? hp.extra_rel[f.child_rel[cx]] : c.rel;
+                    auto lb = [&](int key2) { return (int32_t)(std::lower_bound(relv.begin(), relv.end(), key2) - relv.begin()); };
                     ChildRec cr{};
-                    cr.u_off = c.u_off; cr.rel_off = frel_off[ch];
+                    cr.u_off = c.u_off; cr.rel_off = over ? extra_rel_off[f.child_rel[cx]] : frel_off[ch];
                     cr.eP = f.p ? lb(f.p) : 0;
                     cr.bI = lb(f.p + t.ci * T); cr.eI = lb(f.p + t.ci * T + ni);
                     cr.bJ = lb(f.p + t.cj * T); cr.eJ = lb(f.p + t.cj * T + nj);
@@ -503,7 +501,7 @@ int gse_phase_condense(gse_plan* plan) {
 int gse_phase_boundary(gse_plan* plan) {
     CU(cudaSetDevice(plan->device));
     if (!plan->coordinator) return GSE_OK;
-    enqueue_fwd(plan, 2); enqueue_fwd(plan, 3); enqueue_bwd(plan, 3);
+    enqueue_fwd(plan, 2); enqueue_fwd(plan, 5); enqueue_fwd(plan, 3); enqueue_bwd(plan, 3);
     return gse_check(plan);
 }
 int gse_phase_recover(gse_plan* plan, double* va, double* vm, double* delta_inf) {
@@ -550,27 +548,31 @@ int gse_area_blocks(gse_plan* plan, int32_t a, double* data_ii, double* data_ib,
     CU(cudaMemcpy(b_b, base + nii + nib + nb * nb + ni, nb * 8, cudaMemcpyDeviceToHost));
     return GSE_OK;
 }
-static int unpack_lower(gse_plan* plan, const Front& f, int n, double* full, double* rhs) {
+// packed lower (rows in front order) -> full symmetric in the caller's order; pos[i] = front row of item i
+static int unpack_lower(gse_plan* plan, const Front& f, int n, const std::vector<int>& pos, double* full, double* rhs) {
     std::vector<double> packed((size_t)f.u1 * (f.u1 + 1) / 2);
     cudaError_t e = cudaMemcpy(packed.data(), plan->ubuf.ptr + f.u_off, packed.size() * 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(plan, GSE_E_CUDA, cudaGetErrorString(e));
     for (int i = 0; i < n; ++i)
-        for (int j = 0; j <= i; ++j) { double v = packed[(size_t)i * (i + 1) / 2 + j]; full[(size_t)i * n + j] = v; full[(size_t)j * n + i] = v; }
-    for (int j = 0; j < n; ++j) rhs[j] = packed[(size_t)n * (n + 1) / 2 + j];
+        for (int j = 0; j < n; ++j) {
+            const int qi = std::max(pos[i], pos[j]), qj = std::min(pos[i], pos[j]);
+            full[(size_t)i * n + j] = packed[(size_t)qi * (qi + 1) / 2 + qj];
+        }
+    for (int j = 0; j < n; ++j) rhs[j] = packed[(size_t)n * (n + 1) / 2 + pos[j]];
     return GSE_OK;
 }
 int gse_area_schur(gse_plan* plan, int32_t a, double* s_b, double* b_hat) {
     const HostProgram& hp = plan->hp;
     if (a < 0 || a >= hp.n_areas) return GSE_E_INVALID;
     CU(cudaSetDevice(plan->device));
-    return unpack_lower(plan, hp.fronts[hp.area_root[a]], hp.area_nb[a], s_b, b_hat);
+    return unpack_lower(plan, hp.fronts[hp.area_root[a]], hp.area_nb[a], hp.area_bpos[a], s_b, b_hat);
 }
 int gse_boundary_system(gse_plan* plan, double* s_gamma, double* b_gamma, double* dx_gamma) {
     const HostProgram& hp = plan->hp;
     CU(cudaSetDevice(plan->device));
     if (hp.n_gamma == 0) return GSE_OK;
     if (hp.gamma_root < 0) return fail(plan, GSE_E_INVALID, "boundary system lives on the coordinator rank");
-    int rc = unpack_lower(plan, hp.fronts[hp.gamma_root], hp.n_gamma, s_gamma, b_gamma);
+    int rc = unpack_lower(plan, hp.fronts[hp.gamma_root], hp.n_gamma, hp.gamma_sparse ? hp.gamma_epos : std::vector<int>(hp.gamma_epos), s_gamma, b_gamma);
     if (rc) return rc;
     CU(cudaMemcpy(dx_gamma, plan->xsol.ptr + hp.gamma_base, hp.n_gamma * 8, cudaMemcpyDeviceToHost));
     return GSE_OK;

@@ -29,12 +29,13 @@ struct Front {
     int T = 0, nch = 0;     // update-row chunking
     std::vector<int> rows;  // global positions of [pivots | update rows] (RHS row not listed)
     std::vector<int> children;
+    std::vector<int> child_rel;   // optional, parallel to children: index into HostProgram::extra_rel (else the child's own rel)
     std::vector<int> rel;   // as a child: update row i -> local row of the parent
     int64_t l_off = 0, u_off = 0, gval_off = 0;
     int n_orig = 0;
 };
 
-struct Task { int front, ci, cj; };
+struct Task { int front, ci, cj, phase; };
 
 struct HostProgram {
     // sizes
@@ -45,6 +46,10 @@ struct HostProgram {
     std::vector<int> area_base;          // first interior position of each area
     std::vector<int> area_ni, area_nb;
     std::vector<int> owned;              // 1 if this rank assembles / factors the area
+    bool gamma_sparse = false;           // boundary system factored as a tree (block sparsity) instead of a dense chain
+    std::vector<int> gamma_epos;         // x_Gamma slot -> elimination rank (identity in dense mode)
+    std::vector<std::vector<int>> area_bpos;   // per area: local boundary variable -> row of the area root
+    std::vector<std::vector<int>> extra_rel;   // rel maps that are not a front's own (boundary-root readback)
     int rank = 0, world = 1;
 
     // template evaluation units
@@ -90,6 +95,8 @@ struct BuildOptions {
     bool dense = false;
     int leaf_buses = 48;   // measured best on the PEGASE-9241 shape (tools/gpu_leaf.sh: 12 -> 4.2 ms, 48 -> 3.25 ms per solve)
     int max_pivots = 64;
+    int boundary_mode = 0;     // 0 auto (tree when n_Gamma > 192), 1 dense chain, 2 tree
+    int gamma_leaf_buses = 16; // nested-dissection leaf of the boundary tree, in boundary buses
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;

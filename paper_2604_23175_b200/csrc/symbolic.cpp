@@ -191,6 +191,62 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     hp.n_pos = pos_cursor + ng;
     hp.perm_orig.assign(hp.n_pos, -1);
 
+    // ---- elimination order of the boundary system -----------------------------------------
+    // dense mode: natural slot order, factored as a chain of dense fronts (the reference's
+    // dense_cholesky_solve).  sparse mode: nested dissection on the graph whose cliques are the
+    // areas' local boundary sets -- the same Cholesky factorisation of the same S_Gamma, but
+    // the structural zeros between non-adjacent areas are never touched.
+    const bool sparse_gamma = ng > 0 && (opt.boundary_mode == 2 || (opt.boundary_mode == 0 && ng > 192));
+    hp.gamma_sparse = sparse_gamma;
+    hp.gamma_epos.resize(ng);
+    std::iota(hp.gamma_epos.begin(), hp.gamma_epos.end(), 0);
+    std::vector<std::vector<int>> gamma_nodes;     // per ND node: the x_Gamma slots it eliminates
+    if (sparse_gamma) {
+        std::vector<int> node_of_bus(nbus, -1), ang_slot, mag_slot, node_bus;
+        for (int s = 0; s < ng; ++s) if (d.gamma_quant[s] == 1) {
+            node_of_bus[d.gamma_bus[s]] = (int)node_bus.size(); node_bus.push_back(d.gamma_bus[s]);
+            mag_slot.push_back(s); ang_slot.push_back(-1);
+        }
+        for (int s = 0; s < ng; ++s) if (d.gamma_quant[s] == 0) ang_slot[node_of_bus[d.gamma_bus[s]]] = s;
+        const int nn = (int)node_bus.size();
+        std::vector<int64_t> edges;
+        for (int a = 0; a < K; ++a)
+            for (int i = d.bm_ptr[a]; i < d.bm_ptr[a + 1]; ++i)
+                for (int j = d.bm_ptr[a]; j < d.bm_ptr[a + 1]; ++j)
+                    if (i != j) edges.push_back((int64_t)node_of_bus[d.bm_bus[i]] * nn + node_of_bus[d.bm_bus[j]]);
+        std::sort(edges.begin(), edges.end()); edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+        NDGraph g;
+        g.xadj.assign(nn + 1, 0); g.adj.resize(edges.size());
+        for (size_t i = 0; i < edges.size(); ++i) { g.xadj[edges[i] / nn + 1]++; g.adj[i] = (int)(edges[i] % nn); }
+        for (int i = 0; i < nn; ++i) g.xadj[i + 1] += g.xadj[i];
+        g.stamp.assign(nn, 0); g.level.assign(nn, 0);
+        std::vector<int> all(nn); std::iota(all.begin(), all.end(), 0);
+        std::vector<std::vector<int>> nodes;
+        nd_recurse(g, all, std::max(1, opt.gamma_leaf_buses), nodes);
+        int rank = 0;
+        for (auto& node : nodes) {
+            std::vector<int> slots;
+            for (int b : node) { if (ang_slot[b] >= 0) slots.push_back(ang_slot[b]); slots.push_back(mag_slot[b]); }
+            for (int s : slots) hp.gamma_epos[s] = rank++;
+            gamma_nodes.push_back(std::move(slots));
+        }
+        if (rank != ng) return "boundary ordering did not cover x_Gamma";
+    }
+    std::vector<int> gamma_slot_of_rank(ng);
+    for (int s = 0; s < ng; ++s) gamma_slot_of_rank[hp.gamma_epos[s]] = s;
+    // per area: local boundary variables in boundary elimination order (identity in dense mode)
+    hp.area_bpos.assign(K, {});
+    std::vector<std::vector<int>> bvar_of_pos(K);
+    for (int a = 0; a < K; ++a) {
+        const int nb = as[a].nb;
+        bvar_of_pos[a].resize(nb);
+        std::iota(bvar_of_pos[a].begin(), bvar_of_pos[a].end(), 0);
+        std::sort(bvar_of_pos[a].begin(), bvar_of_pos[a].end(), [&](int x, int y) {
+            return hp.gamma_epos[d.sel[d.sel_ptr[a] + x]] < hp.gamma_epos[d.sel[d.sel_ptr[a] + y]]; });
+        hp.area_bpos[a].resize(nb);
+        for (int q = 0; q < nb; ++q) hp.area_bpos[a][bvar_of_pos[a][q]] = q;
+    }
+
     // ---- rows per area -----------------------------------------------------------
     for (int r = 0; r < m; ++r) {
         int t = d.m_type[r], tg = d.m_target[r];
@@ -384,7 +440,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                     int v = hp.ii_idx[a][p];
                     if (A.epos[u] >= A.epos[v]) colrows[A.epos[v]].push_back(A.epos[u]);
                 }
-                for (int p = hp.ib_ptr[a][u]; p < hp.ib_ptr[a][u + 1]; ++p) colrows[A.epos[u]].push_back(ni + hp.ib_idx[a][p]);
+                for (int p = hp.ib_ptr[a][u]; p < hp.ib_ptr[a][u + 1]; ++p) colrows[A.epos[u]].push_back(ni + hp.area_bpos[a][hp.ib_idx[a][p]]);
             }
             if (opt.dense) for (int c = 0; c < ni; ++c) { colrows[c].clear(); for (int r = c; r < nloc; ++r) colrows[c].push_back(r); }
             for (int c = ni; c < nloc; ++c) for (int r = c; r < nloc; ++r) colrows[c].push_back(r);
@@ -405,7 +461,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         std::vector<int> mark(nloc, -1);
         // area root
         Front root; root.area = a; root.kind = 1; root.p = 0; root.u1 = nb + 1;
-        for (int j = 0; j < nb; ++j) root.rows.push_back(hp.gamma_base + d.sel[d.sel_ptr[a] + j]);
+        for (int q = 0; q < nb; ++q) root.rows.push_back(hp.gamma_base + d.sel[d.sel_ptr[a] + bvar_of_pos[a][q]]);
         const int root_id = A.first_front + A.n_fronts;
         A.root = root_id;
         std::vector<std::vector<int>> kids(A.n_fronts + 1);
@@ -423,7 +479,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 for (int r : structs[ch]) if (r >= e1 && mark[r] != fi) { mark[r] = fi; st.push_back(r); }
             std::sort(st.begin(), st.end());
             f.u1 = (int)st.size() + 1;
-            for (int r : st) f.rows.push_back(r < ni ? hp.area_base[a] + r : hp.gamma_base + d.sel[d.sel_ptr[a] + (r - ni)]);
+            for (int r : st) f.rows.push_back(r < ni ? hp.area_base[a] + r : hp.gamma_base + d.sel[d.sel_ptr[a] + bvar_of_pos[a][r - ni]]);
             int par = A.n_fronts;   // area root by default
             if (!st.empty() && st[0] < ni) par = A.front_of_pos[st[0]] - A.first_front;
             kids[par].push_back(fi);
@@ -516,7 +572,89 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
 
     // ---- coordinator fronts: boundary assembly root + dense factorisation chain -----
     const int first_coord = (int)hp.fronts.size();
-    if (ng > 0) {
+    if (ng > 0 && sparse_gamma) {
+        // rel of every area root into the boundary root (rows in boundary elimination order)
+        std::vector<std::vector<int>> root_rel(K);
+        for (int a = 0; a < K; ++a) {
+            root_rel[a].resize(as[a].nb + 1);
+            for (int q = 0; q < as[a].nb; ++q) root_rel[a][q] = hp.gamma_epos[d.sel[d.sel_ptr[a] + bvar_of_pos[a][q]]];
+            root_rel[a][as[a].nb] = ng;
+            hp.fronts[hp.area_root[a]].parent = -1;
+        }
+        if (coordinator) {
+            // boundary root: S_Gamma / b_Gamma for readback only (not part of the solve in this mode)
+            Front g; g.kind = 2; g.p = 0; g.u1 = ng + 1;
+            for (int q = 0; q < ng; ++q) g.rows.push_back(hp.gamma_base + gamma_slot_of_rank[q]);
+            for (int a = 0; a < K; ++a) { g.children.push_back(hp.area_root[a]); g.child_rel.push_back((int)hp.extra_rel.size()); hp.extra_rel.push_back(root_rel[a]); }
+            choose_chunks(g, opt.tile_rows);
+            hp.gamma_root = first_coord;
+            hp.fronts.push_back(std::move(g));
+            // fronts of the boundary tree: ND nodes cut into pieces of at most PMAX pivots
+            const int first_gf = (int)hp.fronts.size();
+            std::vector<int> front_of_rank(ng, -1), e_lo, e_hi;
+            for (auto& slots : gamma_nodes) {
+                const int nv = (int)slots.size(), pieces = (nv + PMAX - 1) / PMAX;
+                for (int q = 0; q < pieces; ++q) {
+                    const int lo = (int)((int64_t)nv * q / pieces), hi = (int)((int64_t)nv * (q + 1) / pieces);
+                    Front f; f.kind = 3; f.p = hi - lo;
+                    e_lo.push_back(hp.gamma_epos[slots[lo]]); e_hi.push_back(hp.gamma_epos[slots[lo]] + (hi - lo));
+                    for (int i = lo; i < hi; ++i) { front_of_rank[hp.gamma_epos[slots[i]]] = (int)hp.fronts.size(); f.rows.push_back(hp.gamma_base + slots[i]); }
+                    hp.fronts.push_back(std::move(f));
+                }
+            }
+            const int ngf = (int)hp.fronts.size() - first_gf;
+            // cliques (areas) containing each rank
+            std::vector<std::vector<int>> areas_of_rank(ng);
+            for (int a = 0; a < K; ++a) for (int q = 0; q < as[a].nb; ++q) areas_of_rank[root_rel[a][q]].push_back(a);
+            std::vector<std::vector<int>> gstruct(ngf), gkids(ngf);
+            std::vector<int> gmark(ng, -1);
+            for (int fi = 0; fi < ngf; ++fi) {
+                Front& f = hp.fronts[first_gf + fi];
+                std::vector<int>& st = gstruct[fi];
+                for (int e = e_lo[fi]; e < e_hi[fi]; ++e)
+                    for (int a : areas_of_rank[e])
+                        for (int q = 0; q < as[a].nb; ++q) { int r = root_rel[a][q]; if (r >= e_hi[fi] && gmark[r] != fi) { gmark[r] = fi; st.push_back(r); } }
+                for (int ch : gkids[fi]) for (int r : gstruct[ch]) if (r >= e_hi[fi] && gmark[r] != fi) { gmark[r] = fi; st.push_back(r); }
+                std::sort(st.begin(), st.end());
+                f.u1 = (int)st.size() + 1;
+                for (int r : st) f.rows.push_back(hp.gamma_base + gamma_slot_of_rank[r]);
+                if (!st.empty()) { int par = front_of_rank[st[0]] - first_gf; gkids[par].push_back(fi); f.parent = first_gf + par; }
+                choose_chunks(f, opt.tile_rows);
+            }
+            auto local_index = [&](int fi, int r) -> int {   // rank r inside front fi: pivots then update rows
+                if (r < e_hi[fi]) return r - e_lo[fi];
+                const std::vector<int>& st = gstruct[fi];
+                return hp.fronts[first_gf + fi].p + (int)(std::lower_bound(st.begin(), st.end(), r) - st.begin());
+            };
+            for (int fi = 0; fi < ngf; ++fi) {
+                Front& f = hp.fronts[first_gf + fi];
+                for (int ch : gkids[fi]) f.children.push_back(first_gf + ch);
+                if (f.parent >= 0) {
+                    const int par = f.parent - first_gf;
+                    f.rel.resize(f.u1);
+                    for (size_t i = 0; i < gstruct[fi].size(); ++i) f.rel[i] = local_index(par, gstruct[fi][i]);
+                    f.rel[f.u1 - 1] = hp.fronts[f.parent].p + hp.fronts[f.parent].u1 - 1;
+                }
+            }
+            // every area root enters the front of its first-eliminated boundary variable
+            for (int a = 0; a < K; ++a) {
+                Front& r = hp.fronts[hp.area_root[a]];
+                if (as[a].nb == 0) continue;
+                const int fi = front_of_rank[root_rel[a][0]] - first_gf;
+                r.parent = first_gf + fi;
+                r.rel.resize(r.u1);
+                for (int q = 0; q < as[a].nb; ++q) r.rel[q] = local_index(fi, root_rel[a][q]);
+                r.rel[r.u1 - 1] = hp.fronts[r.parent].p + hp.fronts[r.parent].u1 - 1;
+                // children stay in area order: the reference's summation order of assemble_boundary
+                hp.fronts[r.parent].children.push_back(hp.area_root[a]);
+            }
+            for (int fi = 0; fi < ngf; ++fi) {   // area roots first (area order), then boundary-tree children
+                Front& f = hp.fronts[first_gf + fi];
+                std::stable_sort(f.children.begin(), f.children.end(), [&](int x, int y) {
+                    return (hp.fronts[x].kind == 1) > (hp.fronts[y].kind == 1); });
+            }
+        }
+    } else if (ng > 0) {
         for (int a = 0; a < K; ++a) {
             Front& r = hp.fronts[hp.area_root[a]];
             r.parent = first_coord;
@@ -590,13 +728,20 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         if (f.kind == 1) f.level = root_level;
         else if (f.kind == 2) { f.level = root_level + 1; n_levels = std::max(n_levels, f.level + 1); }
     }
-    { int k = 0; for (auto& f : hp.fronts) if (f.kind == 3) { f.level = root_level + 2 + k++; n_levels = std::max(n_levels, f.level + 1); } }
+    // boundary fronts (chain or tree): one level above their deepest child
+    for (auto& f : hp.fronts) if (f.kind == 3) {
+        int lv = root_level + 1;
+        for (int c : f.children) lv = std::max(lv, hp.fronts[c].level + 1);
+        f.level = lv; n_levels = std::max(n_levels, lv + 1);
+    }
     hp.fwd_levels.assign(n_levels, {}); hp.level_phase.assign(n_levels, 1);
     for (size_t fi = 0; fi < hp.fronts.size(); ++fi) {
         Front& f = hp.fronts[fi];
         if (f.area >= 0 && !hp.owned[f.area]) continue;
-        for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj});
-        hp.level_phase[f.level] = f.kind <= 1 ? 1 : f.kind;
+        // phase 1 local_condense, 2 boundary_assemble, 3 boundary_solve, 5 readback-only boundary root
+        const int phase = f.kind <= 1 ? 1 : f.kind == 2 ? (sparse_gamma ? 5 : 2) : 3;
+        for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj, phase});
+        hp.level_phase[f.level] = phase;
     }
     for (auto& lv : hp.fwd_levels)
         std::stable_sort(lv.begin(), lv.end(), [&](const Task& x, const Task& y) {
@@ -620,7 +765,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             if (!hp.owned[a]) continue;
             AreaSym& A = as[a];
             const int ni = A.ni, nloc = A.ni + A.nb;
-            auto lp = [&](int v) { return v < ni ? A.epos[v] : v; };
+            auto lp = [&](int v) { return v < ni ? A.epos[v] : ni + hp.area_bpos[a][v - ni]; };
             auto find = [&](int c, int r) -> int64_t {
                 auto b = A.col_row.begin() + A.col_ptr[c], e = A.col_row.begin() + A.col_ptr[c + 1];
                 auto it = std::lower_bound(b, e, r);

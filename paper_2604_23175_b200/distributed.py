@@ -66,7 +66,8 @@ class CudaEngine:
         self.dev = torch.device("cuda", device)
         self.plan = _native.Plan(net, ms, part, bord, maps, device=device,
                                  dense=cfg.backend == "dense", rank=rank, world=world,
-                                 area_rank=area_rank)
+                                 area_rank=area_rank,
+                                 boundary_mode={"auto": 0, "dense": 1, "sparse": 2}[cfg.boundary])
         self.n_bus, self.n_gamma = net.n_bus, bord.n_gamma
         self.state = torch.empty((2, net.n_bus), dtype=torch.float64, device=self.dev)
         ptr, n, off = self.plan.exchange_buffer()

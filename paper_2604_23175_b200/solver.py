@@ -43,6 +43,11 @@ class SolverConfig:
     dense_threshold: int = 64       # kept for API parity (fronts are dense blocks at every size)
     iterative_refinement: bool = False
     profile_phases: bool = False    # extension: fill per-phase timings from CUDA events (no graph)
+    # extension: how the reduced boundary system is factored.  "dense" = the reference's dense
+    # Cholesky (a chain of dense fronts); "sparse" = the same factorisation with the structural
+    # zeros between non-adjacent areas skipped (nested dissection on the area-clique graph);
+    # "auto" = dense up to n_Gamma = 192, sparse above.
+    boundary: str = "auto"
 
     def __post_init__(self):
         if self.max_outer_iterations < 1:
@@ -51,6 +56,8 @@ class SolverConfig:
             raise ValueError("convergence_tol must be positive")
         if self.backend not in ("dense", "sparse"):
             raise ValueError(f"unknown backend {self.backend!r}")
+        if self.boundary not in ("auto", "dense", "sparse"):
+            raise ValueError(f"unknown boundary mode {self.boundary!r}")
         if self.inner_gn_steps != 1:
             raise NotImplementedError(
                 "inner_gn_steps > 1 is not implemented on the device path yet "
@@ -112,7 +119,8 @@ class MultiAreaEstimator:
         self.device = torch.device("cuda", device)
         self.plan = _native.Plan(net, ms, part, self.bord, self.maps, device=device,
                                  dense=self.cfg.backend == "dense", rank=rank, world=world,
-                                 area_rank=area_rank)
+                                 area_rank=area_rank,
+                                 boundary_mode={"auto": 0, "dense": 1, "sparse": 2}[self.cfg.boundary])
         self.ms = ms
         self.n_gamma = self.bord.n_gamma
         self._flat = np.stack([StateVector.flat_start(net).va, np.ones(net.n_bus)])

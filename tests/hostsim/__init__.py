@@ -31,7 +31,7 @@ def _lib():
 
 class HostSim:
     def __init__(self, net, ms, part, bord, maps, dense=False, leaf=0, pmax=0, rank=0, world=1,
-                 area_rank=None):
+                 area_rank=None, boundary_mode=0):
         from paper_2604_23175_b200._native import make_desc
         L = _lib()
         self.desc, self.keep = make_desc(net, ms, part, bord, maps)
@@ -40,7 +40,7 @@ class HostSim:
         if area_rank is not None:
             self.keep["ar"] = np.ascontiguousarray(area_rank, dtype=np.int32)
             ar = self.keep["ar"].ctypes.data_as(C.POINTER(C.c_int32))
-        self.h = C.c_void_p(L.hostsim_create(C.byref(self.desc), int(dense), leaf, pmax, rank, world, ar, msg, 256))
+        self.h = C.c_void_p(L.hostsim_create(C.byref(self.desc), int(dense), leaf, pmax, rank, world, ar, msg, 256, int(boundary_mode)))
         if not self.h:
             raise RuntimeError(msg.value.decode())
         self.net, self.maps, self.n_gamma = net, maps, bord.n_gamma

@@ -98,8 +98,11 @@ void run_task(Sim& s, const Task& tk, int fidx_unused = 0) {
         if (!diag) region((cj + 1) * (cj + 2) / 2, [&](int lr, int lc, double v) { PJ[(size_t)(lr - p - j0) * ld + lc] = v; });
     }
     region((ci + 1) * (ci + 2) / 2 + cj + 1, [&](int lr, int lc, double v) { tile[(size_t)(lr - p - i0) * nj + (lc - p - j0)] = v; });
-    for (int ch : f.children) {
-        const Front& c = hp.fronts[ch]; const std::vector<int>& rel = c.rel; const double* U = &s.ubuf[c.u_off];
+    for (size_t cx = 0; cx < f.children.size(); ++cx) {
+        const int ch = f.children[cx];
+        const Front& c = hp.fronts[ch];
+        const std::vector<int>& rel = (cx < f.child_rel.size() && f.child_rel[cx] >= 0) ? hp.extra_rel[f.child_rel[cx]] : c.rel;
+        const double* U = &s.ubuf[c.u_off];
         auto lb = [&](int key) { return (int)(std::lower_bound(rel.begin(), rel.end(), key) - rel.begin()); };
         int eP = lb(p), bI = lb(p + i0), eI = lb(p + i0 + ni), bJ = lb(p + j0), eJ = lb(p + j0 + nj);
         auto add = [&](int r0, int r1, int c0, int c1, double* dst, int ldd, int rs, int cs) {
@@ -141,10 +144,10 @@ void backward(Sim& s, int fi) {
 
 extern "C" {
 
-void* hostsim_create(const gse_problem_desc* d, int dense, int leaf, int pmax, int rank, int world, const int32_t* area_rank, char* msg, int msglen) {
+void* hostsim_create(const gse_problem_desc* d, int dense, int leaf, int pmax, int rank, int world, const int32_t* area_rank, char* msg, int msglen, int boundary_mode) {
     Sim* s = new Sim(); s->d = *d;
     BuildOptions bo; bo.dense = dense != 0; if (leaf > 0) bo.leaf_buses = leaf; if (pmax == 32 || pmax == 64) bo.max_pivots = pmax;
-    bo.rank = rank; bo.world = std::max(1, world);
+    bo.rank = rank; bo.world = std::max(1, world); bo.boundary_mode = boundary_mode;
     if (area_rank) bo.area_rank.assign(area_rank, area_rank + d->n_areas);
     std::string e = build_host_program(*d, bo, s->hp);
     if (!e.empty()) { snprintf(msg, msglen, "%s", e.c_str()); delete s; return nullptr; }
@@ -174,8 +177,9 @@ long long hostsim_iterate(void* h, double* va, double* vm, double* delta_inf) {
 // packed (S_b | b_hat) of an area after hostsim_iterate, unpacked to full
 void hostsim_area_schur(void* h, int a, double* s_b, double* b_hat) {
     Sim* s = (Sim*)h; const Front& f = s->hp.fronts[s->hp.area_root[a]]; int n = s->hp.area_nb[a]; const double* U = &s->ubuf[f.u_off];
-    for (int i = 0; i < n; ++i) for (int j = 0; j <= i; ++j) { s_b[(size_t)i * n + j] = s_b[(size_t)j * n + i] = U[(size_t)i * (i + 1) / 2 + j]; }
-    for (int j = 0; j < n; ++j) b_hat[j] = U[(size_t)n * (n + 1) / 2 + j];
+    const std::vector<int>& pos = s->hp.area_bpos[a];   // local boundary variable -> row of the root
+    for (int i = 0; i < n; ++i) for (int j = 0; j < n; ++j) { int qi = std::max(pos[i], pos[j]), qj = std::min(pos[i], pos[j]); s_b[(size_t)i * n + j] = U[(size_t)qi * (qi + 1) / 2 + qj]; }
+    for (int j = 0; j < n; ++j) b_hat[j] = U[(size_t)n * (n + 1) / 2 + pos[j]];
 }
 void hostsim_ref_blocks(void* h, double* out) {   // reference-layout values of all areas, concatenated
     Sim* s = (Sim*)h; std::vector<double> v(s->hp.n_ref_vals);

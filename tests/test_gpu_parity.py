@@ -39,11 +39,12 @@ def _device_state(net):
     return torch.from_numpy(st).cuda()
 
 
+@pytest.mark.parametrize("boundary", ["dense", "sparse"])
 @pytest.mark.parametrize("name", SMALL_CASES + BIG_CASES)
-def test_solve_matches_reference_golden(G, name):
+def test_solve_matches_reference_golden(G, name, boundary):
     net, ms, part, g = build_case(name)
     tol = 1e-10 if name == "path4_slack_boundary" else 1e-6
-    est, rep = G.solve_multiarea(net, ms, part, config=G.SolverConfig(convergence_tol=tol))
+    est, rep = G.solve_multiarea(net, ms, part, config=G.SolverConfig(convergence_tol=tol, boundary=boundary))
     assert rep.iterations == int(g["iterations"])
     assert rep.converged == bool(g["converged"])
     assert rep.n_gamma == int(g["n_gamma"])
@@ -70,15 +71,17 @@ def test_lockstep_with_oracle(G, name):
     assert abs(rep.objective - ref["objective"]) <= 1e-10 * ref["objective"]
 
 
+@pytest.mark.parametrize("boundary_mode", [1, 2])
 @pytest.mark.parametrize("name", SMALL_CASES + ["pegase2869_k8"])
-def test_phase_outputs_match_oracle(G, name):
-    """Blocks, Schur blocks, boundary system and increments of the first iteration."""
+def test_phase_outputs_match_oracle(G, name, boundary_mode):
+    """Blocks, Schur blocks, boundary system and increments of the first iteration
+    (boundary factored as the dense chain and as the block-sparse tree)."""
     from oracle.mase_oracle import Oracle
     from paper_2604_23175_b200._native import Plan
     net, ms, part, g = build_case(name)
     bord, maps = G.build_variable_maps(net, part)
     orc = Oracle(net, ms, part.area_of_bus)
-    plan = Plan(net, ms, part, bord, maps)
+    plan = Plan(net, ms, part, bord, maps, boundary_mode=boundary_mode)
     st = _device_state(net)
     va0, vm0 = st[0].cpu().numpy().copy(), st[1].cpu().numpy().copy()
     orc.local(va0, vm0)
