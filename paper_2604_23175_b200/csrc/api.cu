@@ -63,7 +63,7 @@ struct gse_plan {
     DevBuf<int32_t> f_p, f_u1, f_T, f_nchild, f_child_ptr, f_children, f_rel_off, f_rel, f_reg_off, f_reg_ptr;
     DevBuf<int32_t> f_rows_off, f_rows, f_cb_off, f_cbounds, bcnt;
     DevBuf<BwdTask> btasks;
-    DevBuf<double> bpart;
+    DevBuf<double> bpart, dinv;
     DevBuf<long long> tbuf;
     DevBuf<uint32_t> orig_pos;
     DevBuf<int64_t> f_gval_off, f_l_off, f_u_off;
@@ -202,6 +202,7 @@ gse_plan::~gse_plan() {
     for (auto* b : ib) b->release();
     DevBuf<double>* db[] = {&y_g, &y_b, &br_y, &z, &w, &g, &gw, &wrg, &gval, &refval, &lbuf, &ubuf, &xsol, &obj_partial, &status};
     for (auto* b : db) b->release();
+    dinv.release();
     btasks.release(); bpart.release(); tbuf.release(); crecs.release();
     orig_pos.release(); f_gval_off.release(); f_l_off.release(); f_u_off.release(); tasks.release(); flags.release();
 }
@@ -234,6 +235,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     if (const char* e = getenv("GSE_TILE_ROWS")) { int v = atoi(e); if (v >= 8 && v <= kMaxTile) bo.tile_rows = v / 8 * 8; }
     if (const char* e = getenv("GSE_BOUNDARY")) { int v = atoi(e); if (v >= 0 && v <= 2) bo.boundary_mode = v; }
     if (const char* e = getenv("GSE_GAMMA_LEAF")) { int v = atoi(e); if (v >= 1) bo.gamma_leaf_buses = v; }
+    if (const char* e = getenv("GSE_MAX_PIVOTS")) { int v = atoi(e); if (v == 32 || v == 64) bo.max_pivots = v; }
     if (const char* e = getenv("GSE_LEAF_BUSES")) { int v = atoi(e); if (v >= 1) bo.leaf_buses = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;
@@ -312,6 +314,9 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     ft.u_off = plan->f_u_off.ptr; ft.rows_off = plan->f_rows_off.ptr; ft.rows = plan->f_rows.ptr;
 
     // ---- level launches: tasks grouped by (level, pivot class) ----
+    std::vector<int32_t> dinv_off(nf, 0);
+    { int32_t c = 0; for (size_t i = 0; i < nf; ++i) { dinv_off[i] = c; c += (hp.fronts[i].p + 7) / 8 * 8; }
+      CU(plan->dinv.alloc(c + 8)); plan->ft.dinv = plan->dinv.ptr; }
     std::vector<TaskRec> trecs;
     std::vector<ChildRec> crecs;
     for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
@@ -335,6 +340,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 TaskRec r{};
                 r.front = t.front; r.ci = t.ci; r.cj = t.cj; r.p = f.p; r.u1 = f.u1; r.T = T;
                 r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = direct ? 1 : 0;
+                r.dinv_off = dinv_off[t.front];
                 const int32_t* rp = &hp.reg_ptr[hp.front_reg_off[t.front]];
                 const int ridI = (t.ci + 1) * (t.ci + 2) / 2, ridJ = (t.cj + 1) * (t.cj + 2) / 2;
                 r.reg[0] = rp[0]; r.reg[1] = rp[1];
@@ -363,7 +369,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 ++L.count;
             }
             if (L.count) {
-                if (L.smem > 220 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
+                if (L.smem > 214 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
                 plan->fwd.push_back(L);
             }
         }
@@ -379,7 +385,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
             const int u = hp.fronts[f].u1 - 1;
             const int ns = std::max(1, (u + 63) / 64);
             const Front& fr = hp.fronts[f];
-            for (int sp = 0; sp < ns; ++sp) btasks.push_back({f, sp, ns, pbase, fr.p, u, frows_off[f], 0, fr.l_off, 0});
+            for (int sp = 0; sp < ns; ++sp) btasks.push_back({f, sp, ns, pbase, fr.p, u, frows_off[f], dinv_off[f], fr.l_off, 0});
             pbase += ns; B.count += ns;
         }
         plan->bwd.push_back(B);

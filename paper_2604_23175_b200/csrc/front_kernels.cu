@@ -133,10 +133,12 @@ __global__ void __launch_bounds__(kFrontThreads, HAS_PIVOTS ? 1 : 2)
 front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* __restrict__ gval,
                   double* __restrict__ lbuf, double* __restrict__ ubuf, unsigned long long* err) {
     extern __shared__ __align__(16) double sm[];
+    double* __restrict__ dinv = ft.dinv;
     __shared__ __align__(16) TaskRec hdr;
     __shared__ __align__(16) ChildRec crec[kChildBatch];
     __shared__ int s_inv[kGatherBatch][kInvRows];
     __shared__ double s_ld[48];           // published 8x8 diagonal factor (36) + reciprocal pivots (8)
+    __shared__ double s_rinv[64];         // reciprocal pivots of the whole front (stored for the backward pass)
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
     long long* tb = ft.tbuf ? ft.tbuf + 32 * ((&tasks[blockIdx.x]) - (const TaskRec*)ft.task0) : nullptr;
@@ -238,24 +240,29 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
     GSE_TICK(3);
 
     // ---- blocked panel factorisation (block = 8 columns) ---------------------------------------
+    // Per block: warp 0 updates the 8x8 diagonal tile (four independent MMA chains), factors it in
+    // registers and publishes it while the other warps update the remaining row tiles on the tensor
+    // pipe (look-ahead); then every row solves against the published block (right-looking:
+    // independent FMAs).  Two barriers per 8 pivots.
     if (HAS_PIVOTS && p) {
         const int R = rp + ri + rj;                 // padded rows: [pivots | chunk I | chunk J]
         const int ntile = R >> 3;
         for (int kb = 0; kb < rp; kb += 8) {
             const int t0 = kb >> 3;
             if (warp == 0) {
-                // diagonal tile first: update (tensor pipe), then factor in registers and publish
                 if (kb) {
                     const double* ap = pan + (size_t)(kb + (lane >> 2)) * ld + (lane & 3);
-                    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+                    double c[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
                     int kk = 0;
-                    for (; kk + 4 < kb; kk += 8) {           // two independent chains
-                        dmma_m8n8k4(c0, c1, ap[kk], ap[kk]);
-                        dmma_m8n8k4(e0, e1, ap[kk + 4], ap[kk + 4]);
+                    for (; kk + 12 < kb; kk += 16) {         // four independent chains
+                        dmma_m8n8k4(c[0], c[1], ap[kk], ap[kk]);
+                        dmma_m8n8k4(c[2], c[3], ap[kk + 4], ap[kk + 4]);
+                        dmma_m8n8k4(c[4], c[5], ap[kk + 8], ap[kk + 8]);
+                        dmma_m8n8k4(c[6], c[7], ap[kk + 12], ap[kk + 12]);
                     }
-                    if (kk < kb) dmma_m8n8k4(c0, c1, ap[kk], ap[kk]);
+                    for (; kk < kb; kk += 4) dmma_m8n8k4(c[0], c[1], ap[kk], ap[kk]);
                     double* o = pan + (size_t)(kb + (lane >> 2)) * ld + kb + 2 * (lane & 3);
-                    o[0] -= c0 + e0; o[1] -= c1 + e1;
+                    o[0] -= (c[0] + c[2]) + (c[4] + c[6]); o[1] -= (c[1] + c[3]) + (c[5] + c[7]);
                     __syncwarp();
                 }
                 double d[36];   // lower triangle, row-major: d[i*(i+1)/2 + j]
@@ -280,13 +287,19 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
                         for (int i = j; i < 8; ++i)
                             d[i * (i + 1) / 2 + j] = fma(-d[i * (i + 1) / 2 + k], d[j * (j + 1) / 2 + k], d[i * (i + 1) / 2 + j]);
                 }
-                __syncwarp();
-                if (lane == 0) {
+                // publish: every lane holds the same values; lane l writes entries l and l + 32
+                {
+                    double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-                    for (int i = 0; i < 36; ++i) s_ld[i] = d[i];
+                    for (int i = 0; i < 32; ++i) if (lane == i) v0 = d[i];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) s_ld[36 + k] = rinv[k];
-                    if (badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
+                    for (int i = 32; i < 36; ++i) if (lane == i - 32) v1 = d[i];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) if (lane == 4 + k) v1 = rinv[k];
+                    s_ld[lane] = v0;
+                    if (lane < 12) s_ld[32 + lane] = v1;
+                    if (lane >= 4 && lane < 12 && kb + lane - 4 < p) s_rinv[kb + lane - 4] = v1;
+                    if (lane == 0 && badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
                 }
             } else if (kb) {
                 // rows below the diagonal tile: block column kb -= A[rows, 0:kb] * A[kb:kb+8, 0:kb]^T
@@ -326,10 +339,9 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
                     for (int j = 0; j < 8; ++j) y[j] = myrow[j];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        double acc = y[k];
+                        y[k] *= s_ld[36 + k];
 #pragma unroll
-                        for (int j = 0; j < k; ++j) acc = fma(-y[j], s_ld[k * (k + 1) / 2 + j], acc);
-                        y[k] = acc * s_ld[36 + k];
+                        for (int j = k + 1; j < 8; ++j) y[j] = fma(-y[k], s_ld[j * (j + 1) / 2 + k], y[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) myrow[j] = y[j];
@@ -398,9 +410,11 @@ front_task_kernel(FrontTab ft, const TaskRec* __restrict__ tasks, const double* 
         // ---- factor panel to global (diagonal tasks own their row chunk) ----------------------
         if (HAS_PIVOTS && p && diag) {
             double* L = lbuf + hdr.l_off;
-            if (ci == 0)
+            if (ci == 0) {
                 for (int r = warp; r < p; r += nwarps)
                     for (int k = lane; k < p; k += 32) L[(size_t)r * p + k] = pan[r * ld + k];
+                if (tid < p) dinv[hdr.dinv_off + tid] = s_rinv[tid];
+            }
             double* Li = L + (size_t)(p + i0) * p;
             for (int r = warp; r < ni; r += nwarps)
                 for (int k = lane; k < p; k += 32) Li[(size_t)r * p + k] = Pi[r * ld + k];
@@ -500,9 +514,10 @@ __global__ void __launch_bounds__(128) backward_kernel(FrontTab ft, const BwdTas
     __syncthreads();
     if (tid < 32) {
         double t0 = tv[tid], t1 = tv[tid + 32];
+        const double* di = ft.dinv + tk.dinv_off;
+        const double r0 = tid < p ? di[tid] : 0.0, r1 = tid + 32 < p ? di[tid + 32] : 0.0;
         for (int c = p - 1; c >= 0; --c) {
-            const double tc = __shfl_sync(0xffffffffu, c < 32 ? t0 : t1, c & 31);
-            const double xc = tc / l11[c * 65 + c];
+            const double xc = __shfl_sync(0xffffffffu, c < 32 ? t0 * r0 : t1 * r1, c & 31);
             if (tid == (c & 31)) { if (c < 32) t0 = xc; else t1 = xc; }
             if (tid < c) t0 = fma(-l11[c * 65 + tid], xc, t0);
             if (tid + 32 < c) t1 = fma(-l11[c * 65 + tid + 32], xc, t1);
@@ -519,7 +534,7 @@ void launch_backward(const FrontTab& ft, const BwdTask* tasks, int ntasks, const
 }
 
 cudaError_t configure_kernels() {
-    const int maxsm = 220 * 1024;   // static + dynamic must stay within the 227 KB opt-in limit
+    const int maxsm = 214 * 1024;   // static + dynamic must stay within the 227 KB opt-in limit
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(front_task_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
     if ((e = cudaFuncSetAttribute(front_task_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;

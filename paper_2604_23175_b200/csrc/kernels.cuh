@@ -25,11 +25,11 @@ struct TaskRec {                                      // 128 bytes
     int32_t front, ci, cj, p, u1, T, nchild, child_off;
     int32_t reg[8];                                   // original-entry ranges (relative to gval_off): PP, IP, JP, tile
     int64_t gval_off, l_off, u_off;
-    int32_t flags, pad[9];                            // flags bit 0: tile read directly from the single child's U
+    int32_t flags, dinv_off, pad[8];                  // flags bit 0: tile read directly from the single child's U
 };
 // One child of a task (children that do not reach the task's regions are pruned on the host).
 struct ChildRec { int64_t u_off; int32_t rel_off, eP, bI, eI, bJ, eJ; };   // 32 bytes
-struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, pad; int64_t l_off, pad2; };   // 48 bytes
+struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, dinv_off; int64_t l_off, pad2; };   // 48 bytes
 
 
 // Front tables (SoA over fronts).
@@ -42,6 +42,7 @@ struct FrontTab {
     const int64_t *gval_off, *l_off, *u_off;
     const int32_t *rows_off, *rows;        // global positions of [pivots | update rows]
     const ChildRec* crecs;          // per-task child records
+    double* dinv;                          // reciprocal pivots per front (written forward, read backward)
     long long* tbuf;                       // optional per-task phase clocks (debug), 8 per task
     const void* task0;                     // base of the task array (indexes tbuf)
 };

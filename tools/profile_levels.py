@@ -51,6 +51,9 @@ for i in range(n):
     tot = blk.sum(axis=1)
     w = int(np.argmax(tot))
     print(f"launch {i:2d} ctas {ct[i]:4d} slowest {tot[w]:7d} cyc: " + " ".join(f"{l}={v}" for l, v in zip(labels, blk[w])) + f" | median total {int(np.median(tot))}")
+    row = clk[pos + w]
+    if row[24] > 0:
+        print("      last panel block: diag-dmma=%d load-d=%d factor=%d publish=%d sync1=%d trsm=%d sync2=%d" % tuple(int(row[k + 1] - row[k]) for k in range(24, 31)))
     if ct[i] <= 8 or i in (3, 17):
         row = clk[pos + w]
         ch = [(int(row[8 + 2 * c] - (row[7] if c == 0 else row[7 + 2 * c])), int(row[9 + 2 * c] - row[8 + 2 * c])) for c in range(12) if row[8 + 2 * c] > 0 and row[9 + 2 * c] >= row[8 + 2 * c]]

@@ -3,11 +3,11 @@ import csv, sys, collections, re
 rows = []
 with open(sys.argv[1]) as fh:
     lines = [l for l in fh if not l.startswith("==")]
-rd = csv.DictReader(lines)
+rd = [r for r in csv.DictReader(lines) if r.get("Metric Name") == "gpu__time_duration.sum"]
+if len(sys.argv) > 2 and sys.argv[2] == "second-half":
+    rd = rd[len(rd) // 2:]
 agg = collections.OrderedDict()
 for r in rd:
-    if r.get("Metric Name") != "gpu__time_duration.sum":
-        continue
     name = re.sub(r"\(.*", "", r["Kernel Name"])
     val = float(r["Metric Value"].replace(",", ""))
     unit = r["Metric Unit"]
