@@ -38,6 +38,7 @@ struct DevBuf {
 };
 
 struct LevelLaunch { int pclass; int first, count; size_t smem; int phase; };
+constexpr int kBlkDelta = 0, kBlkResult = 64, kBlkErr = 65, kBlkObj = 66, kBlkStamps = 68, kBlkWords = 68 + 1 + 64 * 8;
 struct BwdLaunch { int first, count, phase; };
 
 }  // namespace
@@ -54,10 +55,12 @@ struct gse_plan {
     DevBuf<double> y_g, y_b, br_y, z, w;
     // evaluation units
     DevBuf<int32_t> vm_bus, vm_row, vm_slot, fl_branch, fl_from, fl_to, fl_row, fl_slot;
-    DevBuf<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq;
-    DevBuf<double> g, gw, wrg;
+    DevBuf<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq, inj_nth;
+    DevBuf<double> val;                       // [g | w*g | w*r]: template partials per slot, weighted residual per row
     // accumulation programs
-    DevBuf<int32_t> acc_ptr, acc_a, acc_b, racc_ptr, racc_a, racc_b;
+    DevBuf<int32_t> acc_ptr, acc_items, acc_uniq, racc_ptr, racc_a, racc_b;
+    DevBuf<uint32_t> acc_pair;
+    AccProg ap{};
     DevBuf<double> gval, refval;
     // fronts
     DevBuf<int32_t> f_p, f_u1, f_T, f_nchild, f_child_ptr, f_children, f_rel_off, f_rel, f_reg_off, f_reg_ptr;
@@ -80,6 +83,15 @@ struct gse_plan {
     std::vector<BwdLaunch> bwd;
     EvalProg ep{};
     FrontTab ft{};
+
+    // persistent dataflow kernel (solve_kernel.cu)
+    SolveProg sp{};
+    DevBuf<unsigned long long> syncblk;       // [delta 64 | result | err copy | J | pad | stamps 1+512 | counters...]
+    unsigned long long* h_blk = nullptr;      // pinned mirror of the first kBlkWords words
+    DevBuf<unsigned long long> trace;         // per-item stamps of the persistent kernel (debug)
+    int solve_grid = 0;
+    size_t solve_smem = 0, sync_bytes = 0;
+    bool persistent = false, stamps = true;
 
     cudaGraphExec_t graph = nullptr;
     const double* graph_va = nullptr;
@@ -107,8 +119,7 @@ int fail(gse_plan* p, int code, const std::string& msg, int area = -1, int pivot
 // all kernels of one outer iteration on plan->stream; phase boundaries marked with events if timed
 int enqueue_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
     launch_eval(plan->ep, va, vm, plan->stream);
-    launch_accumulate(plan->acc_ptr.ptr, plan->acc_a.ptr, plan->acc_b.ptr, plan->g.ptr, plan->gw.ptr, plan->wrg.ptr,
-                      plan->gval.ptr, (int64_t)plan->hp.n_gval, plan->stream);
+    launch_accumulate_staged(plan->ap, plan->stream);
     return 2;
 }
 int enqueue_fwd(gse_plan* plan, int phase) {
@@ -194,15 +205,17 @@ gse_plan::~gse_plan() {
     if (stream) cudaStreamDestroy(stream);
     if (h_flags) cudaFreeHost(h_flags);
     if (h_obj) cudaFreeHost(h_obj);
+    if (h_blk) cudaFreeHost(h_blk);
+    syncblk.release(); trace.release();
     DevBuf<int32_t>* ib[] = {&y_ptr, &y_idx, &br_from, &br_to, &m_type, &m_target, &vm_bus, &vm_row, &vm_slot, &fl_branch,
-                             &fl_from, &fl_to, &fl_row, &fl_slot, &inj_bus, &inj_rowp, &inj_rowq, &inj_slotp, &inj_slotq,
-                             &acc_ptr, &acc_a, &acc_b, &racc_ptr, &racc_a, &racc_b, &f_p, &f_u1, &f_T, &f_nchild,
+                             &fl_from, &fl_to, &fl_row, &fl_slot, &inj_bus, &inj_rowp, &inj_rowq, &inj_slotp, &inj_slotq, &inj_nth,
+                             &acc_ptr, &acc_items, &acc_uniq, &racc_ptr, &racc_a, &racc_b, &f_p, &f_u1, &f_T, &f_nchild,
                              &f_child_ptr, &f_children, &f_rel_off, &f_rel, &f_reg_off, &f_reg_ptr, &f_rows_off, &f_rows, &f_cb_off, &f_cbounds, &bcnt,
                              &bwd_fronts, &upd_bus, &upd_quant, &upd_pos};
     for (auto* b : ib) b->release();
-    DevBuf<double>* db[] = {&y_g, &y_b, &br_y, &z, &w, &g, &gw, &wrg, &gval, &refval, &lbuf, &ubuf, &xsol, &obj_partial, &status};
+    DevBuf<double>* db[] = {&y_g, &y_b, &br_y, &z, &w, &val, &gval, &refval, &lbuf, &ubuf, &xsol, &obj_partial, &status};
     for (auto* b : db) b->release();
-    dinv.release();
+    dinv.release(); acc_pair.release();
     btasks.release(); bpart.release(); tbuf.release(); crecs.release();
     orig_pos.release(); f_gval_off.release(); f_l_off.release(); f_u_off.release(); tasks.release(); flags.release();
 }
@@ -245,6 +258,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
 
     CU(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
     CU(configure_kernels());
+    CU(configure_unit_kernels());
     for (auto& e : plan->ev) CU(cudaEventCreate(&e));
     CU(cudaMallocHost(&plan->h_flags, 2 * sizeof(unsigned long long)));
     CU(cudaMallocHost(&plan->h_obj, sizeof(double)));
@@ -267,11 +281,15 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     CU(plan->fl_branch.upload(hp.fl_branch)); CU(plan->fl_from.upload(hp.fl_from)); CU(plan->fl_to.upload(hp.fl_to));
     CU(plan->fl_row.upload(hp.fl_row)); CU(plan->fl_slot.upload(hp.fl_slot));
     CU(plan->inj_bus.upload(hp.inj_bus)); CU(plan->inj_rowp.upload(hp.inj_rowp)); CU(plan->inj_rowq.upload(hp.inj_rowq));
-    CU(plan->inj_slotp.upload(hp.inj_slotp)); CU(plan->inj_slotq.upload(hp.inj_slotq));
-    CU(plan->g.alloc(hp.n_slots)); CU(plan->gw.alloc(hp.n_slots)); CU(plan->wrg.alloc(hp.n_slots));
-    CU(plan->acc_ptr.upload(hp.acc_ptr)); CU(plan->acc_a.upload(hp.acc_a)); CU(plan->acc_b.upload(hp.acc_b));
+    CU(plan->inj_slotp.upload(hp.inj_slotp)); CU(plan->inj_slotq.upload(hp.inj_slotq)); CU(plan->inj_nth.upload(hp.inj_nth));
+    CU(plan->val.alloc(hp.n_val));
+    if (hp.acc_stage_max > kAccStageMax || hp.acc_pair_max > kAccPairMax) return fail(plan, GSE_E_INVALID, "a normal-equation entry has too many contributions for the staged accumulation");
+    CU(plan->acc_ptr.upload(hp.acc_lptr)); CU(plan->acc_items.upload(hp.acc_items)); CU(plan->acc_uniq.upload(hp.acc_uniq));
+    CU(plan->acc_pair.upload(hp.acc_pair));
     CU(plan->racc_ptr.upload(hp.racc_ptr)); CU(plan->racc_a.upload(hp.racc_a)); CU(plan->racc_b.upload(hp.racc_b));
     CU(plan->gval.alloc(hp.n_gval)); CU(plan->refval.alloc(hp.n_ref_vals));
+    plan->ap = AccProg{plan->acc_items.ptr, plan->acc_uniq.ptr, plan->acc_ptr.ptr, plan->acc_pair.ptr, plan->val.ptr,
+                       plan->gval.ptr, (int32_t)(hp.acc_items.size() / 8)};
     EvalProg& ep = plan->ep;
     ep.y_ptr = plan->y_ptr.ptr; ep.y_idx = plan->y_idx.ptr; ep.y_g = plan->y_g.ptr; ep.y_b = plan->y_b.ptr;
     ep.br_y = plan->br_y.ptr; ep.z = plan->z.ptr; ep.w = plan->w.ptr; ep.slack = d->slack;
@@ -280,8 +298,8 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     ep.fl_branch = plan->fl_branch.ptr; ep.fl_from = plan->fl_from.ptr; ep.fl_to = plan->fl_to.ptr;
     ep.fl_row = plan->fl_row.ptr; ep.fl_slot = plan->fl_slot.ptr;
     ep.inj_bus = plan->inj_bus.ptr; ep.inj_rowp = plan->inj_rowp.ptr; ep.inj_rowq = plan->inj_rowq.ptr;
-    ep.inj_slotp = plan->inj_slotp.ptr; ep.inj_slotq = plan->inj_slotq.ptr;
-    ep.g = plan->g.ptr; ep.gw = plan->gw.ptr; ep.wrg = plan->wrg.ptr;
+    ep.inj_slotp = plan->inj_slotp.ptr; ep.inj_slotq = plan->inj_slotq.ptr; ep.inj_nth = plan->inj_nth.ptr;
+    ep.g = plan->val.ptr; ep.gw = plan->val.ptr + hp.n_slots; ep.wr = plan->val.ptr + 2 * hp.n_slots;
 
     // ---- front tables ----
     const size_t nf = hp.fronts.size();
@@ -319,8 +337,15 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
       CU(plan->dinv.alloc(c + 8)); plan->ft.dinv = plan->dinv.ptr; }
     std::vector<TaskRec> trecs;
     std::vector<ChildRec> crecs;
+    auto ntasks_of = [&](int fr) { const int n = hp.fronts[fr].nch; return n * (n + 1) / 2; };
+    int n_solve_tasks = 0;
+    size_t solve_task_smem = 0;
+    // two passes: the tasks of the solve in level order first (the persistent kernel walks exactly
+    // this prefix), then the readback-only boundary root of the block-sparse mode (phase 5)
+    for (int pass = 0; pass < 2; ++pass)
     for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
         for (int key : {11, 10, 21, 20, 31, 30, 51, 50}) {      // (phase, pivot class)
+            if ((key / 10 == 5) != (pass == 1)) continue;
             const int phase = key / 10, pclass = key % 10;
             LevelLaunch L{pclass, (int)trecs.size(), 0, 0, phase};
             for (const Task& t : hp.fwd_levels[lv]) {
@@ -339,7 +364,8 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, diag, direct));
                 TaskRec r{};
                 r.front = t.front; r.ci = t.ci; r.cj = t.cj; r.p = f.p; r.u1 = f.u1; r.T = T;
-                r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = direct ? 1 : 0;
+                r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = (direct ? 1 : 0) | (f.n_orig > 0 ? 2 : 0);
+                r.phase = phase;
                 r.dinv_off = dinv_off[t.front];
                 const int32_t* rp = &hp.reg_ptr[hp.front_reg_off[t.front]];
                 const int ridI = (t.ci + 1) * (t.ci + 2) / 2, ridJ = (t.cj + 1) * (t.cj + 2) / 2;
@@ -359,6 +385,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                     cr.eP = f.p ? lb(f.p) : 0;
                     cr.bI = lb(f.p + t.ci * T); cr.eI = lb(f.p + t.ci * T + ni);
                     cr.bJ = lb(f.p + t.cj * T); cr.eJ = lb(f.p + t.cj * T + nj);
+                    cr.front = ch; cr.need = ntasks_of(ch);
                     const bool hits_panel = f.p && cr.eP > 0;
                     const bool hits_tile = !direct && cr.eI > cr.bI && cr.eJ > cr.bJ;
                     if (!hits_panel && !hits_tile && !direct) continue;   // pruned (order of the rest is kept)
@@ -368,6 +395,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 trecs.push_back(r);
                 ++L.count;
             }
+            if (pass == 0) { n_solve_tasks = (int)trecs.size(); solve_task_smem = std::max(solve_task_smem, L.smem); }
             if (L.count) {
                 if (L.smem > 214 * 1024) return fail(plan, GSE_E_INVALID, "front task exceeds shared memory");
                 plan->fwd.push_back(L);
@@ -385,7 +413,15 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
             const int u = hp.fronts[f].u1 - 1;
             const int ns = std::max(1, (u + 63) / 64);
             const Front& fr = hp.fronts[f];
-            for (int sp = 0; sp < ns; ++sp) btasks.push_back({f, sp, ns, pbase, fr.p, u, frows_off[f], dinv_off[f], fr.l_off, 0});
+            int dep = fr.parent;
+            while (dep >= 0 && hp.fronts[dep].p == 0) dep = hp.fronts[dep].parent;
+            for (int sp = 0; sp < ns; ++sp) {
+                BwdTask bt{};
+                bt.front = f; bt.split = sp; bt.nsplit = ns; bt.pbase = pbase; bt.p = fr.p; bt.u = u;
+                bt.rows_off = frows_off[f]; bt.dinv_off = dinv_off[f]; bt.l_off = fr.l_off;
+                bt.dep = dep; bt.need = ntasks_of(f); bt.phase = hp.bwd_phase[i];
+                btasks.push_back(bt);
+            }
             pbase += ns; B.count += ns;
         }
         plan->bwd.push_back(B);
@@ -398,6 +434,51 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     CU(plan->status.alloc(2));
     CU(plan->flags.alloc(2));
     CU(cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long)));
+
+    // ---- persistent dataflow kernel: one launch per solve (single-rank plans) ----
+    {
+        int mode = opt ? opt->persistent : 0;                       // 0 auto, 1 on, 2 off
+        if (const char* e = getenv("GSE_PERSISTENT")) mode = atoi(e) ? 1 : 2;
+        if (const char* e = getenv("GSE_STAMPS")) plan->stamps = atoi(e) != 0;
+        SolveProg& sp = plan->sp;
+        sp.n_units = ep.n_fl + ep.n_inj + ep.n_vm;
+        sp.n_eval_items = (sp.n_units + kEvalPerItem - 1) / kEvalPerItem;
+        sp.n_gval = hp.n_gval;
+        sp.n_acc_items = plan->ap.n_items;
+        sp.n_tasks = n_solve_tasks;
+        sp.n_btasks = (int)btasks.size();
+        sp.n_upd = (int)hp.upd_bus.size();
+        sp.n_upd_items = (sp.n_upd + kUpdPerItem - 1) / kUpdPerItem;
+        sp.items_per_it = sp.n_eval_items + sp.n_acc_items + sp.n_tasks + sp.n_btasks + sp.n_upd_items;
+        sp.n_bwd_fronts = 0;
+        for (auto& lv : hp.bwd_levels) sp.n_bwd_fronts += (int)lv.size();
+        sp.n_fronts = (int)nf; sp.n_rows = d->n_rows;
+        sp.tasks = plan->tasks.ptr; sp.btasks = plan->btasks.ptr;
+        sp.acc_items = plan->acc_items.ptr; sp.acc_uniq = plan->acc_uniq.ptr; sp.acc_ptr = plan->acc_ptr.ptr;
+        sp.acc_pair = plan->acc_pair.ptr; sp.val = plan->val.ptr;
+        sp.upd_bus = plan->upd_bus.ptr; sp.upd_quant = plan->upd_quant.ptr; sp.upd_pos = plan->upd_pos.ptr;
+        sp.m_type = plan->m_type.ptr; sp.m_target = plan->m_target.ptr; sp.br_from = plan->br_from.ptr; sp.br_to = plan->br_to.ptr;
+        sp.gval = plan->gval.ptr; sp.lbuf = plan->lbuf.ptr; sp.ubuf = plan->ubuf.ptr; sp.xsol = plan->xsol.ptr;
+        sp.bpart = plan->bpart.ptr; sp.obj_partial = plan->obj_partial.ptr; sp.bcnt = plan->bcnt.ptr;
+        const size_t nctr = CTR_FRONT0 + 2 * nf;
+        plan->sync_bytes = sizeof(unsigned long long) * kBlkWords + sizeof(unsigned) * nctr;
+        CU(plan->syncblk.alloc(kBlkWords + (nctr + 1) / 2));
+        CU(cudaMallocHost(&plan->h_blk, sizeof(unsigned long long) * kBlkWords));
+        unsigned long long* blk = plan->syncblk.ptr;
+        sp.delta = blk + kBlkDelta; sp.result = reinterpret_cast<int32_t*>(blk + kBlkResult);
+        sp.err_out = blk + kBlkErr; sp.obj_out = reinterpret_cast<double*>(blk + kBlkObj);
+        sp.stamps = plan->stamps ? blk + kBlkStamps : nullptr;
+        sp.ctr = reinterpret_cast<unsigned*>(blk + kBlkWords);
+        sp.err = plan->flags.ptr + 1;
+        plan->solve_smem = std::max<size_t>(solve_task_smem, kAccSmemBytes);   // >= BwdScratch too
+        plan->persistent = false;
+        if (mode != 2 && bo.world == 1 && sp.items_per_it > 0) {
+            const int cap = solve_kernel_max_ctas(plan->solve_smem, plan->device);
+            if (cap <= 0) return fail(plan, GSE_E_CUDA, "persistent solve kernel does not fit this device");
+            plan->solve_grid = std::min(cap, sp.items_per_it);
+            plan->persistent = true;
+        }
+    }
     CU(cudaDeviceSynchronize());
     plan->err.code = GSE_OK; plan->err.area = -1; plan->err.pivot = -1; plan->err.message[0] = 0;
     return GSE_OK;
@@ -454,11 +535,57 @@ int gse_objective(gse_plan* plan, const double* va, const double* vm, double* j_
     return GSE_OK;
 }
 
+// The whole GN loop + objective in one cooperative launch; one 4.6 KB readback at the end.
+static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, double* va, double* vm, gse_report* rep) {
+    cudaStream_t s = plan->stream;
+    SolveProg sp = plan->sp;
+    sp.max_it = max_it; sp.tol = cfg->convergence_tol;
+    if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 8 * (size_t)sp.items_per_it * 16, s));
+    auto t0 = std::chrono::steady_clock::now();
+    cudaEventRecord(plan->ev[6], s);
+    CU(cudaMemsetAsync(plan->syncblk.ptr, 0, plan->sync_bytes, s));
+    CU(launch_solve(sp, plan->ep, plan->ft, va, vm, plan->solve_grid, plan->solve_smem, s));
+    CU(cudaMemcpyAsync(plan->h_blk, plan->syncblk.ptr, sizeof(unsigned long long) * kBlkWords, cudaMemcpyDeviceToHost, s));
+    cudaEventRecord(plan->ev[7], s);
+    CU(cudaStreamSynchronize(s));
+    rep->loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    { float ms = 0; cudaEventElapsedTime(&ms, plan->ev[6], plan->ev[7]); rep->gpu_s = ms * 1e-3; }
+    const unsigned long long* blk = plan->h_blk;
+    const int32_t* res = reinterpret_cast<const int32_t*>(blk + kBlkResult);
+    rep->iterations = res[0]; rep->converged = res[1];
+    plan->launches_last = 1;
+    for (int it = 0; it < rep->iterations && it < 64; ++it) memcpy(&rep->delta_inf[it], &blk[kBlkDelta + it], sizeof(double));
+    if (plan->stamps) {
+        // phase end stamps (globaltimer ns) per iteration: 0 eval, 1 accumulate, 2 local condense,
+        // 3 boundary assemble, 4 boundary factor, 5 boundary back-substitution, 6 recovery, 7 update.
+        // Phases overlap in the dataflow schedule; each is charged from the previous phase's end.
+        unsigned long long start = blk[kBlkStamps];
+        for (int it = 0; it < rep->iterations && it < 64; ++it) {
+            const unsigned long long* st = blk + kBlkStamps + 1 + 8 * it;
+            unsigned long long cur = start;
+            auto take = [&](unsigned long long end) { double dt = end > cur ? (end - cur) * 1e-9 : 0.0; if (end > cur) cur = end; return dt; };
+            rep->phase_s[0] += take(std::max(st[0], st[1]));
+            rep->phase_s[1] += take(st[2]);
+            rep->phase_s[2] += take(st[3]);
+            rep->phase_s[3] += take(std::max(st[4], st[5]));
+            rep->phase_s[4] += take(std::max(st[6], st[7]));
+            start = std::max(cur, st[7]);
+        }
+    }
+    if (blk[kBlkErr] != ~0ull) {
+        cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+        return decode_failure(plan, blk[kBlkErr]);
+    }
+    memcpy(&rep->objective, &blk[kBlkObj], sizeof(double));
+    return GSE_OK;
+}
+
 int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse_report* rep) {
     CU(cudaSetDevice(plan->device));
     memset(rep, 0, sizeof *rep);
     const int max_it = std::min(cfg->max_outer_iterations, 64);
     const bool timed = cfg->time_phases != 0;
+    if (!timed && plan->persistent) return solve_persistent(plan, cfg, max_it, va, vm, rep);
     if (!timed) { int rc = ensure_graph(plan, va, vm); if (rc) return rc; }
     plan->launches_last = 0;
     auto t0 = std::chrono::steady_clock::now();
@@ -494,8 +621,8 @@ int gse_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
     CU(cudaSetDevice(plan->device));
     enqueue_phase_assemble(plan, va, vm);
     // reference-layout blocks for component parity (same slot values, second destination map)
-    launch_accumulate(plan->racc_ptr.ptr, plan->racc_a.ptr, plan->racc_b.ptr, plan->g.ptr, plan->gw.ptr, plan->wrg.ptr,
-                      plan->refval.ptr, (int64_t)plan->hp.n_ref_vals, plan->stream);
+    launch_accumulate(plan->racc_ptr.ptr, plan->racc_a.ptr, plan->racc_b.ptr, plan->val.ptr, plan->refval.ptr,
+                      (int64_t)plan->hp.n_ref_vals, plan->stream);
     CU(cudaStreamSynchronize(plan->stream));
     return GSE_OK;
 }
@@ -635,9 +762,8 @@ int gse_profile_iteration(gse_plan* plan, double* va, double* vm, int32_t max_n,
     cudaMemsetAsync(plan->flags.ptr, 0, sizeof(unsigned long long), plan->stream);
     mark();
     launch_eval(plan->ep, va, vm, plan->stream); mark(); k.push_back(0); ph.push_back(0); ct.push_back((plan->ep.n_vm + plan->ep.n_fl + plan->ep.n_inj + 127) / 128);
-    launch_accumulate(plan->acc_ptr.ptr, plan->acc_a.ptr, plan->acc_b.ptr, plan->g.ptr, plan->gw.ptr, plan->wrg.ptr, plan->gval.ptr,
-                      (int64_t)plan->hp.n_gval, plan->stream);
-    mark(); k.push_back(1); ph.push_back(0); ct.push_back((int)((plan->hp.n_gval + 255) / 256));
+    launch_accumulate_staged(plan->ap, plan->stream);
+    mark(); k.push_back(1); ph.push_back(0); ct.push_back(plan->ap.n_items);
     for (int phs : {1, 2, 3})
         for (auto& L : plan->fwd) {
             if (L.phase != phs) continue;
@@ -662,12 +788,36 @@ int gse_profile_iteration(gse_plan* plan, double* va, double* vm, int32_t max_n,
     return n;
 }
 
+// Debug: per-item stamps of the persistent kernel.  enable=1 arms tracing for the next solves (first
+// 16 iterations); enable=0 copies [items][8] words (pull, originals ready, children ready, end,
+// smid | cta << 32) to out and disarms.  Returns the items per iteration.
+int gse_debug_trace(gse_plan* plan, int enable, unsigned long long* out, int64_t max_words) {
+    CU(cudaSetDevice(plan->device));
+    const size_t words = 8 * (size_t)plan->sp.items_per_it * 16;
+    if (enable) {
+        if (!plan->trace.ptr) CU(plan->trace.alloc(words));
+        plan->sp.trace = plan->trace.ptr;
+        return plan->sp.items_per_it;
+    }
+    if (out && plan->trace.ptr) CU(cudaMemcpy(out, plan->trace.ptr, sizeof(unsigned long long) * std::min<size_t>(max_words, words), cudaMemcpyDeviceToHost));
+    plan->sp.trace = nullptr;
+    return plan->sp.items_per_it;
+}
+// Item layout of one iteration of the persistent kernel: eval, accumulate, front, backward, update counts.
+int gse_solve_layout(const gse_plan* plan, int32_t* out) {
+    const SolveProg& sp = plan->sp;
+    out[0] = sp.n_eval_items; out[1] = sp.n_acc_items; out[2] = sp.n_tasks; out[3] = sp.n_btasks; out[4] = sp.n_upd_items;
+    out[5] = plan->solve_grid; out[6] = (int32_t)plan->solve_smem; out[7] = plan->persistent ? 1 : 0;
+    return GSE_OK;
+}
+
 int gse_plan_stats(const gse_plan* plan, double* s, int32_t n) {
     const HostProgram& hp = plan->hp;
-    double v[12] = {(double)plan->launches_last, (double)hp.fronts.size(), (double)hp.fwd_levels.size(), (double)plan->tasks.n,
+    double v[16] = {(double)plan->launches_last, (double)hp.fronts.size(), (double)hp.fwd_levels.size(), (double)plan->tasks.n,
                     (double)hp.max_front, (double)hp.n_lbuf, (double)hp.n_ubuf, (double)hp.n_pairs, (double)hp.n_slots,
-                    hp.alg_bytes, hp.dense_flops, (double)plan->launches_per_iter};
-    for (int i = 0; i < n && i < 12; ++i) s[i] = v[i];
+                    hp.alg_bytes, hp.dense_flops, (double)plan->launches_per_iter,
+                    plan->persistent ? 1.0 : 0.0, (double)plan->solve_grid, (double)plan->solve_smem, (double)plan->sp.items_per_it};
+    for (int i = 0; i < n && i < 16; ++i) s[i] = v[i];
     return GSE_OK;
 }
 

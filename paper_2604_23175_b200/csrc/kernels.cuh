@@ -15,9 +15,10 @@ struct EvalProg {
     int32_t n_vm, n_fl, n_inj;
     const int32_t *vm_bus, *vm_row, *vm_slot;
     const int32_t *fl_branch, *fl_from, *fl_to, *fl_row, *fl_slot;
-    const int32_t *inj_bus, *inj_rowp, *inj_rowq, *inj_slotp, *inj_slotq;
-    // per-slot outputs: gradient, weight*gradient, (weight*residual)*gradient
-    double *g, *gw, *wrg;
+    const int32_t *inj_bus, *inj_rowp, *inj_rowq, *inj_slotp, *inj_slotq, *inj_nth;
+    // outputs = the unified value array val = [g | gw | wr]: per slot the partial and weight * partial,
+    // per measurement row weight * residual
+    double *g, *gw, *wr;
 };
 
 // One (front, row-chunk, col-chunk) task: everything the CTA needs, read with one coalesced load.
@@ -25,11 +26,16 @@ struct TaskRec {                                      // 128 bytes
     int32_t front, ci, cj, p, u1, T, nchild, child_off;
     int32_t reg[8];                                   // original-entry ranges (relative to gval_off): PP, IP, JP, tile
     int64_t gval_off, l_off, u_off;
-    int32_t flags, dinv_off, pad[8];                  // flags bit 0: tile read directly from the single child's U
+    int32_t flags, dinv_off;                          // flags bit 0: tile read directly from the single child's U;
+                                                      //       bit 1: the front has original entries (waits for the accumulation)
+    int32_t phase, pad[7];                            // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
 };
 // One child of a task (children that do not reach the task's regions are pruned on the host).
-struct ChildRec { int64_t u_off; int32_t rel_off, eP, bI, eI, bJ, eJ; };   // 32 bytes
-struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, dinv_off; int64_t l_off, pad2; };   // 48 bytes
+// front / need: dataflow dependency -- the child is complete when its counter reaches need per iteration.
+struct ChildRec { int64_t u_off; int32_t rel_off, eP, bI, eI, bJ, eJ; int32_t front, need, pad[2]; };   // 48 bytes
+// dep: nearest ancestor front with pivots (-1: none); need: forward tasks of the own front
+struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, dinv_off; int64_t l_off; int32_t dep, need, phase, pad[3]; };   // 64 bytes
+static_assert(sizeof(TaskRec) == 128 && sizeof(ChildRec) == 48 && sizeof(BwdTask) == 64, "device record layout");
 
 
 // Front tables (SoA over fronts).
@@ -62,8 +68,18 @@ inline __host__ __device__ size_t task_smem_doubles(int p, int ni, int nj, bool 
 }
 
 void launch_eval(const EvalProg& ep, const double* va, const double* vm, cudaStream_t s);
-void launch_accumulate(const int32_t* ptr, const int32_t* a, const int32_t* b, const double* g,
-                       const double* gw, const double* wrg, double* out, int64_t n, cudaStream_t s);
+// plain form (reference-layout program of the component-parity API): one thread per destination
+void launch_accumulate(const int32_t* ptr, const int32_t* a, const int32_t* b, const double* val,
+                       double* out, int64_t n, cudaStream_t s);
+// staged form (solver layout): one CTA per item, operands in shared memory
+struct AccProg {
+    const int32_t *items, *uniq, *ptr;     // items: 8-int records (plan.hpp); ptr: item-local contribution pointers
+    const uint32_t* pair;                  // per contribution: staged positions (b << 16 | a)
+    const double* val;
+    double* out;
+    int32_t n_items;
+};
+void launch_accumulate_staged(const AccProg& ap, cudaStream_t s);
 // pclass: 0 (assembly only), 32 or 64
 void launch_front_tasks(int pclass, const FrontTab& ft, const TaskRec* tasks, int ntasks,
                         size_t smem_bytes, const double* gval, double* lbuf, double* ubuf,
@@ -78,5 +94,42 @@ void launch_objective(const EvalProg& ep, const int32_t* m_type, const int32_t* 
                       const double* vm, double* partial, double* out, cudaStream_t s);
 int objective_blocks(int n_rows);
 cudaError_t configure_kernels();
+cudaError_t configure_unit_kernels();
+
+// ---- persistent dataflow kernel (solve_kernel.cu): the whole Gauss-Newton loop in ONE launch ----
+// Work items of one iteration, in dependency (topological) order:
+//   [eval blocks | accumulate blocks | front tasks (level order) | backward tasks (top-down) | update blocks]
+// CTAs pull item indices from a global counter and spin on per-front completion counters.
+constexpr int kSolveThreads = 256;
+constexpr int kEvalPerItem = 256, kUpdPerItem = 1024;
+enum { CTR_NEXT = 0, CTR_EVAL = 32, CTR_ACC = 64, CTR_FWD = 96, CTR_BWD = 128, CTR_UPD = 160, CTR_OBJ = 192, CTR_FRONT0 = 224 };
+struct SolveProg {
+    int32_t n_eval_items, n_acc_items, n_tasks, n_btasks, n_upd_items, items_per_it;
+    int32_t n_units, n_upd, n_bwd_fronts, n_fronts, n_rows, max_it;
+    int64_t n_gval;
+    double tol;
+    const TaskRec* tasks;
+    const BwdTask* btasks;
+    const int32_t *acc_items, *acc_uniq, *acc_ptr;
+    const uint32_t* acc_pair;
+    const double* val;
+    const int32_t *upd_bus, *upd_quant, *upd_pos;
+    const int32_t *m_type, *m_target, *br_from, *br_to;
+    double *gval, *lbuf, *ubuf, *xsol, *bpart, *obj_partial;   // obj_partial[nblocks] then the total
+    int32_t* bcnt;
+    unsigned int* ctr;            // CTR_* globals, then fdone[n_fronts], bdone[n_fronts]
+    unsigned long long* delta;    // [64] per-iteration |dx| max as ordered bits
+    unsigned long long* err;      // failure code (min), ~0 = none
+    unsigned long long* stamps;   // optional [1 + 64 * 8] globaltimer stamps (nullptr: off)
+    int32_t* result;              // [0] iterations, [1] converged
+    unsigned long long* err_out;  // copy of *err for the single readback
+    double* obj_out;              // J(x) at the final state
+    unsigned long long* trace;    // optional per-item stamps [item][8]: pull, originals ready, children ready, end, smid (debug)
+};
+size_t solve_kernel_static_smem();
+// returns the number of co-resident CTAs (0 on failure)
+int solve_kernel_max_ctas(size_t dyn_smem, int device);
+cudaError_t launch_solve(const SolveProg& sp, const EvalProg& ep, const FrontTab& ft, double* va, double* vm,
+                         int grid, size_t dyn_smem, cudaStream_t s);
 
 }  // namespace gse

@@ -55,10 +55,20 @@ struct HostProgram {
     // template evaluation units
     std::vector<int32_t> vm_bus, vm_row, vm_slot;
     std::vector<int32_t> fl_branch, fl_from, fl_to, fl_row /*4 per unit*/, fl_slot /*4 per unit*/;
-    std::vector<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq;
+    std::vector<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq, inj_nth /*angle slots of the row*/;
 
     // accumulation: destination-sorted contribution lists (solver layout -> gval)
-    std::vector<int32_t> acc_ptr, acc_a, acc_b;     // b == -1: right-hand-side term wrg[a]
+    // every contribution is val[a] * val[b], val = [g | w*g | w*r per row] (n_val entries)
+    std::vector<int32_t> acc_ptr, acc_a, acc_b;
+    int64_t n_val = 0;
+    // staged form of the same program.  Item record (8 ints): first destination, destinations,
+    // value-list offset, values, pair offset, pairs, local-pointer offset, 0.  The pointer segment holds
+    // the item-local contribution pointers (destinations + 1) followed by the processing order
+    // (destinations by decreasing contribution count).  Segments are padded to multiples of 4
+    // entries (16 bytes) for TMA bulk copies.
+    std::vector<int32_t> acc_items, acc_uniq, acc_lptr;
+    std::vector<uint32_t> acc_pair;                 // per contribution: staged positions (b << 16 | a)
+    int acc_stage_max = 0, acc_pair_max = 0;        // longest value list / pair list of an item
     // reference layout (component parity): per area CSR patterns + a second program
     std::vector<std::vector<int32_t>> ii_ptr, ii_idx, ib_ptr, ib_idx;
     std::vector<int64_t> ref_off;        // per area offset into the ref-layout value array
@@ -90,6 +100,12 @@ struct HostProgram {
     double alg_bytes = 0, dense_flops = 0;
     int max_front = 0;
 };
+
+// staging limits of one accumulation item: 48 KB of values + 44 KB of pairs + 12 KB of pointers / order
+constexpr int kAccStageMax = 6144;     // distinct values
+constexpr int kAccPairMax = 11264;     // contributions
+constexpr int kAccItemDestMax = 1532;  // destinations (pointers + order: at most 3072 entries)
+constexpr size_t kAccSmemBytes = 8 * (size_t)kAccStageMax + 4 * (size_t)kAccPairMax + 4 * 3072;
 
 struct BuildOptions {
     bool dense = false;

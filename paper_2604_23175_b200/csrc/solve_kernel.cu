@@ -1,0 +1,253 @@
+// solve_kernel.cu -- the whole multi-area Gauss-Newton solve as ONE persistent kernel.
+//
+// solve_multiarea's loop (reference solver.py:275-338) -- template evaluation, fused accumulation,
+// per-area Schur-mode factorisation, boundary assembly + factorisation, back-substitution, state
+// update, convergence test -- and the final objective (solver.py:100-103) run inside a single
+// cooperative launch.  One CTA slot per SM-resident block; CTAs pull work items from a global
+// counter in topological order
+//     [eval blocks | accumulate blocks | front tasks (level order) | backward tasks | update blocks]
+// and spin on per-front completion counters instead of waiting for a kernel boundary: a front
+// starts the moment its own children are done, areas progress independently, and nothing returns
+// to the host until the loop has converged (the host then reads iterations, the per-iteration
+// norms, the failure code and J in one copy).
+//
+// Deadlock freedom: an item only waits on items with a smaller index; indices are handed out in
+// increasing order and every CTA of the (cooperative) grid is resident, so the smallest unfinished
+// item is always held by a running CTA whose dependencies are complete.
+// Determinism: no floating-point atomics; every reduction order is fixed by the program, so the
+// result is bit-identical to the level-launch path whatever the CTA interleaving.
+#include "front_body.cuh"
+
+namespace gse {
+
+namespace {
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target) {
+    while (ld_acquire(p) < target) {}
+}
+// called by one thread after a CTA barrier that follows the item's last global write
+__device__ __forceinline__ void signal(unsigned* p) {
+    __threadfence();
+    atomicAdd(p, 1u);
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+    return t;
+}
+
+struct SpinWait {
+    const unsigned* ctr;
+    unsigned epoch;          // iteration + 1
+    unsigned acc_target;
+    unsigned long long* tr;  // trace slots of this item (debug) or nullptr
+    __device__ __forceinline__ void originals(const TaskRec& hdr) const {
+        // every thread acquires the counter itself (one L2 request per warp): no extra barrier
+        if (hdr.flags & 2) wait_ge(ctr + CTR_ACC, acc_target);
+        if (tr && threadIdx.x == 0) tr[1] = globaltimer();
+    }
+    __device__ __forceinline__ void children(const TaskRec& hdr, const ChildRec* cr) const {
+        for (int c = threadIdx.x; c < hdr.nchild; c += blockDim.x) {
+            wait_ge(ctr + CTR_FRONT0 + cr[c].front, (unsigned)cr[c].need * epoch);
+            if (tr) atomicMax(tr + 2, globaltimer());
+        }
+    }
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSolveThreads, 2)
+gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ FrontScratch S;
+    __shared__ int s_item, s_stop;
+    __shared__ unsigned long long s_red[kSolveThreads / 32];
+    __shared__ __align__(8) unsigned long long s_bar;      // mbarrier of the TMA bulk copies (accumulation items)
+    const int tid = threadIdx.x;
+    unsigned bar_parity = 0;
+    if (tid == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    unsigned* ctr = sp.ctr;
+    unsigned* fdone = ctr + CTR_FRONT0;
+    unsigned* bdone = fdone + sp.n_fronts;
+    const int o_acc = sp.n_eval_items, o_front = o_acc + sp.n_acc_items, o_bwd = o_front + sp.n_tasks,
+              o_upd = o_bwd + sp.n_btasks;
+    if (sp.stamps && blockIdx.x == 0 && tid == 0) sp.stamps[0] = globaltimer();
+#define GSE_STAMP(it, k) do { if (sp.stamps) atomicMax(sp.stamps + 1 + 8 * (it) + (k), globaltimer()); } while (0)
+
+    int known = 0;          // iterations [0, known) are complete and did not stop the loop
+    int final_it = 0;       // iterations performed when the loop stopped
+    int converged = 0, failed = 0;
+    for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(ctr + CTR_NEXT, 1u);
+        __syncthreads();
+        const int item = s_item;
+        const int it = min(item / sp.items_per_it, sp.max_it);
+        const int loc = item - it * sp.items_per_it;
+        // ---- iteration boundaries between `known` and `it`: has the loop stopped? ---------------
+        if (it > known) {
+            if (tid == 0) {
+                int stop = 0;
+                for (int j = known + 1; j <= it && !stop; ++j) {
+                    wait_ge(ctr + CTR_UPD, (unsigned)sp.n_upd_items * (unsigned)j);
+                    const unsigned long long e = ld_acquire64(sp.err);
+                    const double dv = __longlong_as_double((long long)ld_acquire64(sp.delta + (j - 1)));
+                    if (e != ~0ull) stop = 2 * 65536 + j;
+                    else if (dv < sp.tol) stop = 1 * 65536 + j;
+                    else if (j == sp.max_it) stop = 3 * 65536 + j;
+                }
+                s_stop = stop;
+            }
+            __syncthreads();
+            const int stop = s_stop;
+            if (stop) { final_it = stop & 65535; converged = (stop >> 16) == 1; failed = (stop >> 16) == 2; break; }
+            known = it;
+        }
+        const unsigned epoch = (unsigned)it + 1u;
+        unsigned long long* tr = sp.trace ? sp.trace + 8 * (size_t)item : nullptr;
+        if (tr && tid == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+            tr[0] = globaltimer(); tr[4] = smid | ((unsigned long long)blockIdx.x << 32);
+        }
+
+        if (loc < o_acc) {
+            // ---- template evaluation: one unit per thread ----------------------------------------
+            const int u = loc * kEvalPerItem + tid;
+            if (u < sp.n_units) eval_unit(ep, u, va, vm);
+            __syncthreads();
+            if (tid == 0) { signal(ctr + CTR_EVAL); GSE_STAMP(it, 0); }
+        } else if (loc < o_front) {
+            // ---- fused accumulation: one staged item (operands gathered to shared memory once) ----
+            wait_ge(ctr + CTR_EVAL, (unsigned)sp.n_eval_items * epoch);
+            if (tr && tid == 0) tr[2] = globaltimer();
+            const AccProg ap{sp.acc_items, sp.acc_uniq, sp.acc_ptr, sp.acc_pair, sp.val, sp.gval, sp.n_acc_items};
+            acc_item_staged(ap, loc - o_acc, sm, &s_bar, bar_parity, tr);
+            __syncthreads();
+            if (tr && tid == 0) tr[7] = globaltimer();
+            if (tid == 0) { signal(ctr + CTR_ACC); GSE_STAMP(it, 1); }
+        } else if (loc < o_bwd) {
+            // ---- multifrontal task -----------------------------------------------------------------
+            load_task_header(S, sp.tasks + (loc - o_front));
+            __syncthreads();
+            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr};
+            if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, nullptr, w);
+            else front_task_body<0>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, nullptr, w);
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(fdone + S.hdr.front, 1u);
+                atomicAdd(ctr + CTR_FWD, 1u);
+                GSE_STAMP(it, 1 + S.hdr.phase);
+            }
+        } else if (loc < o_upd) {
+            // ---- backward substitution task ---------------------------------------------------------
+            const BwdTask tk = sp.btasks[loc - o_bwd];
+            if (tid == 0) {
+                wait_ge(fdone + tk.front, (unsigned)tk.need * epoch);
+                if (tk.dep >= 0) wait_ge(bdone + tk.dep, epoch);
+            }
+            __syncthreads();
+            if (tr && tid == 0) tr[2] = globaltimer();
+            const bool solved = backward_body(*reinterpret_cast<BwdScratch*>(sm), tk, ft, sp.lbuf, sp.xsol, sp.bpart, sp.bcnt);
+            if (solved && tid == 0) {
+                __threadfence();
+                atomicAdd(bdone + tk.front, 1u);
+                atomicAdd(ctr + CTR_BWD, 1u);
+                GSE_STAMP(it, tk.phase == 3 ? 5 : 6);
+            }
+        } else {
+            // ---- state update + stacked infinity norm -----------------------------------------------
+            if (tid == 0) {
+                wait_ge(ctr + CTR_BWD, (unsigned)sp.n_bwd_fronts * epoch);
+                wait_ge(ctr + CTR_FWD, (unsigned)sp.n_tasks * epoch);
+                if (tr) tr[2] = globaltimer();
+            }
+            __syncthreads();
+            unsigned long long bits = 0ull;
+#pragma unroll
+            for (int k = 0; k < kUpdPerItem / kSolveThreads; ++k) {
+                const int v = (loc - o_upd) * kUpdPerItem + k * kSolveThreads + tid;
+                if (v < sp.n_upd) {
+                    const unsigned long long b = update_var(sp.upd_bus, sp.upd_quant, sp.upd_pos, v, sp.xsol, va, vm);
+                    bits = b > bits ? b : bits;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) { const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o); bits = other > bits ? other : bits; }
+            if ((tid & 31) == 0) s_red[tid >> 5] = bits;
+            __syncthreads();
+            if (tid == 0) {
+                for (int k = 1; k < kSolveThreads / 32; ++k) bits = s_red[k] > bits ? s_red[k] : bits;
+                if (bits) atomicMax(sp.delta + it, bits);
+                signal(ctr + CTR_UPD);
+                GSE_STAMP(it, 7);
+            }
+        }
+        if (tr && tid == 0) tr[3] = globaltimer();
+        __syncthreads();   // s_item / scratch are reused by the next item
+    }
+#undef GSE_STAMP
+
+    if (blockIdx.x == 0 && tid == 0) { sp.result[0] = final_it; sp.result[1] = converged; *sp.err_out = ld_acquire64(sp.err); }
+    if (failed) return;
+
+    // ---- objective J(x) at the final state: per-block partials, last CTA adds them in block order ----
+    double* red = sm;
+    const int nblk = (sp.n_rows + kSolveThreads - 1) / kSolveThreads;
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const int r = b * kSolveThreads + tid;
+        red[tid] = r < sp.n_rows ? objective_row(ep, sp.m_type, sp.m_target, sp.br_from, sp.br_to, r, va, vm) : 0.0;
+        __syncthreads();
+        for (int o = kSolveThreads / 2; o > 0; o >>= 1) {
+            if (tid < o) red[tid] += red[tid + o];
+            __syncthreads();
+        }
+        if (tid == 0) sp.obj_partial[b] = red[0];
+        __syncthreads();
+    }
+    if (tid == 0) { __threadfence(); s_item = atomicAdd(ctr + CTR_OBJ, 1u) == gridDim.x - 1; }
+    __syncthreads();
+    if (!s_item) return;
+    __threadfence();
+    double s = 0.0;
+    for (int i = tid; i < nblk; i += kSolveThreads) s += ldc(sp.obj_partial + i);
+    red[tid] = s;
+    __syncthreads();
+    for (int o = kSolveThreads / 2; o > 0; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    if (tid == 0) *sp.obj_out = red[0];
+}
+
+size_t solve_kernel_static_smem() {
+    cudaFuncAttributes a{};
+    if (cudaFuncGetAttributes(&a, gn_solve_kernel) != cudaSuccess) return 0;
+    return a.sharedSizeBytes;
+}
+
+int solve_kernel_max_ctas(size_t dyn_smem, int device) {
+    if (cudaFuncSetAttribute(gn_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem) != cudaSuccess) return 0;
+    int per_sm = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_solve_kernel, kSolveThreads, dyn_smem) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+    return per_sm * sms;
+}
+
+cudaError_t launch_solve(const SolveProg& sp, const EvalProg& ep, const FrontTab& ft, double* va, double* vm,
+                         int grid, size_t dyn_smem, cudaStream_t s) {
+    void* args[] = {(void*)&sp, (void*)&ep, (void*)&ft, (void*)&va, (void*)&vm};
+    return cudaLaunchCooperativeKernel((const void*)gn_solve_kernel, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
+}
+
+}  // namespace gse

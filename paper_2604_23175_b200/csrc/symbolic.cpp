@@ -18,6 +18,8 @@
 //     into it, in ascending row order -- the deterministic, atomic-free
 //     replacement of the five bincount scatters (assembly.py:502-520).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -159,6 +161,74 @@ void choose_chunks(Front& f, int TMAX) {
     int nch = (f.u1 + TMAX - 1) / TMAX;
     int T = round_up((f.u1 + nch - 1) / nch, 8);
     f.T = T; f.nch = (f.u1 + T - 1) / T;
+}
+
+// Staged accumulation program: the destination range is cut into items that one CTA processes
+// entirely out of shared memory.  Per item: the sorted list of distinct value indices (gathered
+// once), the item-local contribution pointers and, per contribution, the two positions in the
+// value list packed as (b << 16 | a).  The pointer and pair segments of an item are contiguous and
+// 16-byte aligned so that one TMA bulk copy each brings them on chip.  Items are sized so that
+// about one wave of CTAs covers the whole program (the persistent kernel keeps ~2 CTAs per SM
+// resident) within the staging limits kAccStageMax / kAccPairMax / kAccItemDestMax.
+void build_acc_items(HostProgram& hp) {
+    const int64_t n = hp.n_gval;
+    hp.acc_items.clear(); hp.acc_uniq.clear(); hp.acc_pair.clear(); hp.acc_lptr.clear();
+    hp.acc_stage_max = 0;
+    if (n == 0) return;
+    const int64_t target_items = 280;
+    int64_t dmax = (n + target_items - 1) / target_items;
+    dmax = std::min<int64_t>(std::max<int64_t>((dmax + 255) / 256 * 256, 256), kAccItemDestMax);
+    std::vector<int32_t> stamp((size_t)hp.n_val, -1), local((size_t)hp.n_val, 0), uniq;
+    auto pad4 = [](auto& v) { while (v.size() % 4) v.push_back(0); };
+    int64_t d0 = 0;
+    while (d0 < n) {
+        const int item = (int)(hp.acc_items.size() / 8);
+        uniq.clear();
+        int64_t d1 = d0;
+        while (d1 < n && d1 - d0 < dmax) {
+            // distinct values / pairs the next destination would add
+            const size_t before = uniq.size();
+            for (int q = hp.acc_ptr[d1]; q < hp.acc_ptr[d1 + 1]; ++q)
+                for (int32_t v : {hp.acc_a[q], hp.acc_b[q]})
+                    if (stamp[v] != item) { stamp[v] = item; uniq.push_back(v); }
+            if (((int)uniq.size() > kAccStageMax || hp.acc_ptr[d1 + 1] - hp.acc_ptr[d0] > kAccPairMax) && d1 > d0) {
+                for (size_t i = before; i < uniq.size(); ++i) stamp[uniq[i]] = -1;
+                uniq.resize(before);
+                break;
+            }
+            ++d1;
+        }
+        std::sort(uniq.begin(), uniq.end());
+        for (size_t i = 0; i < uniq.size(); ++i) local[uniq[i]] = (int32_t)i;
+        const int32_t q0 = hp.acc_ptr[d0], np = hp.acc_ptr[d1] - q0;
+        const int32_t pair_off = (int32_t)hp.acc_pair.size(), ptr_off = (int32_t)hp.acc_lptr.size(), uniq_off = (int32_t)hp.acc_uniq.size();
+        for (int q = q0; q < q0 + np; ++q) hp.acc_pair.push_back(((uint32_t)local[hp.acc_b[q]] << 16) | (uint32_t)local[hp.acc_a[q]]);
+        pad4(hp.acc_pair);
+        for (int64_t dd = d0; dd <= d1; ++dd) hp.acc_lptr.push_back(hp.acc_ptr[dd] - q0);
+        // processing order: destinations by decreasing contribution count, so that the threads of a
+        // warp (consecutive ranks) walk lists of similar length
+        {
+            std::vector<int32_t> ord((size_t)(d1 - d0));
+            std::iota(ord.begin(), ord.end(), 0);
+            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+                return hp.acc_ptr[d0 + x + 1] - hp.acc_ptr[d0 + x] > hp.acc_ptr[d0 + y + 1] - hp.acc_ptr[d0 + y]; });
+            hp.acc_lptr.insert(hp.acc_lptr.end(), ord.begin(), ord.end());
+        }
+        pad4(hp.acc_lptr);
+        hp.acc_uniq.insert(hp.acc_uniq.end(), uniq.begin(), uniq.end());
+        pad4(hp.acc_uniq);
+        const int32_t rec[8] = {(int32_t)d0, (int32_t)(d1 - d0), uniq_off, (int32_t)uniq.size(), pair_off, np, ptr_off, 0};
+        hp.acc_items.insert(hp.acc_items.end(), rec, rec + 8);
+        hp.acc_stage_max = std::max(hp.acc_stage_max, (int)uniq.size());
+        hp.acc_pair_max = std::max(hp.acc_pair_max, (int)np);
+        d0 = d1;
+    }
+    if (getenv("GSE_DEBUG_ACC")) {
+        int n_items = (int)(hp.acc_items.size() / 8), max_nd = 0, max_np = hp.acc_pair_max; double sum_nu = 0;
+        for (int i = 0; i < n_items; ++i) { max_nd = std::max(max_nd, hp.acc_items[8 * i + 1]); sum_nu += hp.acc_items[8 * i + 3]; }
+        fprintf(stderr, "acc items %d (dmax %lld): max dests %d, max pairs %d, max values %d, mean values %.0f, n_val %lld, n_gval %lld, pairs %zu\n",
+                n_items, (long long)dmax, max_nd, max_np, hp.acc_stage_max, sum_nu / std::max(n_items, 1), (long long)hp.n_val, (long long)n, hp.acc_a.size());
+    }
 }
 
 }  // namespace
@@ -307,6 +377,9 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                         u = unit_of_bus[tg] = (int)hp.inj_bus.size();
                         hp.inj_bus.push_back(tg); hp.inj_rowp.push_back(-1); hp.inj_rowq.push_back(-1);
                         hp.inj_slotp.push_back(-1); hp.inj_slotq.push_back(-1);
+                        int nth = 0;
+                        for (int p = d.y_ptr[tg]; p < d.y_ptr[tg + 1]; ++p) nth += d.y_idx[p] != d.slack;
+                        hp.inj_nth.push_back(nth);
                     }
                     if (t == 1) { if (hp.inj_rowp[u] >= 0) return "duplicate injection row"; hp.inj_rowp[u] = r; hp.inj_slotp[u] = gslot; }
                     else { if (hp.inj_rowq[u] >= 0) return "duplicate injection row"; hp.inj_rowq[u] = r; hp.inj_slotq[u] = gslot; }
@@ -372,7 +445,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 }
                 for (int x = s0; x < s1; ++x) {
                     int v = A.slot_var[x];
-                    rdest.push_back(v < ni ? o_bi + v : o_bbv + (v - ni)); ra.push_back((int32_t)(A.slot_base + x)); rb.push_back(-1);
+                    rdest.push_back(v < ni ? o_bi + v : o_bbv + (v - ni)); ra.push_back((int32_t)(A.slot_base + x)); rb.push_back(-(A.rows[k] + 1));
                 }
             }
         }
@@ -708,7 +781,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     int64_t lcur = 0;
     for (auto& f : hp.fronts) {
         if (f.kind != 1) { f.u_off = ucur; ucur += (int64_t)f.u1 * (f.u1 + 1) / 2; }
-        f.l_off = lcur; lcur += (int64_t)(f.p + f.u1) * f.p;
+        f.l_off = lcur; lcur += ((int64_t)(f.p + f.u1) * f.p + 1) & ~(int64_t)1;   // even: 16-byte cp.async of the pivot block
         hp.max_front = std::max(hp.max_front, f.p + f.u1);
         double p = f.p, u = f.u1;
         hp.dense_flops += p * p * p / 3.0 + p * p * u + p * u * u;
@@ -759,6 +832,12 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     }
 
     // ---- solver-layout accumulation program ---------------------------------------------
+    // Every contribution is a product val[a] * val[b] of the unified value array
+    // val = [g (n_slots) | w*g (n_slots) | w*r (n_rows)]: a indexes g, b indexes w*g (matrix
+    // entries) or w*r of the row (right-hand sides, collected above as -(row + 1)).
+    hp.n_val = 2 * hp.n_slots + m;
+    if (hp.n_val > 2147483647LL) return "value array exceeds int32 indexing";
+    auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(hp.n_slots + b) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
     {
         std::vector<int64_t> dest; std::vector<int32_t> pa, pb;
         for (int a = 0; a < K; ++a) {
@@ -785,7 +864,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 }
                 for (int x = s0; x < s1; ++x) {
                     int64_t dd = find(lp(A.slot_var[x]), nloc);
-                    dest.push_back(dd); pa.push_back((int32_t)(A.slot_base + x)); pb.push_back(-1);
+                    dest.push_back(dd); pa.push_back((int32_t)(A.slot_base + x)); pb.push_back(-(A.rows[k] + 1));
                 }
             }
         }
@@ -796,8 +875,9 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         for (int64_t i = 0; i < hp.n_gval; ++i) hp.acc_ptr[i + 1] += hp.acc_ptr[i];
         hp.acc_a.resize(dest.size()); hp.acc_b.resize(dest.size());
         std::vector<int32_t> cur(hp.acc_ptr.begin(), hp.acc_ptr.end() - 1);
-        for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = pa[i]; hp.acc_b[q] = pb[i]; }
+        for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = pa[i]; hp.acc_b[q] = val_index(pb[i]); }
     }
+    build_acc_items(hp);
     // ---- reference-layout program (component parity) ---------------------------------------
     {
         hp.n_ref_vals = hp.ref_off[K];
@@ -806,7 +886,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         for (int64_t i = 0; i < hp.n_ref_vals; ++i) hp.racc_ptr[i + 1] += hp.racc_ptr[i];
         hp.racc_a.resize(rdest.size()); hp.racc_b.resize(rdest.size());
         std::vector<int32_t> cur(hp.racc_ptr.begin(), hp.racc_ptr.end() - 1);
-        for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = ra[i]; hp.racc_b[q] = rb[i]; }
+        for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = ra[i]; hp.racc_b[q] = val_index(rb[i]); }
     }
 
     // ---- state update list ----------------------------------------------------------------

@@ -21,17 +21,19 @@ namespace {
 struct Sim {
     HostProgram hp;
     gse_problem_desc d;
-    std::vector<double> g, gw, wrg, gval, lbuf, ubuf, xsol, w;
+    std::vector<double> val, gval, lbuf, ubuf, xsol, w;   // val = [g | w*g | w*r]
     long long fail_code = -1;
 };
 
 inline int pad_ld(int p) { return ((p + 11) / 16) * 16 + 4; }
 
-void put(Sim& s, int slot, double gv, double w, double wr) { s.g[slot] = gv; s.gw[slot] = w * gv; s.wrg[slot] = wr * gv; }
+void put(Sim& s, int slot, double gv, double w, double) { s.val[slot] = gv; s.val[s.hp.n_slots + slot] = w * gv; }
+void put_wr(Sim& s, int row, double wr) { if (row >= 0) s.val[2 * s.hp.n_slots + row] = wr; }
 
 void flow_row(Sim& s, int row, int slot, bool fs, bool ts, double h, double a, double b, double c, double e) {
     if (row < 0) return;
     double w = s.w[row], wr = w * (s.d.m_z[row] - h);
+    put_wr(s, row, wr);
     if (!fs) put(s, slot++, a, w, wr);
     if (!ts) put(s, slot++, b, w, wr);
     put(s, slot++, c, w, wr); put(s, slot, e, w, wr);
@@ -63,6 +65,7 @@ void eval(Sim& s, const double* va, const double* vm) {
         double wp = rp >= 0 ? s.w[rp] : 0, wq = rq >= 0 ? s.w[rq] : 0;
         double hpv = vi * (vi * gd + sum_p), hq = vi * (-vi * bd + sum_q);
         double wrp = rp >= 0 ? wp * (d.m_z[rp] - hpv) : 0, wrq = rq >= 0 ? wq * (d.m_z[rq] - hq) : 0;
+        put_wr(s, rp, wrp); put_wr(s, rq, wrq);
         int cth = 0, dth = -1, dvm = -1;
         for (int p = p0, q = 0; p < p1; ++p, ++q) { int j = d.y_idx[p]; int thpos = j != d.slack ? cth++ : -1, vmpos = nth + q;
             if (j == i) { dth = thpos; dvm = vmpos; continue; }
@@ -74,13 +77,30 @@ void eval(Sim& s, const double* va, const double* vm) {
         if (rq >= 0) { if (dth >= 0) put(s, sq + dth, vi * sum_p, wq, wrq); put(s, sq + dvm, -2.0 * vi * bd + sum_q, wq, wrq); }
     }
     for (size_t u = 0; u < hp.vm_bus.size(); ++u) { int row = hp.vm_row[u]; double w = s.w[row];
-        put(s, hp.vm_slot[u], 1.0, w, w * (d.m_z[row] - vm[hp.vm_bus[u]])); }
+        put_wr(s, row, w * (d.m_z[row] - vm[hp.vm_bus[u]]));
+        put(s, hp.vm_slot[u], 1.0, w, 0.0); }
 }
 
 void accumulate(Sim& s, const std::vector<int32_t>& ptr, const std::vector<int32_t>& a, const std::vector<int32_t>& b, std::vector<double>& out) {
     for (size_t dd = 0; dd + 1 < ptr.size(); ++dd) { double acc = 0;
-        for (int q = ptr[dd]; q < ptr[dd + 1]; ++q) acc += b[q] < 0 ? s.wrg[a[q]] : s.g[a[q]] * s.gw[b[q]];
+        for (int q = ptr[dd]; q < ptr[dd + 1]; ++q) acc += s.val[a[q]] * s.val[b[q]];
         out[dd] = acc; }
+}
+
+// the staged form of the solver-layout program, item by item as the CUDA kernel walks it
+void accumulate_staged(Sim& s, std::vector<double>& out) {
+    const HostProgram& hp = s.hp;
+    std::vector<double> sv;
+    for (size_t it = 0; it * 8 < hp.acc_items.size(); ++it) {
+        const int32_t* r = &hp.acc_items[8 * it];
+        const int d0 = r[0], nd = r[1], u0 = r[2], nu = r[3], p0 = r[4], l0 = r[6];
+        sv.assign(nu, 0.0);
+        for (int i = 0; i < nu; ++i) sv[i] = s.val[hp.acc_uniq[u0 + i]];
+        for (int k = 0; k < nd; ++k) { double acc = 0;
+            const int dd = hp.acc_lptr[l0 + nd + 1 + k];   // processing order (a permutation of the item's destinations)
+            for (int q = hp.acc_lptr[l0 + dd]; q < hp.acc_lptr[l0 + dd + 1]; ++q) { uint32_t pr = hp.acc_pair[p0 + q]; acc += sv[pr & 0xffffu] * sv[pr >> 16]; }
+            out[d0 + dd] = acc; }
+    }
 }
 
 void run_task(Sim& s, const Task& tk, int fidx_unused = 0) {
@@ -152,7 +172,7 @@ void* hostsim_create(const gse_problem_desc* d, int dense, int leaf, int pmax, i
     std::string e = build_host_program(*d, bo, s->hp);
     if (!e.empty()) { snprintf(msg, msglen, "%s", e.c_str()); delete s; return nullptr; }
     const HostProgram& hp = s->hp;
-    s->g.assign(hp.n_slots, 0); s->gw.assign(hp.n_slots, 0); s->wrg.assign(hp.n_slots, 0);
+    s->val.assign(hp.n_val, 0);
     s->gval.assign(hp.n_gval, 0); s->lbuf.assign(hp.n_lbuf, 0); s->ubuf.assign(hp.n_ubuf, 0); s->xsol.assign(hp.n_pos + 2, 0);
     s->w.assign(d->m_w, d->m_w + d->n_rows);
     return s;
@@ -166,7 +186,7 @@ void hostsim_stats(void* h, double* out) { Sim* s = (Sim*)h; const HostProgram& 
 long long hostsim_iterate(void* h, double* va, double* vm, double* delta_inf) {
     Sim* s = (Sim*)h; const HostProgram& hp = s->hp; s->fail_code = -1;
     eval(*s, va, vm);
-    accumulate(*s, hp.acc_ptr, hp.acc_a, hp.acc_b, s->gval);
+    accumulate_staged(*s, s->gval);
     for (auto& lv : hp.fwd_levels) for (const Task& t : lv) run_task(*s, t);
     for (auto& lv : hp.bwd_levels) for (int f : lv) backward(*s, f);
     double dmax = 0;
