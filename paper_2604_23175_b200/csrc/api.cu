@@ -250,6 +250,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     if (const char* e = getenv("GSE_GAMMA_LEAF")) { int v = atoi(e); if (v >= 1) bo.gamma_leaf_buses = v; }
     if (const char* e = getenv("GSE_MAX_PIVOTS")) { int v = atoi(e); if (v == 32 || v == 64) bo.max_pivots = v; }
     if (const char* e = getenv("GSE_LEAF_BUSES")) { int v = atoi(e); if (v >= 1) bo.leaf_buses = v; }
+    if (const char* e = getenv("GSE_SPLIT_MIN")) { int v = atoi(e); if (v >= 1) bo.split_min_pivots = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;
     std::string msg = build_host_program(*d, bo, hp);
@@ -342,30 +343,34 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     size_t solve_task_smem = 0;
     // two passes: the tasks of the solve in level order first (the persistent kernel walks exactly
     // this prefix), then the readback-only boundary root of the block-sparse mode (phase 5)
+    // within a level: stage 0 = fused + panel tasks, stage 1 = update tasks (a separate launch on the
+    // level path: they read the panels stage 0 stored)
     for (int pass = 0; pass < 2; ++pass)
     for (size_t lv = 0; lv < hp.fwd_levels.size(); ++lv) {
-        for (int key : {11, 10, 21, 20, 31, 30, 51, 50}) {      // (phase, pivot class)
+        for (int skey : {11, 10, 21, 20, 31, 30, 51, 50, 111, 121, 131, 151}) {      // (stage, phase, pivot class)
+            const int key = skey % 100, stage = skey / 100;
             if ((key / 10 == 5) != (pass == 1)) continue;
             const int phase = key / 10, pclass = key % 10;
             LevelLaunch L{pclass, (int)trecs.size(), 0, 0, phase};
             for (const Task& t : hp.fwd_levels[lv]) {
                 const Front& f = hp.fronts[t.front];
                 const int cls = f.p == 0 ? 0 : 1;
-                if (cls != pclass || t.phase != phase) continue;
+                if (cls != pclass || t.phase != phase || (t.kind == 2) != (stage == 1)) continue;
                 const int T = std::max(f.T, 1);
                 const int ni = std::min(T, f.u1 - t.ci * T), nj = std::min(T, f.u1 - t.cj * T);
                 const bool diag = t.ci == t.cj;
+                const int kind = t.kind;
                 // chain fronts: single child, identity map, no original entries -> tile read in place
                 bool direct = f.kind == 3 && f.children.size() == 1 && f.n_orig == 0;
                 if (direct) {
                     const std::vector<int>& rel_c = hp.fronts[f.children[0]].rel;
                     for (size_t q = 0; q < rel_c.size() && direct; ++q) direct = rel_c[q] == (int)q;
                 }
-                L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, diag, direct));
+                L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, diag, direct, kind));
                 TaskRec r{};
                 r.front = t.front; r.ci = t.ci; r.cj = t.cj; r.p = f.p; r.u1 = f.u1; r.T = T;
                 r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = (direct ? 1 : 0) | (f.n_orig > 0 ? 2 : 0);
-                r.phase = phase;
+                r.phase = phase; r.kind = kind; r.nch = f.nch;
                 r.dinv_off = dinv_off[t.front];
                 const int32_t* rp = &hp.reg_ptr[hp.front_reg_off[t.front]];
                 const int ridI = (t.ci + 1) * (t.ci + 2) / 2, ridJ = (t.cj + 1) * (t.cj + 2) / 2;
@@ -386,8 +391,8 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                     cr.bI = lb(f.p + t.ci * T); cr.eI = lb(f.p + t.ci * T + ni);
                     cr.bJ = lb(f.p + t.cj * T); cr.eJ = lb(f.p + t.cj * T + nj);
                     cr.front = ch; cr.need = ntasks_of(ch);
-                    const bool hits_panel = f.p && cr.eP > 0;
-                    const bool hits_tile = !direct && cr.eI > cr.bI && cr.eJ > cr.bJ;
+                    const bool hits_panel = f.p && kind != 2 && cr.eP > 0;
+                    const bool hits_tile = !direct && kind != 1 && cr.eI > cr.bI && cr.eJ > cr.bJ;
                     if (!hits_panel && !hits_tile && !direct) continue;   // pruned (order of the rest is kept)
                     crecs.push_back(cr);
                     ++r.nchild;
@@ -419,7 +424,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
                 BwdTask bt{};
                 bt.front = f; bt.split = sp; bt.nsplit = ns; bt.pbase = pbase; bt.p = fr.p; bt.u = u;
                 bt.rows_off = frows_off[f]; bt.dinv_off = dinv_off[f]; bt.l_off = fr.l_off;
-                bt.dep = dep; bt.need = ntasks_of(f); bt.phase = hp.bwd_phase[i];
+                bt.dep = dep; bt.need = fr.nch; bt.phase = hp.bwd_phase[i];   // need: tasks that store a factor panel
                 btasks.push_back(bt);
             }
             pbase += ns; B.count += ns;
@@ -460,7 +465,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         sp.m_type = plan->m_type.ptr; sp.m_target = plan->m_target.ptr; sp.br_from = plan->br_from.ptr; sp.br_to = plan->br_to.ptr;
         sp.gval = plan->gval.ptr; sp.lbuf = plan->lbuf.ptr; sp.ubuf = plan->ubuf.ptr; sp.xsol = plan->xsol.ptr;
         sp.bpart = plan->bpart.ptr; sp.obj_partial = plan->obj_partial.ptr; sp.bcnt = plan->bcnt.ptr;
-        const size_t nctr = CTR_FRONT0 + 2 * nf;
+        const size_t nctr = CTR_FRONT0 + 3 * nf;
         plan->sync_bytes = sizeof(unsigned long long) * kBlkWords + sizeof(unsigned) * nctr;
         CU(plan->syncblk.alloc(kBlkWords + (nctr + 1) / 2));
         CU(cudaMallocHost(&plan->h_blk, sizeof(unsigned long long) * kBlkWords));
@@ -540,7 +545,7 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     cudaStream_t s = plan->stream;
     SolveProg sp = plan->sp;
     sp.max_it = max_it; sp.tol = cfg->convergence_tol;
-    if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 8 * (size_t)sp.items_per_it * 16, s));
+    if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 16 * (size_t)sp.items_per_it * 16, s));
     auto t0 = std::chrono::steady_clock::now();
     cudaEventRecord(plan->ev[6], s);
     CU(cudaMemsetAsync(plan->syncblk.ptr, 0, plan->sync_bytes, s));
@@ -789,11 +794,11 @@ int gse_profile_iteration(gse_plan* plan, double* va, double* vm, int32_t max_n,
 }
 
 // Debug: per-item stamps of the persistent kernel.  enable=1 arms tracing for the next solves (first
-// 16 iterations); enable=0 copies [items][8] words (pull, originals ready, children ready, end,
-// smid | cta << 32) to out and disarms.  Returns the items per iteration.
+// 16 iterations); enable=0 copies [items][16] words (pull, originals ready, children ready, end,
+// smid | cta << 32, ..., then the 8 phase stamps of a front task) to out and disarms.  Returns the items per iteration.
 int gse_debug_trace(gse_plan* plan, int enable, unsigned long long* out, int64_t max_words) {
     CU(cudaSetDevice(plan->device));
-    const size_t words = 8 * (size_t)plan->sp.items_per_it * 16;
+    const size_t words = 16 * (size_t)plan->sp.items_per_it * 16;
     if (enable) {
         if (!plan->trace.ptr) CU(plan->trace.alloc(words));
         plan->sp.trace = plan->trace.ptr;

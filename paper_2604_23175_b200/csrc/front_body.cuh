@@ -134,11 +134,20 @@ __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec*
 struct NoWait {
     __device__ __forceinline__ void originals(const TaskRec&) const {}
     __device__ __forceinline__ void children(const TaskRec&, const ChildRec*) const {}
+    __device__ __forceinline__ void panels(const TaskRec&) const {}
 };
 
 // One front task; S.hdr is loaded and visible to the whole CTA.  tb: optional 8 clock stamps.
+// Task kinds (TaskRec::kind):
+//   0 fused   -- assemble [pivots | I | J] + tile, factor, update, store (fronts with one row chunk
+//                or few pivots: recomputing the pivot block per task is cheaper than a hand-off);
+//   1 panel   -- assemble [pivots | I], factor the pivot block, solve chunk I against it and store
+//                its slice of the factor panel (ci == cj on the host side; no tile);
+//   2 update  -- assemble the tile, then read the finished panels L_I, L_J of the front back from
+//                the factor storage and run the trailing update (no pivot rows in shared memory).
 // wait.originals() runs before the first read of gval, wait.children() before the first read of a
-// child's update matrix (a CTA barrier follows it before any such read).
+// child's update matrix (it ends with a CTA barrier when it waited), wait.panels() before
+// the first read of the front's own factor panels (kind 2).
 template <int HAS_PIVOTS, class Wait>
 __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, const FrontTab& ft, const double* gval,
                                                 double* lbuf, double* ubuf, unsigned long long* err, long long* tb,
@@ -151,16 +160,19 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     double* s_rinv = S.rinv;
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
-#define GSE_TICK(k) do { if (tb && tid == 0) tb[k] = clock64(); } while (0)
+#define GSE_TICK(k) do { if (tb && tid == 0) tb[k] = (long long)gtimer(); } while (0)   // globaltimer, ns
     GSE_TICK(0);
     const int f = hdr.front, ci = hdr.ci, cj = hdr.cj;
     const int p = HAS_PIVOTS ? hdr.p : 0;
     const int u1 = hdr.u1, T = hdr.T;
     const int i0 = ci * T, ni = min(T, u1 - i0), j0 = cj * T, nj = min(T, u1 - j0);
     const bool diag = ci == cj;
+    const int kind = HAS_PIVOTS ? hdr.kind : 0;
+    const bool no_tile = kind == 1;
     const bool direct = (hdr.flags & 1) != 0;      // tile comes straight from the single child's U
+    const int pp = kind == 2 ? 0 : p;              // pivot rows assembled and factored by this task
     const int ld = pad_ld(p);
-    const int rp = p ? round8(p) : 0, ri = p ? round8(ni) : 0, rj = (p && !diag) ? round8(nj) : 0;
+    const int rp = pp ? round8(pp) : 0, ri = p ? round8(ni) : 0, rj = (p && !diag) ? round8(nj) : 0;
     const int ldt = round8(nj) | 1;
     double* pan = sm;
     double* tile = sm + (size_t)(rp + ri + rj) * ld;
@@ -170,12 +182,12 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         reinterpret_cast<int4*>(crec)[tid] = reinterpret_cast<const int4*>(ft.crecs + hdr.child_off)[tid];
 
     {
-        const int total = ((rp + ri + rj) * ld + (direct ? 0 : round8(ni) * ldt) + 1) >> 1;
+        const int total = ((rp + ri + rj) * ld + ((direct || no_tile) ? 0 : round8(ni) * ldt) + 1) >> 1;
         double2* z2 = reinterpret_cast<double2*>(sm);
         for (int t = tid; t < total; t += nth) z2[t] = make_double2(0.0, 0.0);
     }
     __syncthreads();
-    if (HAS_PIVOTS && tid < rp - p) pan[(p + tid) * ld + p + tid] = 1.0;   // identity on padded pivots
+    if (HAS_PIVOTS && pp && tid < rp - p) pan[(p + tid) * ld + p + tid] = 1.0;   // identity on padded pivots
     GSE_TICK(1);
 
     // ---- original entries (written by accumulate_kernel into gval), four loads in flight ------
@@ -198,19 +210,20 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                     if (e0 + k * nth < e) dst[((int)(q[k] >> 16) - rsub) * ldd + ((int)(q[k] & 0xffffu) - csub)] = v[k];
             }
         };
-        if (p) {
+        if (pp) {
             scatter(hdr.reg[0], hdr.reg[1], pan, ld, 0, 0);
             scatter(hdr.reg[2], hdr.reg[3], pan + (size_t)rp * ld, ld, p + i0, 0);
             if (!diag) scatter(hdr.reg[4], hdr.reg[5], pan + (size_t)(rp + ri) * ld, ld, p + j0, 0);
         }
-        scatter(hdr.reg[6], hdr.reg[7], tile, ldt, p + i0, p + j0);
+        if (!no_tile) scatter(hdr.reg[6], hdr.reg[7], tile, ldt, p + i0, p + j0);
     }
     __syncthreads();
     GSE_TICK(2);
 
     // ---- extend-add of the children's update matrices, fixed child order (gather form) -------
     // (the child list of a task is pruned on the host to the children that reach its regions)
-    wait.children(hdr, ft.crecs + hdr.child_off);
+    // (everything static -- child records, row maps -- is staged BEFORE waiting for the children, so
+    // that only the loads of their update matrices follow the hand-off)
     for (int cb0 = 0; cb0 < nchild; cb0 += kGatherBatch) {
         const int nb = min(kGatherBatch, nchild - cb0);
         const int Rp = rp + ri + rj;
@@ -226,7 +239,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         for (int c = 0; c < nb; ++c) {
             const ChildRec& cr = crec[cbase + c];
             const int32_t* rel = ft.rel + cr.rel_off;
-            const int eP = p ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = diag ? 0 : cr.eJ - cr.bJ;
+            const int eP = pp ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = diag ? 0 : cr.eJ - cr.bJ;
             for (int t = tid; t < eP + nI + nJ; t += nth) {
                 if (t < eP) s_inv[c][rel[t]] = t;
                 else if (t < eP + nI) { const int i = cr.bI + t - eP; s_inv[c][rp + rel[i] - p - i0] = i; }
@@ -234,8 +247,8 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
             }
         }
         __syncthreads();
-        if (cb0 == 0) GSE_TICK(7);
-        GatherArgs ga{pan, tile, &s_inv[0][0], ubuf, p, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, direct ? 1 : 0, warp, lane, nwarps};
+        if (cb0 == 0) { GSE_TICK(7); wait.children(hdr, ft.crecs + hdr.child_off); }
+        GatherArgs ga{pan, tile, &s_inv[0][0], ubuf, pp, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
         const ChildRec* cb = crec + cbase;
         switch (nb) {
             case 1: gather_batch<1>(ga, cb); break;
@@ -252,7 +265,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     // registers and publishes it while the other warps update the remaining row tiles on the tensor
     // pipe (look-ahead); then every row solves against the published block (right-looking:
     // independent FMAs).  Two barriers per 8 pivots.
-    if (HAS_PIVOTS && p) {
+    if (HAS_PIVOTS && pp) {
         const int R = rp + ri + rj;                 // padded rows: [pivots | chunk I | chunk J]
         const int ntile = R >> 3;
         for (int kb = 0; kb < rp; kb += 8) {
@@ -360,9 +373,35 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     }
     GSE_TICK(4);
 
+    // ---- update tasks: the front's finished panels come back from the factor storage -----------
+    if (HAS_PIVOTS && kind == 2) {
+        wait.panels(hdr);
+        const double* L = lbuf + hdr.l_off;
+        const int nrow = ni + (diag ? 0 : nj);
+        // one warp per row, six rows (twelve independent loads per lane) in flight
+        for (int rb = warp; rb < nrow; rb += 6 * nwarps) {
+            double v[6][2];
+#pragma unroll
+            for (int g = 0; g < 6; ++g) {
+                const int r = rb + g * nwarps;
+                const double* src = L + (size_t)(p + (r < ni ? i0 + r : j0 + r - ni)) * p;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) v[g][h] = (r < nrow && lane + 32 * h < p) ? ldc(src + lane + 32 * h) : 0.0;
+            }
+#pragma unroll
+            for (int g = 0; g < 6; ++g) {
+                const int r = rb + g * nwarps;
+                double* dst = pan + (size_t)(r < ni ? r : ri + r - ni) * ld;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) if (r < nrow && lane + 32 * h < p) dst[lane + 32 * h] = v[g][h];
+            }
+        }
+        __syncthreads();
+    }
+
     // ---- trailing update on the FP64 tensor pipe: U_IJ = F_IJ - L_I L_J^T -------------------
-    {
-        const double* Pi = pan + (size_t)rp * ld;
+    const double* Pi = pan + (size_t)rp * ld;
+    if (!no_tile) {
         const double* Pj = diag ? Pi : pan + (size_t)(rp + ri) * ld;
         const int nbi = round8(ni) >> 3, nbj = round8(nj) >> 3;
         const int ngj = (nbj + 3) >> 2;                 // groups of four 8-wide column blocks
@@ -414,9 +453,11 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                 }
             }
         }
-        GSE_TICK(5);
+    }
+    GSE_TICK(5);
+    {
         // ---- factor panel to global (diagonal tasks own their row chunk) ----------------------
-        if (HAS_PIVOTS && p && diag) {
+        if (HAS_PIVOTS && pp && diag) {
             double* L = lbuf + hdr.l_off;
             if (ci == 0) {
                 for (int r = warp; r < p; r += nwarps)

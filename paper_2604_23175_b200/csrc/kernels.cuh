@@ -28,7 +28,8 @@ struct TaskRec {                                      // 128 bytes
     int64_t gval_off, l_off, u_off;
     int32_t flags, dinv_off;                          // flags bit 0: tile read directly from the single child's U;
                                                       //       bit 1: the front has original entries (waits for the accumulation)
-    int32_t phase, pad[7];                            // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
+    int32_t phase, kind, nch, pad[5];                 // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
+                                                      // kind: 0 fused, 1 panel, 2 update (front_body.cuh); nch: row chunks of the front
 };
 // One child of a task (children that do not reach the task's regions are pruned on the host).
 // front / need: dataflow dependency -- the child is complete when its counter reaches need per iteration.
@@ -60,11 +61,11 @@ inline __host__ __device__ int pad_ld(int p) { return ((((p + 7) & ~7) + 11) / 1
 inline __host__ __device__ int round8(int x) { return (x + 7) & ~7; }
 
 // shared-memory doubles needed by one front task
-inline __host__ __device__ size_t task_smem_doubles(int p, int ni, int nj, bool diag, bool direct = false) {
+inline __host__ __device__ size_t task_smem_doubles(int p, int ni, int nj, bool diag, bool direct = false, int kind = 0) {
     size_t ld = pad_ld(p);
-    size_t rows = (p ? round8(p) : 0) + (p ? round8(ni) : 0) + ((p && !diag) ? round8(nj) : 0);
+    size_t rows = ((p && kind != 2) ? round8(p) : 0) + (p ? round8(ni) : 0) + ((p && !diag) ? round8(nj) : 0);
     size_t ldt = (size_t)(round8(nj) | 1);
-    return rows * ld + (direct ? 0 : (size_t)round8(ni) * ldt) + 16;
+    return rows * ld + ((direct || kind == 1) ? 0 : (size_t)round8(ni) * ldt) + 16;
 }
 
 void launch_eval(const EvalProg& ep, const double* va, const double* vm, cudaStream_t s);
@@ -103,6 +104,8 @@ cudaError_t configure_unit_kernels();
 constexpr int kSolveThreads = 256;
 constexpr int kEvalPerItem = 256, kUpdPerItem = 1024;
 enum { CTR_NEXT = 0, CTR_EVAL = 32, CTR_ACC = 64, CTR_FWD = 96, CTR_BWD = 128, CTR_UPD = 160, CTR_OBJ = 192, CTR_FRONT0 = 224 };
+// per-front counters after CTR_FRONT0: fdone[n_fronts] (tasks that wrote U), pdone[n_fronts] (tasks that
+// stored a factor panel), bdone[n_fronts] (backward solves)
 struct SolveProg {
     int32_t n_eval_items, n_acc_items, n_tasks, n_btasks, n_upd_items, items_per_it;
     int32_t n_units, n_upd, n_bwd_fronts, n_fronts, n_rows, max_it;
@@ -117,7 +120,7 @@ struct SolveProg {
     const int32_t *m_type, *m_target, *br_from, *br_to;
     double *gval, *lbuf, *ubuf, *xsol, *bpart, *obj_partial;   // obj_partial[nblocks] then the total
     int32_t* bcnt;
-    unsigned int* ctr;            // CTR_* globals, then fdone[n_fronts], bdone[n_fronts]
+    unsigned int* ctr;            // CTR_* globals, then fdone / pdone / bdone [n_fronts] each
     unsigned long long* delta;    // [64] per-iteration |dx| max as ordered bits
     unsigned long long* err;      // failure code (min), ~0 = none
     unsigned long long* stamps;   // optional [1 + 64 * 8] globaltimer stamps (nullptr: off)

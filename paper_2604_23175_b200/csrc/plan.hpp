@@ -35,7 +35,7 @@ struct Front {
     int n_orig = 0;
 };
 
-struct Task { int front, ci, cj, phase; };
+struct Task { int front, ci, cj, phase, kind; };   // kind: 0 fused, 1 panel, 2 update (front_body.cuh)
 
 struct HostProgram {
     // sizes
@@ -113,6 +113,7 @@ struct BuildOptions {
     int max_pivots = 64;
     int boundary_mode = 0;     // 0 auto (tree when n_Gamma > 192), 1 dense chain, 2 tree
     int gamma_leaf_buses = 16; // nested-dissection leaf of the boundary tree, in boundary buses
+    int split_min_pivots = 32; // fronts with several row chunks and at least this many pivots run as panel + update tasks
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;

@@ -32,8 +32,11 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// Spin until *p >= target.  Called by ONE thread per dependency (the rest of the CTA parks on a
+// barrier, which costs no issue slots); the back-off keeps a waiting CTA from stealing load/store
+// bandwidth from the CTA it shares the SM with -- often the very producer it is waiting for.
 __device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target) {
-    while (ld_acquire(p) < target) {}
+    while (ld_acquire(p) < target) __nanosleep(40);
 }
 // called by one thread after a CTA barrier that follows the item's last global write
 __device__ __forceinline__ void signal(unsigned* p) {
@@ -51,16 +54,25 @@ struct SpinWait {
     unsigned epoch;          // iteration + 1
     unsigned acc_target;
     unsigned long long* tr;  // trace slots of this item (debug) or nullptr
+    int n_fronts;
     __device__ __forceinline__ void originals(const TaskRec& hdr) const {
-        // every thread acquires the counter itself (one L2 request per warp): no extra barrier
-        if (hdr.flags & 2) wait_ge(ctr + CTR_ACC, acc_target);
-        if (tr && threadIdx.x == 0) tr[1] = globaltimer();
+        if (!(hdr.flags & 2)) return;
+        if (threadIdx.x == 0) { wait_ge(ctr + CTR_ACC, acc_target); if (tr) tr[1] = globaltimer(); }
+        __syncthreads();
+    }
+    __device__ __forceinline__ void panels(const TaskRec& hdr) const {
+        if (threadIdx.x == 0) {
+            wait_ge(ctr + CTR_FRONT0 + n_fronts + hdr.front, (unsigned)hdr.nch * epoch);
+            if (tr) tr[5] = globaltimer();
+        }
+        __syncthreads();
     }
     __device__ __forceinline__ void children(const TaskRec& hdr, const ChildRec* cr) const {
         for (int c = threadIdx.x; c < hdr.nchild; c += blockDim.x) {
             wait_ge(ctr + CTR_FRONT0 + cr[c].front, (unsigned)cr[c].need * epoch);
             if (tr) atomicMax(tr + 2, globaltimer());
         }
+        __syncthreads();
     }
 };
 
@@ -79,7 +91,8 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
     __syncthreads();
     unsigned* ctr = sp.ctr;
     unsigned* fdone = ctr + CTR_FRONT0;
-    unsigned* bdone = fdone + sp.n_fronts;
+    unsigned* pdone = fdone + sp.n_fronts;
+    unsigned* bdone = pdone + sp.n_fronts;
     const int o_acc = sp.n_eval_items, o_front = o_acc + sp.n_acc_items, o_bwd = o_front + sp.n_tasks,
               o_upd = o_bwd + sp.n_btasks;
     if (sp.stamps && blockIdx.x == 0 && tid == 0) sp.stamps[0] = globaltimer();
@@ -114,7 +127,7 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             known = it;
         }
         const unsigned epoch = (unsigned)it + 1u;
-        unsigned long long* tr = sp.trace ? sp.trace + 8 * (size_t)item : nullptr;
+        unsigned long long* tr = sp.trace ? sp.trace + 16 * (size_t)item : nullptr;
         if (tr && tid == 0) {
             unsigned smid;
             asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
@@ -129,8 +142,8 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             if (tid == 0) { signal(ctr + CTR_EVAL); GSE_STAMP(it, 0); }
         } else if (loc < o_front) {
             // ---- fused accumulation: one staged item (operands gathered to shared memory once) ----
-            wait_ge(ctr + CTR_EVAL, (unsigned)sp.n_eval_items * epoch);
-            if (tr && tid == 0) tr[2] = globaltimer();
+            if (tid == 0) { wait_ge(ctr + CTR_EVAL, (unsigned)sp.n_eval_items * epoch); if (tr) tr[2] = globaltimer(); }
+            __syncthreads();
             const AccProg ap{sp.acc_items, sp.acc_uniq, sp.acc_ptr, sp.acc_pair, sp.val, sp.gval, sp.n_acc_items};
             acc_item_staged(ap, loc - o_acc, sm, &s_bar, bar_parity, tr);
             __syncthreads();
@@ -140,13 +153,19 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             // ---- multifrontal task -----------------------------------------------------------------
             load_task_header(S, sp.tasks + (loc - o_front));
             __syncthreads();
-            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr};
-            if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, nullptr, w);
-            else front_task_body<0>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, nullptr, w);
+            if (tr && tid == 0) {
+                tr[6] = (unsigned long long)S.hdr.kind | ((unsigned long long)S.hdr.front << 8) | ((unsigned long long)S.hdr.ci << 32) | ((unsigned long long)S.hdr.cj << 48);
+                tr[7] = (unsigned long long)S.hdr.p | ((unsigned long long)S.hdr.u1 << 16) | ((unsigned long long)S.hdr.nchild << 32) | ((unsigned long long)S.hdr.phase << 48);
+            }
+            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr, sp.n_fronts};
+            if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
+            else front_task_body<0>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
             __syncthreads();
             if (tid == 0) {
                 __threadfence();
-                atomicAdd(fdone + S.hdr.front, 1u);
+                const int kind = S.hdr.p ? S.hdr.kind : 0;
+                if (kind != 2 && S.hdr.p && S.hdr.ci == S.hdr.cj) atomicAdd(pdone + S.hdr.front, 1u);
+                if (kind != 1) atomicAdd(fdone + S.hdr.front, 1u);
                 atomicAdd(ctr + CTR_FWD, 1u);
                 GSE_STAMP(it, 1 + S.hdr.phase);
             }
@@ -154,7 +173,7 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             // ---- backward substitution task ---------------------------------------------------------
             const BwdTask tk = sp.btasks[loc - o_bwd];
             if (tid == 0) {
-                wait_ge(fdone + tk.front, (unsigned)tk.need * epoch);
+                wait_ge(pdone + tk.front, (unsigned)tk.need * epoch);
                 if (tk.dep >= 0) wait_ge(bdone + tk.dep, epoch);
             }
             __syncthreads();

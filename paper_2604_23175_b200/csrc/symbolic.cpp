@@ -813,11 +813,17 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         if (f.area >= 0 && !hp.owned[f.area]) continue;
         // phase 1 local_condense, 2 boundary_assemble, 3 boundary_solve, 5 readback-only boundary root
         const int phase = f.kind <= 1 ? 1 : f.kind == 2 ? (sparse_gamma ? 5 : 2) : 3;
-        for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj, phase});
+        // wide fronts: one panel task per row chunk (factor + solve, stored) and one update task per
+        // tile (reads the stored panels) instead of tasks that each redo the pivot block
+        const bool split = f.p > 0 && f.nch >= 2 && f.p >= opt.split_min_pivots;
+        if (split) for (int ci = 0; ci < f.nch; ++ci) hp.fwd_levels[f.level].push_back({(int)fi, ci, ci, phase, 1});
+        for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj, phase, split ? 2 : 0});
         hp.level_phase[f.level] = phase;
     }
+    // within a level: panel and fused tasks (largest first), then the update tasks
     for (auto& lv : hp.fwd_levels)
         std::stable_sort(lv.begin(), lv.end(), [&](const Task& x, const Task& y) {
+            if ((x.kind == 2) != (y.kind == 2)) return y.kind == 2;
             const Front& a = hp.fronts[x.front]; const Front& b = hp.fronts[y.front];
             return (int64_t)a.p * (a.p + a.u1) > (int64_t)b.p * (b.p + b.u1); });
     for (int lv = n_levels - 1; lv >= 0; --lv) {

@@ -109,15 +109,16 @@ void run_task(Sim& s, const Task& tk, int fidx_unused = 0) {
     const int p = f.p, u1 = f.u1, T = std::max(f.T, 1), ci = tk.ci, cj = tk.cj;
     const int i0 = ci * T, ni = std::min(T, u1 - i0), j0 = cj * T, nj = std::min(T, u1 - j0);
     const bool diag = ci == cj; const int ld = pad_ld(p);
+    const int kind = tk.kind;   // 0 fused, 1 panel (factor + solve chunk I, store), 2 update (panels read back from lbuf)
     std::vector<double> PP((size_t)p * ld, 0.0), PI((size_t)ni * ld, 0.0), PJ((size_t)(diag ? 0 : nj) * ld, 0.0), tile((size_t)ni * nj, 0.0);
     const int32_t* rptr = &hp.reg_ptr[hp.front_reg_off[tk.front]];
     auto region = [&](int rid, auto&& fn) { for (int e = rptr[rid]; e < rptr[rid + 1]; ++e) { uint32_t q = hp.orig_pos[f.gval_off + e]; fn((int)(q >> 16), (int)(q & 0xffff), s.gval[f.gval_off + e]); } };
-    if (p) {
+    if (p && kind != 2) {
         region(0, [&](int lr, int lc, double v) { PP[(size_t)lr * ld + lc] = v; });
         region((ci + 1) * (ci + 2) / 2, [&](int lr, int lc, double v) { PI[(size_t)(lr - p - i0) * ld + lc] = v; });
         if (!diag) region((cj + 1) * (cj + 2) / 2, [&](int lr, int lc, double v) { PJ[(size_t)(lr - p - j0) * ld + lc] = v; });
     }
-    region((ci + 1) * (ci + 2) / 2 + cj + 1, [&](int lr, int lc, double v) { tile[(size_t)(lr - p - i0) * nj + (lc - p - j0)] = v; });
+    if (kind != 1) region((ci + 1) * (ci + 2) / 2 + cj + 1, [&](int lr, int lc, double v) { tile[(size_t)(lr - p - i0) * nj + (lc - p - j0)] = v; });
     for (size_t cx = 0; cx < f.children.size(); ++cx) {
         const int ch = f.children[cx];
         const Front& c = hp.fronts[ch];
@@ -127,10 +128,15 @@ void run_task(Sim& s, const Task& tk, int fidx_unused = 0) {
         int eP = lb(p), bI = lb(p + i0), eI = lb(p + i0 + ni), bJ = lb(p + j0), eJ = lb(p + j0 + nj);
         auto add = [&](int r0, int r1, int c0, int c1, double* dst, int ldd, int rs, int cs) {
             for (int i = r0; i < r1; ++i) for (int j = c0; j < c1 && j <= i; ++j) dst[(size_t)(rel[i] - rs) * ldd + (rel[j] - cs)] += U[(size_t)i * (i + 1) / 2 + j]; };
-        if (p) { add(0, eP, 0, eP, PP.data(), ld, 0, 0); add(bI, eI, 0, eP, PI.data(), ld, p + i0, 0); if (!diag) add(bJ, eJ, 0, eP, PJ.data(), ld, p + j0, 0); }
-        add(bI, eI, bJ, eJ, tile.data(), nj, p + i0, p + j0);
+        if (p && kind != 2) { add(0, eP, 0, eP, PP.data(), ld, 0, 0); add(bI, eI, 0, eP, PI.data(), ld, p + i0, 0); if (!diag) add(bJ, eJ, 0, eP, PJ.data(), ld, p + j0, 0); }
+        if (kind != 1) add(bI, eI, bJ, eJ, tile.data(), nj, p + i0, p + j0);
     }
-    if (p) {   // left-looking row Cholesky over [PP; PI; PJ]
+    if (p && kind == 2) {   // the front's stored panels
+        const double* L = &s.lbuf[f.l_off];
+        for (int r = 0; r < ni; ++r) for (int k = 0; k < p; ++k) PI[(size_t)r * ld + k] = L[(size_t)(p + i0 + r) * p + k];
+        if (!diag) for (int r = 0; r < nj; ++r) for (int k = 0; k < p; ++k) PJ[(size_t)r * ld + k] = L[(size_t)(p + j0 + r) * p + k];
+    }
+    if (p && kind != 2) {   // left-looking row Cholesky over [PP; PI; PJ]
         auto row = [&](int r) -> double* { return r < p ? &PP[(size_t)r * ld] : r < p + ni ? &PI[(size_t)(r - p) * ld] : &PJ[(size_t)(r - p - ni) * ld]; };
         const int R = p + ni + (diag ? 0 : nj);
         for (int k = 0; k < p; ++k) {
@@ -144,10 +150,10 @@ void run_task(Sim& s, const Task& tk, int fidx_unused = 0) {
     }
     double* U = &s.ubuf[f.u_off];
     const std::vector<double>& PJJ = diag ? PI : PJ;
-    for (int i = 0; i < ni; ++i) for (int j = 0; j < nj; ++j) { int I = i0 + i, J = j0 + j; if (J > I) continue;
+    if (kind != 1) for (int i = 0; i < ni; ++i) for (int j = 0; j < nj; ++j) { int I = i0 + i, J = j0 + j; if (J > I) continue;
         double acc = 0; for (int k = 0; k < p; ++k) acc += PI[(size_t)i * ld + k] * PJJ[(size_t)j * ld + k];
         U[(size_t)I * (I + 1) / 2 + J] = tile[(size_t)i * nj + j] - acc; }
-    if (p && diag) { double* L = &s.lbuf[f.l_off];
+    if (p && diag && kind != 2) { double* L = &s.lbuf[f.l_off];
         if (ci == 0) for (int r = 0; r < p; ++r) for (int k = 0; k < p; ++k) L[(size_t)r * p + k] = PP[(size_t)r * ld + k];
         for (int r = 0; r < ni; ++r) for (int k = 0; k < p; ++k) L[(size_t)(p + i0 + r) * p + k] = PI[(size_t)r * ld + k]; }
 }

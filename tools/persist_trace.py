@@ -27,9 +27,9 @@ L.gse_solve_layout(est.plan._h, lay.ctypes.data_as(C.c_void_p))
 n_eval, n_acc, n_task, n_bwd, n_upd, grid, smem, persistent = (int(v) for v in lay)
 per_it = L.gse_debug_trace(est.plan._h, 1, None, 0)
 state, rep = est.estimate()
-tr = np.zeros(per_it * 16 * 8, dtype=np.uint64)
+tr = np.zeros(per_it * 16 * 16, dtype=np.uint64)
 L.gse_debug_trace(est.plan._h, 0, tr.ctypes.data_as(C.c_void_p), tr.size)
-tr = tr.reshape(-1, 8).astype(np.int64)
+tr = tr.reshape(-1, 16).astype(np.int64)
 print(f"{name}: persistent={persistent} grid={grid} smem={smem} items/it={per_it} "
       f"(eval {n_eval}, acc {n_acc}, front {n_task}, bwd {n_bwd}, upd {n_upd}); iterations={rep.iterations} "
       f"gpu_s={est.last_gpu_s*1e3:.3f} ms")
@@ -60,6 +60,35 @@ for it in range(rep.iterations):
         s0 = blk[:, 0].min()
         for i in range(0, len(b), step):
             print(f"     {i:5d}: {(b[i,0]-s0)/1e3:7.1f} {(max(b[i,1],b[i,2],b[i,0])-s0)/1e3:7.1f} {(b[i,3]-s0)/1e3:7.1f}  sm {b[i,4] & 0xffff}")
+        # per front: when its children were ready, when panels / updates finished
+        fr = {}
+        for i in range(len(b)):
+            kind = int(b[i, 6] & 0xff); f = int((b[i, 6] >> 8) & 0xffffff); pv = int(b[i, 7] & 0xffff); u1 = int((b[i, 7] >> 16) & 0xffff)
+            nchild = int((b[i, 7] >> 32) & 0xffff)
+            d = fr.setdefault(f, dict(p=pv, u1=u1, kinds=set(), n=0, ready=[], pend=[], uend=[], nchild=0, pull=[], pready=[]))
+            d["kinds"].add(kind); d["n"] += 1; d["nchild"] = max(d["nchild"], nchild)
+            d["pull"].append(b[i, 0] - s0)
+            d["ready"].append(max(b[i, 1], b[i, 2], b[i, 0]) - s0)
+            (d["pend"] if kind == 1 else d["uend"]).append(b[i, 3] - s0)
+            if kind == 2: d["pready"].append(b[i, 5] - s0)
+        print("   fronts by completion (front: p u1 tasks kinds nchild | children ready(max)  panels end(max)  panel-wait end(max)  all end(max)  last pull):")
+        items = sorted(fr.items(), key=lambda kv: max(kv[1]["uend"] or kv[1]["pend"]))
+        for f, d in items[-45:]:
+            print(f"     {f:5d}: {d['p']:3d} {d['u1']:4d} {d['n']:4d} {sorted(d['kinds'])} {d['nchild']:3d} | {max(d['ready'])/1e3:7.1f} "
+                  f"{(max(d['pend']) if d['pend'] else 0)/1e3:7.1f} {(max(d['pready']) if d['pready'] else 0)/1e3:7.1f} {max(d['uend'] or d['pend'])/1e3:7.1f} {max(d['pull'])/1e3:7.1f}")
+        # phase breakdown (us) of the tasks on the critical chain: stamps 8.. = start, zero, orig, gather end, panel end,
+        # update end, store end, inv-map built
+        print("   task phases (front kind ci cj | zero orig invmap [child wait] gather panel [panel wait+load] update store signal):")
+        for f, d in items[-14:]:
+            for i in range(len(b)):
+                if int((b[i, 6] >> 8) & 0xffffff) != f: continue
+                kind = int(b[i, 6] & 0xff); ci = int((b[i, 6] >> 32) & 0xffff); cj = int((b[i, 6] >> 48) & 0xffff)
+                if ci > 1 or cj > 0 and kind != 2: continue
+                st = b[i, 8:16]
+                cw = max(b[i, 2], st[7]) if b[i, 2] else st[7]
+                pw = b[i, 5] if kind == 2 else st[4]
+                print(f"     {f:5d} k{kind} {ci},{cj} | {(st[1]-st[0])/1e3:5.1f} {(st[2]-st[1])/1e3:5.1f} {(st[7]-st[2])/1e3:5.1f} [{(cw-st[7])/1e3:5.1f}] "
+                      f"{(st[3]-cw)/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} [{(pw-st[4])/1e3:5.1f}] {(st[5]-pw)/1e3:5.1f} {(st[6]-st[5])/1e3:5.1f} {(b[i,3]-st[6])/1e3:5.1f}")
         b = blk[bounds[3]:bounds[4]]
         step = max(1, len(b) // 25)
         print("   backward wavefront:")
