@@ -210,37 +210,51 @@ def run_gpu(args):
     value = iters / tot_dev
     e2e_value = it_per_solve * args.steps / tot_e2e
 
-    # ---- per-phase device times (CUDA events on the plan's stream, ungraphed pass) ----------------
+    # ---- roofline of the dominant kernel -------------------------------------------------------------
+    # One solve = ONE launch of gn_solve_kernel (the persistent dataflow kernel: every GN iteration
+    # and the objective).  Its duration is measured live above (CUDA events on the plan's stream
+    # around the launch).  Algorithmic work per launch = per-iteration figures x
+    # iterations; the FP64 tensor bound is the larger of the two lower bounds, so it is the primary.
     peaks, peak_src = measured_peaks()
-    roof, phases, stats = None, None, {}
+    roof, phases, stats, level_phases = None, None, est.plan.stats() if world == 1 else {}, None
     if world == 1:
-        prof = G.MultiAreaEstimator(net, ms, part, config=G.SolverConfig(profile_phases=True), device=local)
-        for _ in range(3):
-            prof.estimate()
-        acc = np.zeros(5)
-        reps = 5
-        for _ in range(reps):
-            flush.zero_()
-            torch.cuda.synchronize(dev)
-            _, r = prof.estimate()
-            acc += np.array([r.timings[p] for p in G.solver.PHASES])
-        per_iter = acc / (reps * it_per_solve)           # seconds per GN iteration per phase
-        stats = prof.plan.stats()
-        phases = dict(zip(G.solver.PHASES, (float(x) for x in per_iter)))
+        t_launch = tot_dev / args.steps
         fp64_peak = dgemm_peak(torch, dev)
-        t_asm = phases["assembly"]
-        t_dense = phases["local_condense"] + phases["boundary_assemble"] + phases["boundary_solve"]
-        hbm = {"kernel": "eval_templates_kernel+accumulate_kernel", "bound": "hbm",
-               "achieved": stats["alg_bytes"] / t_asm / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-               "frac": stats["alg_bytes"] / t_asm / 1e9 / peaks["hbm_gbs"], "traffic": None,
-               "peak_source": f"MEASURED_PEAKS.json ({peak_src})", "bytes_per_launch": stats["alg_bytes"]}
-        dense = {"kernel": "front_task_kernel", "bound": "tensor", "achieved": stats["dense_flops"] / t_dense / 1e12,
-                 "peak": fp64_peak, "unit": "TFLOP/s", "frac": stats["dense_flops"] / t_dense / 1e12 / fp64_peak,
-                 "traffic": None, "peak_source": "cuBLAS FP64 DGEMM 4096^3 measured in this run",
-                 "flops_per_iteration": stats["dense_flops"]}
-        roof = dense if t_dense >= t_asm else hbm
-        roof["other"] = hbm if roof is dense else dense
-        prof.close()
+        flops = stats["dense_flops"] * it_per_solve
+        abytes = stats["alg_bytes"] * it_per_solve
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(args.workload, {}).get("gn_solve_kernel")
+        phases = {p: float(rep.timings[p]) / it_per_solve for p in G.solver.PHASES}   # in-kernel globaltimer stamps
+        t_asm = max(phases["assembly"], 1e-9)
+        roof = {"kernel": "gn_solve_kernel", "bound": "tensor", "achieved": flops / t_launch / 1e12, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": flops / t_launch / 1e12 / fp64_peak, "traffic": traffic,
+                "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full, profiles/)",
+                "peak_source": "cuBLAS FP64 DGEMM 4096^3 measured in this run (MEASURED_PEAKS.json has no FP64 figure)",
+                "flops_per_launch": flops, "launch_s": t_launch,
+                "other": {"bound": "hbm", "achieved": abytes / t_launch / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                          "frac": abytes / t_launch / 1e9 / peaks["hbm_gbs"], "bytes_per_launch": abytes,
+                          "peak_source": f"MEASURED_PEAKS.json ({peak_src})",
+                          "assembly_phase": {"what": "template evaluation + fused accumulation items inside the kernel "
+                                                     "(phase time from in-kernel globaltimer stamps)",
+                                             "achieved": stats["alg_bytes"] / t_asm / 1e9,
+                                             "frac": stats["alg_bytes"] / t_asm / 1e9 / peaks["hbm_gbs"],
+                                             "bytes_per_iteration": stats["alg_bytes"], "s_per_iteration": t_asm}}}
+        if not args.no_profile:
+            # the same solve on the level-launch path (one kernel per tree level, CUDA events between phases)
+            prof = G.MultiAreaEstimator(net, ms, part, config=G.SolverConfig(profile_phases=True), device=local)
+            for _ in range(3):
+                prof.estimate()
+            acc = np.zeros(5)
+            reps = 5
+            for _ in range(reps):
+                flush.zero_()
+                torch.cuda.synchronize(dev)
+                _, r = prof.estimate()
+                acc += np.array([r.timings[p] for p in G.solver.PHASES])
+            level_phases = dict(zip(G.solver.PHASES, (float(x) for x in acc / (reps * it_per_solve))))
+            prof.close()
 
     # ---- CPU baseline: the oracle port, bounded sample ---------------------------------------------
     cpu = None
@@ -272,7 +286,10 @@ def run_gpu(args):
     if roof:
         line["roofline"] = roof
         line["phase_s_per_iteration"] = phases
-        line["plan"] = {k: stats[k] for k in ("fronts", "levels", "tasks", "max_front", "launches_per_iter")}
+        if level_phases:
+            line["level_path_phase_s_per_iteration"] = level_phases
+        line["plan"] = {k: stats[k] for k in ("fronts", "levels", "tasks", "max_front", "persistent", "solve_ctas",
+                                             "solve_smem_bytes", "items_per_iteration")}
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -289,6 +306,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="pegase9241_k16", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-profile", action="store_true", help="skip the per-phase profile pass (development sweeps)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

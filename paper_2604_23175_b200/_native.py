@@ -370,9 +370,9 @@ class Plan:
         return lib().gse_boundary_delta_dev(self._h)
 
     def stats(self):
-        s = np.zeros(12)
-        lib().gse_plan_stats(self._h, _fp(s), 12)
+        s = np.zeros(16)
+        lib().gse_plan_stats(self._h, _fp(s), 16)
         keys = ("launches_last", "fronts", "levels", "tasks", "max_front", "factor_doubles",
                 "update_doubles", "pair_contributions", "slots", "alg_bytes", "dense_flops",
-                "launches_per_iter")
+                "launches_per_iter", "persistent", "solve_ctas", "solve_smem_bytes", "items_per_iteration")
         return dict(zip(keys, (float(v) for v in s)))

@@ -545,7 +545,7 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     cudaStream_t s = plan->stream;
     SolveProg sp = plan->sp;
     sp.max_it = max_it; sp.tol = cfg->convergence_tol;
-    if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 16 * (size_t)sp.items_per_it * 16, s));
+    if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 32 * (size_t)sp.items_per_it * 16, s));
     auto t0 = std::chrono::steady_clock::now();
     cudaEventRecord(plan->ev[6], s);
     CU(cudaMemsetAsync(plan->syncblk.ptr, 0, plan->sync_bytes, s));
@@ -798,7 +798,7 @@ int gse_profile_iteration(gse_plan* plan, double* va, double* vm, int32_t max_n,
 // smid | cta << 32, ..., then the 8 phase stamps of a front task) to out and disarms.  Returns the items per iteration.
 int gse_debug_trace(gse_plan* plan, int enable, unsigned long long* out, int64_t max_words) {
     CU(cudaSetDevice(plan->device));
-    const size_t words = 16 * (size_t)plan->sp.items_per_it * 16;
+    const size_t words = 32 * (size_t)plan->sp.items_per_it * 16;
     if (enable) {
         if (!plan->trace.ptr) CU(plan->trace.alloc(words));
         plan->sp.trace = plan->trace.ptr;

@@ -115,6 +115,19 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
 
 constexpr int kChildBatch = 32;
 
+// Diagonal 8x8 blocks of the pivot triangle are kept RIGHT-looking: as soon as a block column
+// [kc, kc + 8) of the panel is final, every later diagonal block t takes its share
+// D_t -= A[t, kc:kc+8] A[t, kc:kc+8]^T (two MMAs).  The block about to be factored is then always
+// up to date and the serial chain of the panel never waits for a long left-looking product.
+__device__ __forceinline__ void diag_rank8(double* pan, int ld, int t, int kc, int lane) {
+    const double* ap = pan + (size_t)(t * 8 + (lane >> 2)) * ld + kc + (lane & 3);
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    dmma_m8n8k4(c0, c1, ap[0], ap[0]);
+    dmma_m8n8k4(e0, e1, ap[4], ap[4]);
+    double* o = pan + (size_t)(t * 8 + (lane >> 2)) * ld + t * 8 + 2 * (lane & 3);
+    o[0] -= c0 + e0; o[1] -= c1 + e1;
+}
+
 // Static shared scratch of one front task (the panels / tile live in dynamic shared memory).
 struct __align__(16) FrontScratch {
     TaskRec hdr;
@@ -261,36 +274,26 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     GSE_TICK(3);
 
     // ---- blocked panel factorisation (block = 8 columns) ---------------------------------------
-    // Per block: warp 0 updates the 8x8 diagonal tile (four independent MMA chains), factors it in
-    // registers and publishes it while the other warps update the remaining row tiles on the tensor
-    // pipe (look-ahead); then every row solves against the published block (right-looking:
-    // independent FMAs).  Two barriers per 8 pivots.
+    // Per block: warp 0 brings the 8x8 diagonal tile up to date (rank-8 share of the previous block
+    // column; see diag_rank8), factors it in registers and publishes it while the other warps
+    // update the remaining row tiles on the tensor pipe (left-looking, look-ahead); then every row
+    // solves against the published block (independent FMAs).  Two barriers per 8 pivots.
     if (HAS_PIVOTS && pp) {
         const int R = rp + ri + rj;                 // padded rows: [pivots | chunk I | chunk J]
         const int ntile = R >> 3;
+        long long pc[7] = {0, 0, 0, 0, 0, 0, 0}, pt = tb ? clock64() : 0;   // debug: cycles per panel sub-phase (thread 0)
+#define GSE_PC(k) do { if (tb) { const long long now = clock64(); pc[k] += now - pt; pt = now; } } while (0)
         for (int kb = 0; kb < rp; kb += 8) {
             const int t0 = kb >> 3;
             if (warp == 0) {
-                if (kb) {
-                    const double* ap = pan + (size_t)(kb + (lane >> 2)) * ld + (lane & 3);
-                    double c[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                    int kk = 0;
-                    for (; kk + 12 < kb; kk += 16) {         // four independent chains
-                        dmma_m8n8k4(c[0], c[1], ap[kk], ap[kk]);
-                        dmma_m8n8k4(c[2], c[3], ap[kk + 4], ap[kk + 4]);
-                        dmma_m8n8k4(c[4], c[5], ap[kk + 8], ap[kk + 8]);
-                        dmma_m8n8k4(c[6], c[7], ap[kk + 12], ap[kk + 12]);
-                    }
-                    for (; kk < kb; kk += 4) dmma_m8n8k4(c[0], c[1], ap[kk], ap[kk]);
-                    double* o = pan + (size_t)(kb + (lane >> 2)) * ld + kb + 2 * (lane & 3);
-                    o[0] -= (c[0] + c[2]) + (c[4] + c[6]); o[1] -= (c[1] + c[3]) + (c[5] + c[7]);
-                    __syncwarp();
-                }
+                if (kb) { diag_rank8(pan, ld, t0, kb - 8, lane); __syncwarp(); }   // the last block column's share
+                GSE_PC(0);
                 double d[36];   // lower triangle, row-major: d[i*(i+1)/2 + j]
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
                     for (int j = 0; j <= i; ++j) d[i * (i + 1) / 2 + j] = pan[(kb + i) * ld + kb + j];
+                GSE_PC(1);
                 double rinv[8];
                 int badk = -1;
 #pragma unroll
@@ -308,23 +311,26 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                         for (int i = j; i < 8; ++i)
                             d[i * (i + 1) / 2 + j] = fma(-d[i * (i + 1) / 2 + k], d[j * (j + 1) / 2 + k], d[i * (i + 1) / 2 + j]);
                 }
+                GSE_PC(2);
                 // publish: every lane holds the same values; lane l writes entries l and l + 32
                 {
-                    double v0 = 0.0, v1 = 0.0;
+                    if (lane == 0) {
+                        double2* o2 = reinterpret_cast<double2*>(s_ld);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) if (lane == i) v0 = d[i];
+                        for (int i = 0; i < 18; ++i) o2[i] = make_double2(d[2 * i], d[2 * i + 1]);
 #pragma unroll
-                    for (int i = 32; i < 36; ++i) if (lane == i - 32) v1 = d[i];
+                        for (int k = 0; k < 4; ++k) o2[18 + k] = make_double2(rinv[2 * k], rinv[2 * k + 1]);
+                        double2* r2 = reinterpret_cast<double2*>(s_rinv + kb);     // (padded pivots: reciprocal 1)
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) if (lane == 4 + k) v1 = rinv[k];
-                    s_ld[lane] = v0;
-                    if (lane < 12) s_ld[32 + lane] = v1;
-                    if (lane >= 4 && lane < 12 && kb + lane - 4 < p) s_rinv[kb + lane - 4] = v1;
-                    if (lane == 0 && badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
+                        for (int k = 0; k < 4; ++k) r2[k] = make_double2(rinv[2 * k], rinv[2 * k + 1]);
+                        if (badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
+                    }
                 }
             } else if (kb) {
-                // rows below the diagonal tile: block column kb -= A[rows, 0:kb] * A[kb:kb+8, 0:kb]^T
+                // later pivot tiles: their diagonal blocks take the last block column's share now
                 const int nw = nwarps - 1;
+                for (int t = t0 + warp; t < (rp >> 3); t += nw) diag_rank8(pan, ld, t, kb - 8, lane);
+                // rows below the diagonal tile: block column kb -= A[rows, 0:kb] * A[kb:kb+8, 0:kb]^T
                 for (int tb2 = t0 + 1 + (warp - 1); tb2 < ntile; tb2 += 2 * nw) {
                     const int ta = tb2, tc2 = tb2 + nw;
                     const bool two = tc2 < ntile;
@@ -346,7 +352,9 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                     }
                 }
             }
+            GSE_PC(3);
             __syncthreads();
+            GSE_PC(4);
             // every row at or below the block solves against the published 8x8 factor
             if (tid >= kb && tid < R) {
                 double* myrow = pan + (size_t)tid * ld + kb;
@@ -368,8 +376,12 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                     for (int j = 0; j < 8; ++j) myrow[j] = y[j];
                 }
             }
+            GSE_PC(5);
             __syncthreads();
+            GSE_PC(6);
         }
+#undef GSE_PC
+        if (tb && tid == 0) for (int k = 0; k < 7; ++k) tb[8 + k] = pc[k];
     }
     GSE_TICK(4);
 

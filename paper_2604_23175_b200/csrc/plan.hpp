@@ -113,7 +113,10 @@ struct BuildOptions {
     int max_pivots = 64;
     int boundary_mode = 0;     // 0 auto (tree when n_Gamma > 192), 1 dense chain, 2 tree
     int gamma_leaf_buses = 16; // nested-dissection leaf of the boundary tree, in boundary buses
-    int split_min_pivots = 32; // fronts with several row chunks and at least this many pivots run as panel + update tasks
+    // fronts with several row chunks and at least this many pivots run as panel + update tasks.  Measured on the
+    // PEGASE-9241 shape (tools/gpu_sweep2.sh): the panel is bound by its serial 8x8 chain, not by its row count,
+    // so the split only adds a hand-off (2.06 ms vs 2.03 ms per solve) -- off by default, kept for wide fronts.
+    int split_min_pivots = 1 << 20;
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;

@@ -127,7 +127,7 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             known = it;
         }
         const unsigned epoch = (unsigned)it + 1u;
-        unsigned long long* tr = sp.trace ? sp.trace + 16 * (size_t)item : nullptr;
+        unsigned long long* tr = sp.trace ? sp.trace + 32 * (size_t)item : nullptr;
         if (tr && tid == 0) {
             unsigned smid;
             asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));

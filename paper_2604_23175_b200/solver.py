@@ -42,7 +42,9 @@ class SolverConfig:
     backend: str = "sparse"         # "dense": chain of dense fronts per area instead of nested dissection
     dense_threshold: int = 64       # kept for API parity (fronts are dense blocks at every size)
     iterative_refinement: bool = False
-    profile_phases: bool = False    # extension: fill per-phase timings from CUDA events (no graph)
+    # extension: run the level-launch path (one kernel per tree level, no CUDA graph) with CUDA events
+    # between the phases instead of the single persistent kernel (which stamps its phases itself)
+    profile_phases: bool = False
     # extension: how the reduced boundary system is factored.  "dense" = the reference's dense
     # Cholesky (a chain of dense fronts); "sparse" = the same factorisation with the structural
     # zeros between non-adjacent areas skipped (nested dissection on the area-clique graph);
@@ -183,9 +185,10 @@ class MultiAreaEstimator:
                 self.last_deltas = [rep.delta_inf[i] for i in range(iterations)]
                 self.last_loop_s, self.last_gpu_s = rep.loop_s, rep.gpu_s
                 self.launches_per_solve = int(self.plan.stats()["launches_last"])
-                if cfg.profile_phases:
-                    for p, v in zip(PHASES, rep.phase_s):
-                        timings[p] = float(v)
+                # persistent path: device globaltimer stamps per phase; profile_phases: CUDA events
+                # between the phases of the level-launch path
+                for p, v in zip(PHASES, rep.phase_s):
+                    timings[p] = float(v)
             else:
                 iterations, converged = 0, False
                 self.last_deltas = []

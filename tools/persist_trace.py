@@ -27,9 +27,9 @@ L.gse_solve_layout(est.plan._h, lay.ctypes.data_as(C.c_void_p))
 n_eval, n_acc, n_task, n_bwd, n_upd, grid, smem, persistent = (int(v) for v in lay)
 per_it = L.gse_debug_trace(est.plan._h, 1, None, 0)
 state, rep = est.estimate()
-tr = np.zeros(per_it * 16 * 16, dtype=np.uint64)
+tr = np.zeros(per_it * 16 * 32, dtype=np.uint64)
 L.gse_debug_trace(est.plan._h, 0, tr.ctypes.data_as(C.c_void_p), tr.size)
-tr = tr.reshape(-1, 16).astype(np.int64)
+tr = tr.reshape(-1, 32).astype(np.int64)
 print(f"{name}: persistent={persistent} grid={grid} smem={smem} items/it={per_it} "
       f"(eval {n_eval}, acc {n_acc}, front {n_task}, bwd {n_bwd}, upd {n_upd}); iterations={rep.iterations} "
       f"gpu_s={est.last_gpu_s*1e3:.3f} ms")
@@ -88,7 +88,8 @@ for it in range(rep.iterations):
                 cw = max(b[i, 2], st[7]) if b[i, 2] else st[7]
                 pw = b[i, 5] if kind == 2 else st[4]
                 print(f"     {f:5d} k{kind} {ci},{cj} | {(st[1]-st[0])/1e3:5.1f} {(st[2]-st[1])/1e3:5.1f} {(st[7]-st[2])/1e3:5.1f} [{(cw-st[7])/1e3:5.1f}] "
-                      f"{(st[3]-cw)/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} [{(pw-st[4])/1e3:5.1f}] {(st[5]-pw)/1e3:5.1f} {(st[6]-st[5])/1e3:5.1f} {(b[i,3]-st[6])/1e3:5.1f}")
+                      f"{(st[3]-cw)/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} [{(pw-st[4])/1e3:5.1f}] {(st[5]-pw)/1e3:5.1f} {(st[6]-st[5])/1e3:5.1f} {(b[i,3]-st[6])/1e3:5.1f}"
+                      + ("   panel cyc: diagupd %d lds %d factor %d publish %d sync %d rowsolve %d sync %d" % tuple(b[i, 16:23]) if kind != 2 else ""))
         b = blk[bounds[3]:bounds[4]]
         step = max(1, len(b) // 25)
         print("   backward wavefront:")
