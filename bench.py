@@ -28,17 +28,28 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-WORKLOADS = {"pegase2869_k8": "pegase2869", "pegase9241_k16": "pegase9241", "activsg10k_k32": "activsg10k"}
+WORKLOADS = {"pegase2869_k8": "pegase2869", "pegase9241_k16": "pegase9241", "activsg10k_k32": "activsg10k",
+             "tiled101k_k176": "tiled"}
 
 
 def build_workload(name):
     import paper_2604_23175_b200 as G
     from paper_2604_23175_b200 import synth
     shape = WORKLOADS[name]
+    if shape == "tiled":
+        # BASELINE.json configs[4]: ~100k buses tiled from PEGASE areas (11 tiles of the 9241-bus shape with
+        # its committed 16-area partition each: 101,651 buses, 176 areas, n_Gamma = 7996)
+        net, _ = synth.tiled_network(synth.shaped_network("pegase9241"), 11)
+        ms = G.generate_measurements(net, G.MeasurementConfig(seed=0))
+        part = G.load_partition(net, synth.tile_partition(synth.golden_partition("pegase9241"), 11))
+        return net, ms, part
     net = synth.shaped_network(shape)
     ms = G.generate_measurements(net, G.MeasurementConfig(seed=0))
     part = G.load_partition(net, synth.golden_partition(shape))
     return net, ms, part
+
+
+METRIC_NAMES = {"pegase9241_k16": "GN iterations/s (PEGASE-9241-shape MASE, 16 areas)"}
 
 
 def measured_peaks():
@@ -113,7 +124,7 @@ def run_reference(args):
     res, sec, setup, runs = cpu_reference(net, ms, part, threads, budget_s=max(5.0, 2.0 * args.steps))
     value = res["iterations"] / sec
     line = {
-        "impl": "reference", "metric": "GN iterations/s (PEGASE-9241-shape MASE, 16 areas)", "value": value,
+        "impl": "reference", "metric": METRIC_NAMES.get(args.workload, f"GN iterations/s ({args.workload} MASE)"), "value": value,
         "unit": "GN iterations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
@@ -268,7 +279,7 @@ def run_gpu(args):
 
     m, nb = ms.m, net.n_bus
     line = {
-        "metric": "GN iterations/s (PEGASE-9241-shape MASE, 16 areas)", "value": value, "unit": "GN iterations/s",
+        "metric": METRIC_NAMES.get(args.workload, f"GN iterations/s ({args.workload} MASE)"), "value": value, "unit": "GN iterations/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": tot_dev / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
