@@ -69,7 +69,8 @@ typedef struct {
     int32_t max_pivots;      /* front pivot-block width, 32 or 64 (0 = default 64)          */
     int32_t rank, world;     /* area sharding: this process / number of processes           */
     const int32_t *area_rank;/* [n_areas] owner rank per area, NULL = all on rank 0          */
-    int32_t persistent;      /* reserved (dataflow scheduler)                               */
+    int32_t persistent;      /* gse_solve scheduler: 0 auto (persistent dataflow kernel on single-rank plans),
+                              * 1 persistent, 2 level launches captured in a CUDA graph             */
     int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default 48) */
     int32_t boundary_mode;   /* boundary factorisation: 0 auto, 1 dense chain (dense_cholesky_solve), 2 block-sparse tree */
 } gse_options;
@@ -118,6 +119,10 @@ int gse_solve(gse_plan *plan, const gse_config *cfg, double *va_dev, double *vm_
               gse_report *report);
 /* One outer iteration (used when the caller wants on_iteration callbacks, solver.py:334). */
 int gse_iterate(gse_plan *plan, double *va_dev, double *vm_dev, double *delta_inf);
+/* One inner GN step of every owned area with the boundary state held fixed: SolverConfig.inner_gn_steps > 1
+ * (solver.py:253-260: fused_accumulate, numeric_refactor, cache.solve(b_i), apply_interior_delta).
+ * *delta_inf = max |delta x_i| of the step. */
+int gse_inner_step(gse_plan *plan, double *va_dev, double *vm_dev, double *delta_inf);
 
 /* ---- phase-level entry points (component parity + the multi-GPU driver) ------------ */
 /* fused_accumulate for every owned area (assembly.py:486-524). */

@@ -597,23 +597,48 @@ double orc_objective(const orc_t *o, const double *va, const double *vm) {
     }
     return sum + comp;
 }
+/* One inner GN step of every area with the boundary held fixed (reference solver.py:253-260):
+   assemble, refactor, dx_i = G_ii^-1 b_i, apply to the interior state.  Returns max |dx_i| or -1. */
+double orc_inner_step(orc_t *o, double *va, double *vm) {
+    int K = o->d.n_areas; double dmax = 0.0;
+    double *zero = xcalloc(o->n_gamma > 0 ? o->n_gamma : 1, sizeof(double));
+    for (int a = 0; a < K; a++) {
+        area_t *A = &o->areas[a];
+        eval_rows(o, A, va, vm); accumulate(o, A);
+        A->fail_pivot = chol_refactor(&A->ch, A->data_ii);
+        if (A->fail_pivot >= 0) { o->err_kind = 1; o->err_area = a; o->err_pivot = A->fail_pivot; free(zero); return -1.0; }
+        recover(A, zero);
+        for (int i = 0; i < A->n_ia; i++) va[A->ia_bus[i]] += A->dxi[i];
+        for (int i = 0; i < A->n_int_bus; i++) vm[A->int_bus[i]] += A->dxi[A->n_ia + i];
+        for (int i = 0; i < A->n_i; i++) if (fabs(A->dxi[i]) > dmax) dmax = fabs(A->dxi[i]);
+    }
+    free(zero);
+    return dmax;
+}
 /* Full GN loop.  trace_delta[max_iter]; trace_va/vm optional [max_iter][n_bus].
    Returns iterations (>0), or -1 on a non-SPD failure (see orc_last_error). */
-int orc_solve(orc_t *o, int max_iter, double tol, double *va, double *vm, int threads,
-              double *trace_delta, double *trace_va, double *trace_vm, int32_t *converged) {
+int orc_solve_inner(orc_t *o, int max_iter, int inner_steps, double tol, double *va, double *vm, int threads,
+                    double *trace_delta, double *trace_va, double *trace_vm, int32_t *converged) {
     int nb = o->d.n_bus; *converged = 0;
     for (int b = 0; b < nb; b++) { va[b] = 0.0; vm[b] = 1.0; }
     va[o->d.slack] = o->d.slack_va;
     for (int it = 1; it <= max_iter; it++) {
+        double inner = 0.0;
+        for (int s = 0; s + 1 < inner_steps; s++) { double d = orc_inner_step(o, va, vm); if (d < 0) return -1; if (d > inner) inner = d; }
         if (orc_local(o, va, vm, threads)) return -1;
         if (orc_boundary(o)) return -1;
         double dinf = orc_recover(o, va, vm, threads);
+        if (inner > dinf) dinf = inner;
         if (trace_delta) trace_delta[it - 1] = dinf;
         if (trace_va) memcpy(trace_va + (size_t)(it - 1) * nb, va, sizeof(double) * nb);
         if (trace_vm) memcpy(trace_vm + (size_t)(it - 1) * nb, vm, sizeof(double) * nb);
         if (dinf < tol) { *converged = 1; return it; }
     }
     return max_iter;
+}
+int orc_solve(orc_t *o, int max_iter, double tol, double *va, double *vm, int threads,
+              double *trace_delta, double *trace_va, double *trace_vm, int32_t *converged) {
+    return orc_solve_inner(o, max_iter, 1, tol, va, vm, threads, trace_delta, trace_va, trace_vm, converged);
 }
 /* component-level helpers for tests: dense SPD solve and standalone Schur of user blocks */
 int orc_dense_cholesky_solve(const double *a, const double *b, int n, double *x) {

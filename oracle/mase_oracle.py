@@ -72,6 +72,8 @@ def _lib():
         lib.orc_objective.argtypes = [C.c_void_p, _f64p, _f64p]
         lib.orc_solve.argtypes = [C.c_void_p, C.c_int, C.c_double, _f64p, _f64p, C.c_int,
                                   _f64p, _f64p, _f64p, _i32p]
+        lib.orc_solve_inner.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _f64p, _f64p, C.c_int,
+                                        _f64p, _f64p, _f64p, _i32p]
         lib.orc_dense_cholesky_solve.argtypes = [_f64p, _f64p, C.c_int, _f64p]
         _LIB = lib
     return _LIB
@@ -237,7 +239,7 @@ class Oracle:
         vm = np.ascontiguousarray(vm, dtype=np.float64)
         return float(_lib().orc_objective(self._h, _p(va, _f64p), _p(vm, _f64p)))
 
-    def solve(self, max_iter=10, tol=1e-6, threads=1, trace=False):
+    def solve(self, max_iter=10, tol=1e-6, threads=1, trace=False, inner=1):
         """Flat-start GN loop -> dict(va, vm, iterations, converged, deltas, J[, trace])."""
         nb = self.n_bus
         va, vm = np.zeros(nb), np.zeros(nb)
@@ -245,8 +247,8 @@ class Oracle:
         tva = np.zeros((max_iter, nb)) if trace else None
         tvm = np.zeros((max_iter, nb)) if trace else None
         conv = np.zeros(1, dtype=np.int32)
-        it = _lib().orc_solve(
-            self._h, max_iter, tol, _p(va, _f64p), _p(vm, _f64p), threads, _p(deltas, _f64p),
+        it = _lib().orc_solve_inner(
+            self._h, max_iter, inner, tol, _p(va, _f64p), _p(vm, _f64p), threads, _p(deltas, _f64p),
             _p(tva, _f64p) if trace else None, _p(tvm, _f64p) if trace else None,
             _p(conv, _i32p))
         if it < 0:

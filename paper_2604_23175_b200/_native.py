@@ -101,6 +101,7 @@ def lib():
     L.gse_set_measurements.argtypes = [vp, f64p]
     L.gse_solve.argtypes = [vp, C.POINTER(Config), vp, vp, C.POINTER(Report)]
     L.gse_iterate.argtypes = [vp, vp, vp, f64p]
+    L.gse_inner_step.argtypes = [vp, vp, vp, f64p]
     L.gse_phase_assemble.argtypes = [vp, vp, vp]
     L.gse_phase_condense.argtypes = [vp]
     L.gse_phase_boundary.argtypes = [vp]
@@ -130,7 +131,7 @@ def lib():
 
 EXPORTED = [
     "gse_plan_create", "gse_plan_destroy", "gse_last_error", "gse_set_weights",
-    "gse_set_measurements", "gse_solve", "gse_iterate", "gse_phase_assemble",
+    "gse_set_measurements", "gse_solve", "gse_iterate", "gse_inner_step", "gse_phase_assemble",
     "gse_phase_condense", "gse_phase_boundary", "gse_phase_recover", "gse_check", "gse_objective",
     "gse_area_dims", "gse_area_pattern", "gse_area_blocks", "gse_area_schur", "gse_area_delta",
     "gse_boundary_system", "gse_set_boundary_delta", "gse_exchange_buffer_dev",
@@ -279,6 +280,11 @@ class Plan:
     def iterate(self, va_ptr, vm_ptr):
         d = C.c_double()
         self._call(lib().gse_iterate(self._h, va_ptr, vm_ptr, C.byref(d)))
+        return d.value
+
+    def inner_step(self, va_ptr, vm_ptr):
+        d = C.c_double()
+        self._call(lib().gse_inner_step(self._h, va_ptr, vm_ptr, C.byref(d)))
         return d.value
 
     def objective(self, va_ptr, vm_ptr):

@@ -287,8 +287,7 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
     if (hp.acc_stage_max > kAccStageMax || hp.acc_pair_max > kAccPairMax) return fail(plan, GSE_E_INVALID, "a normal-equation entry has too many contributions for the staged accumulation");
     CU(plan->acc_ptr.upload(hp.acc_lptr)); CU(plan->acc_items.upload(hp.acc_items)); CU(plan->acc_uniq.upload(hp.acc_uniq));
     CU(plan->acc_pair.upload(hp.acc_pair));
-    CU(plan->racc_ptr.upload(hp.racc_ptr)); CU(plan->racc_a.upload(hp.racc_a)); CU(plan->racc_b.upload(hp.racc_b));
-    CU(plan->gval.alloc(hp.n_gval)); CU(plan->refval.alloc(hp.n_ref_vals));
+    CU(plan->gval.alloc(hp.n_gval));
     plan->ap = AccProg{plan->acc_items.ptr, plan->acc_uniq.ptr, plan->acc_ptr.ptr, plan->acc_pair.ptr, plan->val.ptr,
                        plan->gval.ptr, (int32_t)(hp.acc_items.size() / 8)};
     EvalProg& ep = plan->ep;
@@ -529,6 +528,34 @@ int gse_iterate(gse_plan* plan, double* va, double* vm, double* delta_inf) {
     return GSE_OK;
 }
 
+// One inner Gauss-Newton step of every owned area with the boundary state held fixed
+// (reference solver.py:253-260: fused_accumulate -> numeric_refactor -> cache.solve(b_i) ->
+// apply_interior_delta).  On the device: assembly, the interior fronts of the forward pass, the
+// interior back-substitution with delta_x_Gamma = 0, and the state update of the interior
+// variables only.  *delta_inf = max |delta x_i| of this step.
+int gse_inner_step(gse_plan* plan, double* va, double* vm, double* delta_inf) {
+    CU(cudaSetDevice(plan->device));
+    cudaStream_t s = plan->stream;
+    const HostProgram& hp = plan->hp;
+    CU(cudaMemsetAsync(plan->flags.ptr, 0, sizeof(unsigned long long), s));
+    enqueue_phase_assemble(plan, va, vm);
+    enqueue_fwd(plan, 1);
+    if (hp.n_gamma) CU(cudaMemsetAsync(plan->xsol.ptr + hp.gamma_base, 0, sizeof(double) * hp.n_gamma, s));
+    enqueue_bwd(plan, 4);
+    const int n_interior = (int)plan->upd_bus.n - hp.n_gamma;      // update list = interiors of every area, then x_Gamma
+    launch_update(plan->upd_bus.ptr, plan->upd_quant.ptr, plan->upd_pos.ptr, n_interior, plan->xsol.ptr, va, vm, plan->flags.ptr, s);
+    CU(cudaMemcpyAsync(plan->h_flags, plan->flags.ptr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (plan->h_flags[1] != ~0ull) {
+        unsigned long long code = plan->h_flags[1];
+        cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+        return decode_failure(plan, code);
+    }
+    double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
+    if (delta_inf) *delta_inf = dv;
+    return GSE_OK;
+}
+
 int gse_objective(gse_plan* plan, const double* va, const double* vm, double* j_out) {
     CU(cudaSetDevice(plan->device));
     launch_objective(plan->ep, plan->m_type.ptr, plan->m_target.ptr, plan->br_from.ptr, plan->br_to.ptr, plan->hp.n_rows, va, vm,
@@ -624,6 +651,11 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
 // ---- phase-level entry points ------------------------------------------------------------------
 int gse_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
     CU(cudaSetDevice(plan->device));
+    if (!plan->hp.ref_program_built) {      // the reference-layout program is only needed here: built on first use
+        build_reference_program(plan->hp);
+        CU(plan->racc_ptr.upload(plan->hp.racc_ptr)); CU(plan->racc_a.upload(plan->hp.racc_a)); CU(plan->racc_b.upload(plan->hp.racc_b));
+        CU(plan->refval.alloc(plan->hp.n_ref_vals));
+    }
     enqueue_phase_assemble(plan, va, vm);
     // reference-layout blocks for component parity (same slot values, second destination map)
     launch_accumulate(plan->racc_ptr.ptr, plan->racc_a.ptr, plan->racc_b.ptr, plan->val.ptr, plan->refval.ptr,
@@ -676,6 +708,7 @@ int gse_area_pattern(const gse_plan* plan, int32_t a, int32_t* ii_ptr, int32_t* 
 int gse_area_blocks(gse_plan* plan, int32_t a, double* data_ii, double* data_ib, double* g_bb, double* b_i, double* b_b) {
     const HostProgram& hp = plan->hp;
     if (a < 0 || a >= hp.n_areas || !hp.owned[a]) return fail(plan, GSE_E_INVALID, "area not owned by this plan");
+    if (!plan->refval.ptr) return fail(plan, GSE_E_INVALID, "gse_area_blocks needs a preceding gse_phase_assemble");
     CU(cudaSetDevice(plan->device));
     const size_t nii = hp.ii_idx[a].size(), nib = hp.ib_idx[a].size(), nb = hp.area_nb[a], ni = hp.area_ni[a];
     const double* base = plan->refval.ptr + hp.ref_off[a];

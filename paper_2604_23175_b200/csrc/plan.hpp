@@ -72,8 +72,12 @@ struct HostProgram {
     // reference layout (component parity): per area CSR patterns + a second program
     std::vector<std::vector<int32_t>> ii_ptr, ii_idx, ib_ptr, ib_idx;
     std::vector<int64_t> ref_off;        // per area offset into the ref-layout value array
-    std::vector<int32_t> racc_ptr, racc_a, racc_b;
+    std::vector<int32_t> racc_ptr, racc_a, racc_b;   // built on demand: build_reference_program
     int64_t n_ref_vals = 0;
+    bool ref_program_built = false;
+    // per area template layout (rows, slot pointers, slot variables, first global slot)
+    std::vector<std::vector<int>> tmpl_rows, tmpl_slot_ptr, tmpl_slot_var;
+    std::vector<int64_t> tmpl_slot_base;
     std::vector<int32_t> perm_orig;      // per position: original local variable (error reports)
 
     // fronts / tasks / levels
@@ -124,5 +128,6 @@ struct BuildOptions {
 
 // symbolic.cpp
 std::string build_host_program(const gse_problem_desc& d, const BuildOptions& opt, HostProgram& hp);
+void build_reference_program(HostProgram& hp);
 
 }  // namespace gse

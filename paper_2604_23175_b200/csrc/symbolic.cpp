@@ -18,6 +18,7 @@
 //     into it, in ascending row order -- the deterministic, atomic-free
 //     replacement of the five bincount scatters (assembly.py:502-520).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -236,6 +237,17 @@ void build_acc_items(HostProgram& hp) {
 std::string build_host_program(const gse_problem_desc& d, const BuildOptions& opt, HostProgram& hp) {
     const int nbus = d.n_bus, K = d.n_areas, m = d.n_rows, ng = d.n_gamma;
     if (nbus <= 0 || K <= 0 || m < 0) return "empty problem";
+    const bool dbg_time = getenv("GSE_DEBUG_TIME") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    double t_sec[6] = {0, 0, 0, 0, 0, 0};
+    auto t_mark = std::chrono::steady_clock::now();
+    auto sec = [&](int k) { if (!dbg_time) return; auto now = std::chrono::steady_clock::now(); t_sec[k] += std::chrono::duration<double>(now - t_mark).count(); t_mark = now; };
+    auto lap = [&](const char* what) {
+        if (!dbg_time) return;
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "  plan build: %-28s %.3f s\n", what, std::chrono::duration<double>(now - t_prev).count());
+        t_prev = now;
+    };
     const int PMAX = opt.max_pivots;
     hp.n_bus = nbus; hp.n_rows = m; hp.n_areas = K; hp.n_gamma = ng; hp.slack = d.slack;
     hp.rank = opt.rank; hp.world = opt.world;
@@ -326,6 +338,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         as[d.area_of_bus[owner]].rows.push_back(r);
     }
 
+    lap("boundary ordering, rows");
     // ---- template slots + evaluation units ------------------------------------------
     std::vector<int> loc_va(nbus, -1), loc_vm(nbus, -1);
     std::vector<int> unit_of_branch(d.n_branch, -1), unit_of_bus(nbus, -1);
@@ -335,8 +348,8 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     double nnz_total = 0, rhs_total = 0;
 
     // reference-layout program pieces are collected per area then concatenated
-    std::vector<int64_t> rdest; std::vector<int32_t> ra, rb;   // (dest, a, b) in program order
 
+    t_mark = std::chrono::steady_clock::now();
     for (int a = 0; a < K; ++a) {
         AreaSym& A = as[a];
         const int ni = A.ni, nb = A.nb;
@@ -405,51 +418,36 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         if (!closure_ok) return "measurement row references a bus outside its area's variable map";
         slot_cursor += (int64_t)A.slot_var.size();
 
+        sec(0);
         // ---- reference-layout CSR patterns of G_ii, G_ib ------------------------------
-        std::vector<int64_t> cii, cib;
-        for (size_t k = 0; k < A.rows.size(); ++k)
-            for (int x = A.slot_ptr[k]; x < A.slot_ptr[k + 1]; ++x) {
-                int va = A.slot_var[x]; if (va >= ni) continue;
-                for (int y = A.slot_ptr[k]; y < A.slot_ptr[k + 1]; ++y) {
-                    int vb = A.slot_var[y];
-                    if (vb < ni) cii.push_back((int64_t)va * ni + vb); else cib.push_back((int64_t)va * std::max(nb, 1) + (vb - ni));
-                }
-            }
-        std::sort(cii.begin(), cii.end()); cii.erase(std::unique(cii.begin(), cii.end()), cii.end());
-        std::sort(cib.begin(), cib.end()); cib.erase(std::unique(cib.begin(), cib.end()), cib.end());
-        hp.ii_ptr[a].assign(ni + 1, 0); hp.ii_idx[a].resize(cii.size());
-        for (size_t i = 0; i < cii.size(); ++i) { hp.ii_ptr[a][cii[i] / std::max(ni, 1) + 1]++; hp.ii_idx[a][i] = (int32_t)(cii[i] % std::max(ni, 1)); }
-        for (int i = 0; i < ni; ++i) hp.ii_ptr[a][i + 1] += hp.ii_ptr[a][i];
-        hp.ib_ptr[a].assign(ni + 1, 0); hp.ib_idx[a].resize(cib.size());
-        for (size_t i = 0; i < cib.size(); ++i) { hp.ib_ptr[a][cib[i] / std::max(nb, 1) + 1]++; hp.ib_idx[a][i] = (int32_t)(cib[i] % std::max(nb, 1)); }
-        for (int i = 0; i < ni; ++i) hp.ib_ptr[a][i + 1] += hp.ib_ptr[a][i];
-        // ref value layout of the area: [data_ii | data_ib | g_bb | b_i | b_b]
-        int64_t base = hp.ref_off[a];
-        int64_t o_ib = base + (int64_t)cii.size(), o_bb = o_ib + (int64_t)cib.size();
-        int64_t o_bi = o_bb + (int64_t)nb * nb, o_bbv = o_bi + ni;
-        hp.ref_off[a + 1] = o_bbv + nb;
-        nnz_total += (double)cii.size() + (double)cib.size() + (double)nb * nb; rhs_total += ni + nb;
-        if (hp.owned[a]) {
-            for (size_t k = 0; k < A.rows.size(); ++k) {
-                int s0 = A.slot_ptr[k], s1 = A.slot_ptr[k + 1];
-                for (int x = s0; x < s1; ++x) {
-                    int va = A.slot_var[x];
-                    for (int y = s0; y < s1; ++y) {
-                        int vb = A.slot_var[y]; int64_t dest;
-                        if (va < ni && vb < ni) dest = base + (std::lower_bound(cii.begin(), cii.end(), (int64_t)va * ni + vb) - cii.begin());
-                        else if (va < ni) dest = o_ib + (std::lower_bound(cib.begin(), cib.end(), (int64_t)va * std::max(nb, 1) + (vb - ni)) - cib.begin());
-                        else if (vb >= ni) dest = o_bb + (int64_t)(va - ni) * nb + (vb - ni);
-                        else continue;
-                        rdest.push_back(dest); ra.push_back((int32_t)(A.slot_base + x)); rb.push_back((int32_t)(A.slot_base + y));
+        // (per interior variable: the sorted, de-duplicated columns its rows reach)
+        {
+            std::vector<std::vector<int>> cols_ii(ni), cols_ib(ni);
+            for (size_t k = 0; k < A.rows.size(); ++k)
+                for (int x = A.slot_ptr[k]; x < A.slot_ptr[k + 1]; ++x) {
+                    int va = A.slot_var[x]; if (va >= ni) continue;
+                    for (int y = A.slot_ptr[k]; y < A.slot_ptr[k + 1]; ++y) {
+                        int vb = A.slot_var[y];
+                        if (vb < ni) cols_ii[va].push_back(vb); else cols_ib[va].push_back(vb - ni);
                     }
                 }
-                for (int x = s0; x < s1; ++x) {
-                    int v = A.slot_var[x];
-                    rdest.push_back(v < ni ? o_bi + v : o_bbv + (v - ni)); ra.push_back((int32_t)(A.slot_base + x)); rb.push_back(-(A.rows[k] + 1));
-                }
+            hp.ii_ptr[a].assign(ni + 1, 0); hp.ib_ptr[a].assign(ni + 1, 0);
+            for (int v = 0; v < ni; ++v) {
+                for (auto* c : {&cols_ii[v], &cols_ib[v]}) { std::sort(c->begin(), c->end()); c->erase(std::unique(c->begin(), c->end()), c->end()); }
+                hp.ii_ptr[a][v + 1] = hp.ii_ptr[a][v] + (int32_t)cols_ii[v].size();
+                hp.ib_ptr[a][v + 1] = hp.ib_ptr[a][v] + (int32_t)cols_ib[v].size();
+                hp.ii_idx[a].insert(hp.ii_idx[a].end(), cols_ii[v].begin(), cols_ii[v].end());
+                hp.ib_idx[a].insert(hp.ib_idx[a].end(), cols_ib[v].begin(), cols_ib[v].end());
             }
         }
+        // ref value layout of the area: [data_ii | data_ib | g_bb | b_i | b_b]
+        hp.ref_off[a + 1] = hp.ref_off[a] + (int64_t)hp.ii_idx[a].size() + (int64_t)hp.ib_idx[a].size() + (int64_t)nb * nb + ni + nb;
+        nnz_total += (double)hp.ii_idx[a].size() + (double)hp.ib_idx[a].size() + (double)nb * nb; rhs_total += ni + nb;
+        // template layout kept for the (lazily built) reference-layout program
+        hp.tmpl_rows.push_back(A.rows); hp.tmpl_slot_ptr.push_back(A.slot_ptr); hp.tmpl_slot_var.push_back(A.slot_var);
+        hp.tmpl_slot_base.push_back(A.slot_base);
 
+        sec(1);
         // ---- ordering of the interior --------------------------------------------------
         A.epos.assign(ni, -1); A.order.assign(ni, -1);
         int ep = 0;
@@ -503,6 +501,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         if (ep != ni) return "ordering did not cover the interior";
         A.n_fronts = (int)hp.fronts.size() - A.first_front;
 
+        sec(2);
         // ---- lower-triangular pattern in position space ------------------------------
         const int nloc = ni + nb;
         auto lpos = [&](int v) { return v < ni ? A.epos[v] : v; };
@@ -529,6 +528,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         }
         (void)lpos;
 
+        sec(3);
         // ---- update sets + assembly tree of the interior fronts ---------------------
         std::vector<std::vector<int>> structs(A.n_fronts);   // local positions (>= pivots' end), sorted
         std::vector<int> mark(nloc, -1);
@@ -640,9 +640,13 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             choose_chunks(hp.fronts[root_id], opt.tile_rows);
         }
         for (int b : touched) { loc_va[b] = -1; loc_vm[b] = -1; }
+        sec(4);
     }
     hp.n_slots = slot_cursor;
+    if (dbg_time) fprintf(stderr, "  plan build (areas): slots/units %.3f  ref patterns+program %.3f  ordering %.3f  lower pattern %.3f  fronts+entries %.3f\n",
+                          t_sec[0], t_sec[1], t_sec[2], t_sec[3], t_sec[4]);
 
+    lap("areas: slots, patterns, fronts");
     // ---- coordinator fronts: boundary assembly root + dense factorisation chain -----
     const int first_coord = (int)hp.fronts.size();
     if (ng > 0 && sparse_gamma) {
@@ -768,6 +772,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             hp.reg_ptr.insert(hp.reg_ptr.end(), nreg + 1, 0);
         }
 
+    lap("coordinator fronts");
     // ---- storage offsets ----------------------------------------------------------------
     // update matrices: area roots first, contiguous in area order (the exchange buffer)
     hp.xchg_off = 0; hp.xchg_area_off.assign(K + 1, 0);
@@ -837,6 +842,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         if (!fs.empty()) { hp.bwd_levels.push_back(fs); hp.bwd_phase.push_back(phase); }
     }
 
+    lap("offsets, levels, tasks");
     // ---- solver-layout accumulation program ---------------------------------------------
     // Every contribution is a product val[a] * val[b] of the unified value array
     // val = [g (n_slots) | w*g (n_slots) | w*r (n_rows)]: a indexes g, b indexes w*g (matrix
@@ -883,18 +889,11 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         std::vector<int32_t> cur(hp.acc_ptr.begin(), hp.acc_ptr.end() - 1);
         for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = pa[i]; hp.acc_b[q] = val_index(pb[i]); }
     }
+    lap("accumulation program (sort)");
     build_acc_items(hp);
-    // ---- reference-layout program (component parity) ---------------------------------------
-    {
-        hp.n_ref_vals = hp.ref_off[K];
-        hp.racc_ptr.assign(hp.n_ref_vals + 1, 0);
-        for (int64_t dd : rdest) hp.racc_ptr[dd + 1]++;
-        for (int64_t i = 0; i < hp.n_ref_vals; ++i) hp.racc_ptr[i + 1] += hp.racc_ptr[i];
-        hp.racc_a.resize(rdest.size()); hp.racc_b.resize(rdest.size());
-        std::vector<int32_t> cur(hp.racc_ptr.begin(), hp.racc_ptr.end() - 1);
-        for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = ra[i]; hp.racc_b[q] = val_index(rb[i]); }
-    }
-
+    lap("accumulation items");
+    hp.n_ref_vals = hp.ref_off[K];
+    lap("reference-layout program");
     // ---- state update list ----------------------------------------------------------------
     for (int a = 0; a < K; ++a) {
         if (!hp.owned[a]) continue;
@@ -909,6 +908,54 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
 
     hp.alg_bytes = 16.0 * m + 32.0 * nbus + 96.0 * d.n_branch + 8.0 * nnz_total + 8.0 * rhs_total;
     return "";
+}
+
+// Second accumulation program with the reference's block layout (AreaNormalBlocks: CSR G_ii / G_ib
+// values, dense G_bb, b_i, b_b -- assembly.py:32-53), used only by the component-parity entry
+// point gse_phase_assemble; built on first use so that a plain solve does not pay for it.
+void build_reference_program(HostProgram& hp) {
+    if (hp.ref_program_built) return;
+    hp.ref_program_built = true;
+    const int K = hp.n_areas;
+    std::vector<int64_t> rdest; std::vector<int32_t> ra, rb;   // (dest, a, b) in program order
+    for (int a = 0; a < K; ++a) {
+        if (!hp.owned[a]) continue;
+        const int ni = hp.area_ni[a], nb = hp.area_nb[a];
+        const std::vector<int>& rows = hp.tmpl_rows[a]; const std::vector<int>& slot_ptr = hp.tmpl_slot_ptr[a];
+        const std::vector<int>& slot_var = hp.tmpl_slot_var[a];
+        const int64_t slot_base = hp.tmpl_slot_base[a];
+        const int64_t base = hp.ref_off[a];
+        const int64_t o_ib = base + (int64_t)hp.ii_idx[a].size(), o_bb = o_ib + (int64_t)hp.ib_idx[a].size();
+        const int64_t o_bi = o_bb + (int64_t)nb * nb, o_bbv = o_bi + ni;
+        auto find = [](const std::vector<int32_t>& ptr, const std::vector<int32_t>& idx, int r, int c) {
+            return (int64_t)(std::lower_bound(idx.begin() + ptr[r], idx.begin() + ptr[r + 1], c) - idx.begin());
+        };
+        for (size_t k = 0; k < rows.size(); ++k) {
+            const int s0 = slot_ptr[k], s1 = slot_ptr[k + 1];
+            for (int x = s0; x < s1; ++x) {
+                const int va = slot_var[x];
+                for (int y = s0; y < s1; ++y) {
+                    const int vb = slot_var[y]; int64_t dest;
+                    if (va < ni && vb < ni) dest = base + find(hp.ii_ptr[a], hp.ii_idx[a], va, vb);
+                    else if (va < ni) dest = o_ib + find(hp.ib_ptr[a], hp.ib_idx[a], va, vb - ni);
+                    else if (vb >= ni) dest = o_bb + (int64_t)(va - ni) * nb + (vb - ni);
+                    else continue;
+                    rdest.push_back(dest); ra.push_back((int32_t)(slot_base + x)); rb.push_back((int32_t)(slot_base + y));
+                }
+            }
+            for (int x = s0; x < s1; ++x) {
+                const int v = slot_var[x];
+                rdest.push_back(v < ni ? o_bi + v : o_bbv + (v - ni)); ra.push_back((int32_t)(slot_base + x)); rb.push_back(-(rows[k] + 1));
+            }
+        }
+    }
+    auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(hp.n_slots + b) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
+    hp.racc_ptr.assign(hp.n_ref_vals + 1, 0);
+    for (int64_t dd : rdest) hp.racc_ptr[dd + 1]++;
+    for (int64_t i = 0; i < hp.n_ref_vals; ++i) hp.racc_ptr[i + 1] += hp.racc_ptr[i];
+    hp.racc_a.resize(rdest.size()); hp.racc_b.resize(rdest.size());
+    std::vector<int32_t> cur(hp.racc_ptr.begin(), hp.racc_ptr.end() - 1);
+    for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = ra[i]; hp.racc_b[q] = val_index(rb[i]); }
 }
 
 }  // namespace gse

@@ -60,10 +60,8 @@ class SolverConfig:
             raise ValueError(f"unknown backend {self.backend!r}")
         if self.boundary not in ("auto", "dense", "sparse"):
             raise ValueError(f"unknown boundary mode {self.boundary!r}")
-        if self.inner_gn_steps != 1:
-            raise NotImplementedError(
-                "inner_gn_steps > 1 is not implemented on the device path yet "
-                "(SURVEY.md section 8 row f2)")
+        if self.inner_gn_steps < 1:
+            raise ValueError("inner_gn_steps must be >= 1")
 
     @property
     def effective_dense_threshold(self):
@@ -178,7 +176,7 @@ class MultiAreaEstimator:
         va_ptr, vm_ptr = self._ptrs()
         self.torch.cuda.current_stream(self.device).synchronize()
         try:
-            if on_iteration is None:
+            if on_iteration is None and cfg.inner_gn_steps == 1:
                 rep = self.plan.solve(va_ptr, vm_ptr, cfg.max_outer_iterations,
                                       cfg.convergence_tol, cfg.profile_phases)
                 iterations, converged, j = rep.iterations, bool(rep.converged), rep.objective
@@ -194,10 +192,16 @@ class MultiAreaEstimator:
                 self.last_deltas = []
                 t0 = time.perf_counter()
                 for it in range(1, cfg.max_outer_iterations + 1):
-                    delta = self.plan.iterate(va_ptr, vm_ptr)
+                    # inner GN steps on the interiors with the boundary held fixed (all but the last,
+                    # whose blocks feed the condensation -- reference solver.py:253-260)
+                    inner = 0.0
+                    for _ in range(cfg.inner_gn_steps - 1):
+                        inner = max(inner, self.plan.inner_step(va_ptr, vm_ptr))
+                    delta = max(inner, self.plan.iterate(va_ptr, vm_ptr))
                     iterations = it
                     self.last_deltas.append(delta)
-                    on_iteration(it, self._read_state(), delta)
+                    if on_iteration is not None:
+                        on_iteration(it, self._read_state(), delta)
                     if delta < cfg.convergence_tol:
                         converged = True
                         break

@@ -129,6 +129,19 @@ def main(which):
         solve_and_record("rand120_k4", net, ms, R.partition_network(net, 4, seed=1), True,
                          recipe={"gen": "random_network(120, 3, 0.3)", "meas_seed": 2, "k": 4,
                                  "part_seed": 1})
+    if "inner" in which:
+        # inner_gn_steps > 1 (reference solver.py:253-260): extra interior-only GN steps per outer round
+        net = R.load_case("/root/reference/pkg/cases/ieee118.m")
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=0))
+        solve_and_record("ieee118_k6_inner2", net, ms, R.partition_network(net, 6, seed=0), True,
+                         cfg=R.SolverConfig(inner_gn_steps=2),
+                         recipe={"case": "ieee118.m", "meas_seed": 0, "k": 6, "part_seed": 0, "inner": 2})
+        net = random_network(120, 3, 0.3)
+        ms = R.generate_measurements(net, R.MeasurementConfig(seed=2))
+        solve_and_record("rand120_k4_inner3", net, ms, R.partition_network(net, 4, seed=1), True,
+                         cfg=R.SolverConfig(inner_gn_steps=3),
+                         recipe={"gen": "random_network(120, 3, 0.3)", "meas_seed": 2, "k": 4,
+                                 "part_seed": 1, "inner": 3})
     for shape in ("pegase2869", "pegase9241", "activsg10k"):
         if shape not in which:
             continue

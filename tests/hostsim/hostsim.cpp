@@ -209,6 +209,7 @@ void hostsim_area_schur(void* h, int a, double* s_b, double* b_hat) {
 }
 void hostsim_ref_blocks(void* h, double* out) {   // reference-layout values of all areas, concatenated
     Sim* s = (Sim*)h; std::vector<double> v(s->hp.n_ref_vals);
+    build_reference_program(s->hp);
     accumulate(*s, s->hp.racc_ptr, s->hp.racc_a, s->hp.racc_b, v);
     memcpy(out, v.data(), v.size() * sizeof(double));
 }

@@ -290,3 +290,22 @@ def test_weight_scaling_property_full_size(G):
     assert r1.iterations == r2.iterations == int(g["iterations"])
     assert max(np.max(np.abs(e1.va - e2.va)), np.max(np.abs(e1.vm - e2.vm))) < 1e-10
     assert r2.objective == pytest.approx(4.0 * r1.objective, rel=1e-10)
+
+
+@pytest.mark.parametrize("name,inner", [("ieee118_k6_inner2", 2), ("rand120_k4_inner3", 3)])
+def test_inner_gn_steps_match_reference_golden(G, name, inner):
+    """SolverConfig.inner_gn_steps > 1 (reference solver.py:253-260): same iteration count, per-iteration
+    stacked norms, iterates, final state and J as the reference run stored in the fixture."""
+    net, ms, part, g = build_case(name)
+    trace = []
+    est, rep = G.solve_multiarea(net, ms, part, config=G.SolverConfig(inner_gn_steps=inner),
+                                 on_iteration=lambda it, s, d: trace.append((s, d)))
+    assert rep.iterations == int(g["iterations"]) and rep.converged == bool(g["converged"])
+    assert np.allclose([d for _, d in trace], g["deltas"], rtol=1e-6, atol=1e-12)
+    for (s, _), va, vm in zip(trace, g["trace_va"], g["trace_vm"]):
+        assert np.max(np.abs(s.va - va)) < 1e-9 and np.max(np.abs(s.vm - vm)) < 1e-9
+    assert _state_err(est.va, est.vm, g["va"], g["vm"]) < 1e-8
+    assert abs(rep.objective - float(g["objective"])) <= 1e-10 * float(g["objective"])
+    # without the callback the same loop runs (inner steps are host-sequenced): identical result
+    est2, rep2 = G.solve_multiarea(net, ms, part, config=G.SolverConfig(inner_gn_steps=inner))
+    assert rep2.iterations == rep.iterations and np.array_equal(est2.va, est.va) and np.array_equal(est2.vm, est.vm)

@@ -64,6 +64,18 @@ def test_solve_matches_reference(name):
         assert np.max(np.abs(res["trace_vm"] - g["trace_vm"])) < 1e-9
 
 
+@pytest.mark.parametrize("name,inner", [("ieee118_k6_inner2", 2), ("rand120_k4_inner3", 3)])
+def test_inner_gn_steps_match_reference(name, inner):
+    # SolverConfig.inner_gn_steps > 1 (reference solver.py:253-260)
+    net, ms, part, g = build_case(name)
+    res = Oracle(net, ms, part.area_of_bus).solve(trace=True, inner=inner)
+    assert res["iterations"] == int(g["iterations"]) and res["converged"] == bool(g["converged"])
+    assert np.allclose(res["deltas"], g["deltas"], rtol=1e-6, atol=1e-12)
+    assert np.max(np.abs(res["trace_va"] - g["trace_va"])) < 1e-9
+    assert np.max(np.abs(res["trace_vm"] - g["trace_vm"])) < 1e-9
+    assert abs(res["objective"] - float(g["objective"])) <= 1e-10 * float(g["objective"])
+
+
 def test_reference_hand_values_dense_solve():
     # reference tests/test_linalg.py:42-50: [[4,2],[2,3]] x = [2,1] -> [0.5, 0]; pivot 1 of [[1,2],[2,1]]
     x = dense_cholesky_solve(np.array([[4.0, 2.0], [2.0, 3.0]]), np.array([2.0, 1.0]))
