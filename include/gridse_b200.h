@@ -162,6 +162,30 @@ int gse_boundary_system(gse_plan *plan, double *s_gamma, double *b_gamma, double
  * caller-supplied delta_xb, linalg.py:427). */
 int gse_set_boundary_delta(gse_plan *plan, const double *dx_gamma);
 
+/* ---- standalone linear algebra on caller-supplied matrices (reference linalg.py) ------------------
+ * A matrix plan is a one-area Schur-mode plan whose blocks come from the caller instead of from
+ * measurement templates; it reuses the plan type (gse_plan_destroy, gse_last_error, gse_area_schur). */
+/* symbolic_analyze (linalg.py:395-398) for G_ii [n_i x n_i, CSR, sorted columns, structurally
+ * symmetric] with the coupling pattern of G_ib [n_i x n_b CSR] that schur_condense will be given.
+ * opt->backend_dense = 1: one dense chain in natural order (dense_cholesky_solve, linalg.py:46-61). */
+int gse_matrix_plan_create(int32_t n_i, int32_t n_b, const int32_t *ii_ptr, const int32_t *ii_idx,
+                           const int32_t *ib_ptr, const int32_t *ib_idx, const gse_options *opt,
+                           gse_plan **out);
+/* Values in the reference's block layout (AreaNormalBlocks, assembly.py:32-53): data_ii / data_ib
+ * aligned with the CSR patterns, g_bb row-major n_b x n_b, b_i, b_b.  NULL = zeros.  Host arrays. */
+int gse_matrix_set_values(gse_plan *plan, const double *data_ii, const double *data_ib,
+                          const double *g_bb, const double *b_i, const double *b_b);
+/* numeric_refactor + schur_condense (linalg.py:401-424); then gse_area_schur(plan, 0, ...) returns
+ * (S_b, b_hat).  GSE_E_NOT_SPD_AREA with the original pivot index on a non-positive pivot. */
+int gse_matrix_condense(gse_plan *plan);
+/* interior_recover (linalg.py:427-434): dx_i = G_ii^-1 (b_i - G_ib dx_b) with the factor and b_i of the
+ * last gse_matrix_condense; dx_b NULL = zeros (a plain cache.solve(b_i)). */
+int gse_matrix_recover(gse_plan *plan, const double *dx_b, double *dx_i);
+/* assemble_boundary (solver.py:106-119) for caller-supplied Schur blocks: s_b = the areas' n_b x n_b
+ * blocks concatenated, b_hat likewise, sel_ptr / sel the boundary selectors.  Host in, host out. */
+int gse_assemble_boundary(int32_t n_gamma, int32_t n_areas, const int32_t *sel_ptr, const int32_t *sel,
+                          const double *s_b, const double *b_hat, double *s_gamma, double *b_gamma);
+
 /* ---- multi-GPU exchange buffers ---------------------------- */
 /* Device pointer + length (doubles) of the packed per-area (S_b | b_hat) exchange buffer;
  * area a occupies [off[a], off[a+1]) with off = gse_exchange_offsets (n_areas+1 entries);
@@ -180,6 +204,12 @@ double *gse_status_dev(gse_plan *plan);
  * iteration (SURVEY.md section 8(d) A_min), [10]=dense flops per iteration (fronts),
  * [11]=launches per iteration. */
 int gse_plan_stats(const gse_plan *plan, double *stats, int32_t n);
+/* Item layout of one iteration of the persistent kernel: out[0..4] = eval, accumulate, front, backward,
+ * update items; out[5] = resident CTAs, out[6] = dynamic shared memory, out[7] = 1 if gse_solve uses it. */
+int gse_solve_layout(const gse_plan *plan, int32_t *out);
+/* Debug: per-item timeline of the persistent kernel (tools/persist_trace.py).  enable = 1 arms tracing for
+ * the next solves; enable = 0 copies [items][32] words to out and disarms.  Returns items per iteration. */
+int gse_debug_trace(gse_plan *plan, int enable, unsigned long long *out, int64_t max_words);
 /* The CUDA stream (cudaStream_t) every kernel of the plan is launched on. */
 void *gse_stream(gse_plan *plan);
 const char *gse_version(void);

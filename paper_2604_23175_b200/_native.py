@@ -102,6 +102,11 @@ def lib():
     L.gse_solve.argtypes = [vp, C.POINTER(Config), vp, vp, C.POINTER(Report)]
     L.gse_iterate.argtypes = [vp, vp, vp, f64p]
     L.gse_inner_step.argtypes = [vp, vp, vp, f64p]
+    L.gse_matrix_plan_create.argtypes = [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, C.POINTER(Options), C.POINTER(vp)]
+    L.gse_matrix_set_values.argtypes = [vp, f64p, f64p, f64p, f64p, f64p]
+    L.gse_matrix_condense.argtypes = [vp]
+    L.gse_matrix_recover.argtypes = [vp, f64p, f64p]
+    L.gse_assemble_boundary.argtypes = [C.c_int32, C.c_int32, i32p, i32p, f64p, f64p, f64p, f64p]
     L.gse_phase_assemble.argtypes = [vp, vp, vp]
     L.gse_phase_condense.argtypes = [vp]
     L.gse_phase_boundary.argtypes = [vp]
@@ -136,7 +141,8 @@ EXPORTED = [
     "gse_area_dims", "gse_area_pattern", "gse_area_blocks", "gse_area_schur", "gse_area_delta",
     "gse_boundary_system", "gse_set_boundary_delta", "gse_exchange_buffer_dev",
     "gse_exchange_offsets", "gse_boundary_delta_dev", "gse_status_dev", "gse_plan_stats",
-    "gse_version", "gse_stream",
+    "gse_version", "gse_stream", "gse_matrix_plan_create", "gse_matrix_set_values", "gse_matrix_condense",
+    "gse_matrix_recover", "gse_assemble_boundary", "gse_debug_trace", "gse_solve_layout",
 ]
 
 
@@ -382,3 +388,84 @@ class Plan:
                 "update_doubles", "pair_contributions", "slots", "alg_bytes", "dense_flops",
                 "launches_per_iter", "persistent", "solve_ctas", "solve_smem_bytes", "items_per_iteration")
         return dict(zip(keys, (float(v) for v in s)))
+
+
+class MatrixPlan:
+    """One-area Schur-mode plan on caller-supplied blocks (``gse_matrix_*``): the device engine
+    behind ``linalg.symbolic_analyze / numeric_refactor / schur_condense / interior_recover /
+    dense_cholesky_solve``."""
+
+    def __init__(self, n_i, n_b, ii_ptr, ii_idx, ib_ptr=None, ib_idx=None, *, dense=False, device=0):
+        L = lib()
+        self.n_i, self.n_b = int(n_i), int(n_b)
+        self._keep = [np.ascontiguousarray(a, dtype=np.int32) if a is not None else None
+                      for a in (ii_ptr, ii_idx, ib_ptr, ib_idx)]
+        for i in (1, 3):        # ctypes needs a non-null buffer even for empty index lists
+            if self._keep[i] is not None and self._keep[i].size == 0:
+                self._keep[i] = np.zeros(1, dtype=np.int32)
+        opt = Options()
+        opt.device, opt.backend_dense = int(device), int(bool(dense))
+        self._h = C.c_void_p()
+        args = [(_ip(a) if a is not None else None) for a in self._keep]
+        rc = L.gse_matrix_plan_create(self.n_i, self.n_b, *args, C.byref(opt), C.byref(self._h))
+        if rc != GSE_OK:
+            if not self._h:
+                raise NativeError(rc, -1, -1, "invalid matrix pattern")
+            err = self._error()
+            self.close()
+            raise err
+
+    _error = Plan._error
+    _call = Plan._call
+    close = Plan.close
+    __del__ = Plan.__del__
+
+    @staticmethod
+    def _opt(a):
+        if a is None:
+            return None, None
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        return a, (_fp(a) if a.size else None)
+
+    def set_values(self, data_ii=None, data_ib=None, g_bb=None, b_i=None, b_b=None):
+        keep = [self._opt(a) for a in (data_ii, data_ib, g_bb, b_i, b_b)]
+        self._call(lib().gse_matrix_set_values(self._h, *[k[1] for k in keep]))
+
+    def condense(self):
+        self._call(lib().gse_matrix_condense(self._h))
+
+    def schur(self):
+        s_b, b_hat = np.zeros((self.n_b, self.n_b)), np.zeros(self.n_b)
+        if self.n_b:
+            self._call(lib().gse_area_schur(self._h, 0, _fp(s_b), _fp(b_hat)))
+        return s_b, b_hat
+
+    def recover(self, dx_b=None):
+        dx_i = np.zeros(max(self.n_i, 1))
+        k = self._opt(dx_b)
+        self._call(lib().gse_matrix_recover(self._h, k[1], _fp(dx_i)))
+        return dx_i[:self.n_i]
+
+
+def assemble_boundary_device(s_blocks, b_hats, selectors, n_gamma):
+    """``gse_assemble_boundary``: S_Gamma / b_Gamma summed on the device in area order."""
+    sel_ptr = np.zeros(len(selectors) + 1, dtype=np.int32)
+    sel_ptr[1:] = np.cumsum([len(s) for s in selectors])
+    sel = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.int32) for s in selectors] or [np.zeros(0, np.int32)]))
+    sb = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.float64).ravel() for s in s_blocks] or [np.zeros(0)]))
+    bh = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.float64).ravel() for b in b_hats] or [np.zeros(0)]))
+    if sel.size == 0:
+        sel = np.zeros(1, dtype=np.int32)
+    if sb.size == 0:
+        sb = np.zeros(1)
+    if bh.size == 0:
+        bh = np.zeros(1)
+    s_gamma, b_gamma = np.zeros((n_gamma, n_gamma)), np.zeros(n_gamma)
+    out_s = s_gamma if n_gamma else np.zeros((1, 1))
+    out_b = b_gamma if n_gamma else np.zeros(1)
+    rc = lib().gse_assemble_boundary(int(n_gamma), len(selectors), _ip(sel_ptr), _ip(sel), _fp(sb), _fp(bh), _fp(out_s), _fp(out_b))
+    if rc == GSE_E_NO_DEVICE:
+        raise NoDeviceError(rc, -1, -1, "no CUDA device visible: gridse-b200 has no CPU fallback")
+    if rc != GSE_OK:
+        raise NativeError(rc, -1, -1, "gse_assemble_boundary failed")
+    return s_gamma, b_gamma

@@ -226,7 +226,13 @@ const char* gse_version(void) { return "gridse-b200 0.1.0 (sm_100a)"; }
 
 const gse_error* gse_last_error(const gse_plan* plan) { return &plan->err; }
 
+static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildOptions bo, gse_plan** out);
+
 int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan** out) {
+    return create_plan(d, opt, BuildOptions{}, out);
+}
+
+static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildOptions bo, gse_plan** out) {
     if (!d || !out) return GSE_E_INVALID;
     gse_plan* plan = new gse_plan();
     *out = plan;
@@ -235,7 +241,6 @@ int gse_plan_create(const gse_problem_desc* d, const gse_options* opt, gse_plan*
         return fail(plan, GSE_E_NO_DEVICE, "no CUDA device visible: gridse-b200 has no CPU fallback");
     plan->device = opt ? opt->device : 0;
     CU(cudaSetDevice(plan->device));
-    BuildOptions bo;
     if (opt) {
         bo.dense = opt->backend_dense != 0;
         if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
@@ -646,6 +651,125 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
     { float ms = 0; cudaEventElapsedTime(&ms, plan->ev[6], plan->ev[7]); rep->gpu_s = ms * 1e-3; }
     if (status != GSE_OK) return status;
     return gse_objective(plan, va, vm, &rep->objective);
+}
+
+// ---- generic Schur-mode matrix plans (standalone linear algebra of reference linalg.py) ---------
+// One "area" whose interior block G_ii and coupling G_ib are given by pattern; the forward pass of
+// the multifrontal tree is numeric_refactor + schur_condense, the interior back-substitution is
+// interior_recover / cache.solve.  Built from a synthetic one-area problem without measurement rows
+// (every variable is the magnitude of its own bus), as a non-coordinator rank so that the tree stops
+// at the area root (= S_b | b_hat).
+int gse_matrix_plan_create(int32_t n_i, int32_t n_b, const int32_t* ii_ptr, const int32_t* ii_idx, const int32_t* ib_ptr,
+                           const int32_t* ib_idx, const gse_options* opt, gse_plan** out) {
+    if (n_i < 0 || n_b < 0 || n_i + n_b == 0 || !out || (n_i && (!ii_ptr || !ii_idx))) return GSE_E_INVALID;
+    const int n = n_i + n_b;
+    std::vector<int32_t> zero1{0, 0}, y_ptr(n + 1, 0), aob(n, 0), im_ptr{0, n_i}, bm_ptr{0, n_b}, sel_ptr{0, n_b};
+    std::vector<int32_t> im_bus(n_i), bm_bus(n_b), sel(n_b), gbus(n_b), gq(n_b, 1);
+    for (int i = 0; i < n_i; ++i) im_bus[i] = i;
+    for (int j = 0; j < n_b; ++j) { bm_bus[j] = n_i + j; sel[j] = j; gbus[j] = n_i + j; }
+    int32_t none = 0; double nonef = 0.0;
+    gse_problem_desc d{};
+    d.n_bus = n; d.n_branch = 0; d.n_rows = 0; d.n_areas = 1; d.n_gamma = n_b; d.slack = -1;
+    d.y_ptr = y_ptr.data(); d.y_idx = &none; d.y_g = &nonef; d.y_b = &nonef;
+    d.br_from = &none; d.br_to = &none; d.br_y = &nonef;
+    d.m_type = &none; d.m_target = &none; d.m_z = &nonef; d.m_w = &nonef;
+    d.area_of_bus = aob.data();
+    d.ia_ptr = zero1.data(); d.ia_bus = &none; d.im_ptr = im_ptr.data(); d.im_bus = im_bus.data();
+    d.ba_ptr = zero1.data(); d.ba_bus = &none; d.bm_ptr = bm_ptr.data(); d.bm_bus = bm_bus.data();
+    d.sel_ptr = sel_ptr.data(); d.sel = sel.data(); d.gamma_bus = gbus.data(); d.gamma_quant = gq.data();
+    BuildOptions bo;
+    bo.ext_pattern = true;
+    bo.ext_ii_ptr.assign(ii_ptr ? ii_ptr : zero1.data(), (ii_ptr ? ii_ptr : zero1.data()) + n_i + 1);
+    bo.ext_ii_idx.assign(ii_idx, ii_idx + bo.ext_ii_ptr[n_i]);
+    if (ib_ptr) { bo.ext_ib_ptr.assign(ib_ptr, ib_ptr + n_i + 1); bo.ext_ib_idx.assign(ib_idx, ib_idx + ib_ptr[n_i]); }
+    else bo.ext_ib_ptr.assign(n_i + 1, 0);
+    for (int u = 0; u < n_i; ++u) {
+        for (int p = bo.ext_ii_ptr[u]; p < bo.ext_ii_ptr[u + 1]; ++p)
+            if (bo.ext_ii_idx[p] < 0 || bo.ext_ii_idx[p] >= n_i || (p > bo.ext_ii_ptr[u] && bo.ext_ii_idx[p] <= bo.ext_ii_idx[p - 1])) return GSE_E_INVALID;
+        for (int p = bo.ext_ib_ptr[u]; p < bo.ext_ib_ptr[u + 1]; ++p)
+            if (bo.ext_ib_idx[p] < 0 || bo.ext_ib_idx[p] >= n_b || (p > bo.ext_ib_ptr[u] && bo.ext_ib_idx[p] <= bo.ext_ib_idx[p - 1])) return GSE_E_INVALID;
+    }
+    gse_options o{};
+    if (opt) o = *opt;
+    o.rank = 1; o.world = 2;                  // not the coordinator: no boundary factorisation
+    const int32_t owner = 1;
+    o.area_rank = &owner;
+    o.persistent = 2;
+    return create_plan(&d, &o, bo, out);
+}
+
+// values in the reference's block layout (AreaNormalBlocks); nullptr = zeros
+int gse_matrix_set_values(gse_plan* plan, const double* data_ii, const double* data_ib, const double* g_bb, const double* b_i,
+                          const double* b_b) {
+    const HostProgram& hp = plan->hp;
+    if (hp.gval_src.size() != (size_t)hp.n_gval) return fail(plan, GSE_E_INVALID, "not a matrix plan");
+    CU(cudaSetDevice(plan->device));
+    const int64_t nii = (int64_t)hp.ii_idx[0].size(), nib = (int64_t)hp.ib_idx[0].size(), nb = hp.area_nb[0], ni = hp.area_ni[0];
+    const int64_t o_ib = nii, o_bb = o_ib + nib, o_bi = o_bb + nb * nb, o_bbv = o_bi + ni;
+    std::vector<double> g((size_t)hp.n_gval, 0.0);
+    for (size_t e = 0; e < g.size(); ++e) {
+        const int64_t s = hp.gval_src[e];
+        if (s < 0) continue;
+        const double* src = s < o_ib ? data_ii : s < o_bb ? data_ib : s < o_bi ? g_bb : s < o_bbv ? b_i : b_b;
+        const int64_t off = s < o_ib ? 0 : s < o_bb ? o_ib : s < o_bi ? o_bb : s < o_bbv ? o_bi : o_bbv;
+        if (src) g[e] = src[s - off];
+    }
+    CU(cudaMemcpy(plan->gval.ptr, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return GSE_OK;
+}
+
+// numeric_refactor + schur_condense: the forward pass over the interior fronts and the area root
+int gse_matrix_condense(gse_plan* plan) {
+    CU(cudaSetDevice(plan->device));
+    enqueue_fwd(plan, 1);
+    return gse_check(plan);
+}
+
+// interior_recover: dx_i = G_ii^-1 (b_i - G_ib dx_b) from the factor of the last gse_matrix_condense
+int gse_matrix_recover(gse_plan* plan, const double* dx_b, double* dx_i) {
+    const HostProgram& hp = plan->hp;
+    CU(cudaSetDevice(plan->device));
+    if (hp.n_gamma) {
+        if (dx_b) CU(cudaMemcpy(plan->xsol.ptr + hp.gamma_base, dx_b, sizeof(double) * hp.n_gamma, cudaMemcpyHostToDevice));
+        else CU(cudaMemset(plan->xsol.ptr + hp.gamma_base, 0, sizeof(double) * hp.n_gamma));
+    }
+    enqueue_bwd(plan, 4);
+    CU(cudaStreamSynchronize(plan->stream));
+    return gse_area_delta(plan, 0, dx_i);
+}
+
+// assemble_boundary (solver.py:106-119): S_Gamma[sel, sel] += S_b, b_Gamma[sel] += b_hat, areas in
+// ascending order.  Host in / host out; the sums run on the device in area order per entry.
+int gse_assemble_boundary(int32_t n_gamma, int32_t n_areas, const int32_t* sel_ptr, const int32_t* sel, const double* s_b,
+                          const double* b_hat, double* s_gamma, double* b_gamma) {
+    if (n_gamma < 0 || n_areas < 0) return GSE_E_INVALID;
+    if (n_gamma == 0) return GSE_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return GSE_E_NO_DEVICE;
+    std::vector<int32_t> inv((size_t)n_areas * n_gamma, -1);
+    std::vector<int64_t> off(n_areas + 1, 0);
+    for (int a = 0; a < n_areas; ++a) {
+        const int nb = sel_ptr[a + 1] - sel_ptr[a];
+        off[a + 1] = off[a] + (int64_t)nb * nb;
+        for (int i = 0; i < nb; ++i) {
+            const int s = sel[sel_ptr[a] + i];
+            if (s < 0 || s >= n_gamma) return GSE_E_INVALID;
+            inv[(size_t)a * n_gamma + s] = i;
+        }
+    }
+    DevBuf<int32_t> d_inv, d_selptr; DevBuf<int64_t> d_off; DevBuf<double> d_sb, d_bh, d_sg, d_bg;
+    cudaError_t e = cudaSuccess;
+    auto ok = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+    ok(d_inv.upload(inv)); ok(d_off.upload(off)); ok(d_selptr.upload(std::vector<int32_t>(sel_ptr, sel_ptr + n_areas + 1)));
+    ok(d_sb.upload(std::vector<double>(s_b, s_b + off[n_areas]))); ok(d_bh.upload(std::vector<double>(b_hat, b_hat + sel_ptr[n_areas])));
+    ok(d_sg.alloc((size_t)n_gamma * n_gamma)); ok(d_bg.alloc(n_gamma));
+    if (e == cudaSuccess) {
+        launch_assemble_boundary(n_gamma, n_areas, d_inv.ptr, d_off.ptr, d_selptr.ptr, d_sb.ptr, d_bh.ptr, d_sg.ptr, d_bg.ptr, nullptr);
+        ok(cudaMemcpy(s_gamma, d_sg.ptr, sizeof(double) * (size_t)n_gamma * n_gamma, cudaMemcpyDeviceToHost));
+        ok(cudaMemcpy(b_gamma, d_bg.ptr, sizeof(double) * n_gamma, cudaMemcpyDeviceToHost));
+    }
+    d_inv.release(); d_off.release(); d_selptr.release(); d_sb.release(); d_bh.release(); d_sg.release(); d_bg.release();
+    return e == cudaSuccess ? GSE_OK : GSE_E_CUDA;
 }
 
 // ---- phase-level entry points ------------------------------------------------------------------

@@ -101,6 +101,37 @@ __global__ void __launch_bounds__(256) objective_final_kernel(const double* __re
     if (threadIdx.x == 0) *out = red[0];
 }
 
+// assemble_boundary (reference solver.py:106-119) for caller-supplied Schur blocks: one thread per
+// entry of S_Gamma (and one per entry of b_Gamma), areas added in ascending order -> the same sums
+// in the same order as the reference's loop.  inv[a][slot] = local boundary index of x_Gamma slot.
+__global__ void __launch_bounds__(256) assemble_boundary_kernel(int n_gamma, int n_areas, const int32_t* __restrict__ inv,
+                                                                const int64_t* __restrict__ off, const int32_t* __restrict__ sel_ptr,
+                                                                const double* __restrict__ s_b, const double* __restrict__ b_hat,
+                                                                double* __restrict__ s_gamma, double* __restrict__ b_gamma) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nn = (int64_t)n_gamma * n_gamma;
+    if (t < nn) {
+        const int I = (int)(t / n_gamma), J = (int)(t % n_gamma);
+        double s = 0.0;
+        for (int a = 0; a < n_areas; ++a) {
+            const int i = inv[(size_t)a * n_gamma + I], j = inv[(size_t)a * n_gamma + J];
+            if (i >= 0 && j >= 0) s += s_b[off[a] + (int64_t)i * (sel_ptr[a + 1] - sel_ptr[a]) + j];
+        }
+        s_gamma[t] = s;
+    } else if (t < nn + n_gamma) {
+        const int I = (int)(t - nn);
+        double s = 0.0;
+        for (int a = 0; a < n_areas; ++a) { const int i = inv[(size_t)a * n_gamma + I]; if (i >= 0) s += b_hat[sel_ptr[a] + i]; }
+        b_gamma[I] = s;
+    }
+}
+
+void launch_assemble_boundary(int n_gamma, int n_areas, const int32_t* inv, const int64_t* off, const int32_t* sel_ptr,
+                              const double* s_b, const double* b_hat, double* s_gamma, double* b_gamma, cudaStream_t s) {
+    const int64_t n = (int64_t)n_gamma * n_gamma + n_gamma;
+    assemble_boundary_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n_gamma, n_areas, inv, off, sel_ptr, s_b, b_hat, s_gamma, b_gamma);
+}
+
 cudaError_t configure_unit_kernels() {
     return cudaFuncSetAttribute(accumulate_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccSmemBytes);
 }

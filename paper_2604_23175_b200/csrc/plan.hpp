@@ -93,6 +93,7 @@ struct HostProgram {
     std::vector<int32_t> reg_ptr;        // flattened per-front region pointers
     std::vector<int32_t> front_reg_off;  // per front offset into reg_ptr
     int64_t n_gval = 0, n_lbuf = 0, n_ubuf = 0;
+    std::vector<int64_t> gval_src;       // generic matrix plan: source of every original entry in the caller's layout
     // exchange buffer = U storage of the area roots, contiguous in area order
     int64_t xchg_off = 0, xchg_len = 0;
     std::vector<int64_t> xchg_area_off;  // n_areas + 1 (relative to xchg_off)
@@ -124,6 +125,10 @@ struct BuildOptions {
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;
+    // generic matrix plan (gse_matrix_plan_create): one area whose G_ii / G_ib patterns come from the
+    // caller instead of from measurement templates
+    bool ext_pattern = false;
+    std::vector<int32_t> ext_ii_ptr, ext_ii_idx, ext_ib_ptr, ext_ib_idx;
 };
 
 // symbolic.cpp

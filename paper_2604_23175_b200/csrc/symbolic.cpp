@@ -421,7 +421,10 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         sec(0);
         // ---- reference-layout CSR patterns of G_ii, G_ib ------------------------------
         // (per interior variable: the sorted, de-duplicated columns its rows reach)
-        {
+        if (opt.ext_pattern) {      // generic matrix plan: the caller supplies the patterns
+            hp.ii_ptr[a] = opt.ext_ii_ptr; hp.ii_idx[a] = opt.ext_ii_idx;
+            hp.ib_ptr[a] = opt.ext_ib_ptr; hp.ib_idx[a] = opt.ext_ib_idx;
+        } else {
             std::vector<std::vector<int>> cols_ii(ni), cols_ib(ni);
             for (size_t k = 0; k < A.rows.size(); ++k)
                 for (int x = A.slot_ptr[k]; x < A.slot_ptr[k + 1]; ++x) {
@@ -635,6 +638,36 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 hp.reg_ptr.insert(hp.reg_ptr.end(), rp.begin(), rp.end());
                 for (size_t i = 0; i < ents.size(); ++i) { hp.orig_pos.push_back(ents[i].pos); A.col_dest[ents[i].q] = hp.n_gval + (int64_t)i; }
                 hp.n_gval += (int64_t)ents.size();
+            }
+            if (opt.ext_pattern) {
+                // where every original entry comes from, as an index into the caller's value layout
+                // [data_ii | data_ib | g_bb (row-major) | b_i | b_b]  (AreaNormalBlocks, assembly.py:32-53)
+                const int64_t o_ib = (int64_t)hp.ii_idx[a].size(), o_bb = o_ib + (int64_t)hp.ib_idx[a].size();
+                const int64_t o_bi = o_bb + (int64_t)nb * nb, o_bbv = o_bi + ni;
+                hp.gval_src.assign((size_t)hp.n_gval, -1);
+                auto find = [](const std::vector<int32_t>& ptr, const std::vector<int32_t>& idx, int r, int c) -> int64_t {
+                    auto b = idx.begin() + ptr[r], e = idx.begin() + ptr[r + 1];
+                    auto it = std::lower_bound(b, e, c);
+                    return (it == e || *it != c) ? -1 : (int64_t)(it - idx.begin());
+                };
+                for (int c = 0; c < nloc; ++c)
+                    for (int q = A.col_ptr[c]; q < A.col_ptr[c + 1]; ++q) {
+                        const int r = A.col_row[q];
+                        const int64_t dst = A.col_dest[q];
+                        if (dst < 0) continue;
+                        int64_t src;
+                        if (c < ni) {
+                            const int uc = A.order[c];
+                            if (r == nloc) src = o_bi + uc;
+                            else if (r < ni) src = find(hp.ii_ptr[a], hp.ii_idx[a], A.order[r], uc);
+                            else { const int64_t f = find(hp.ib_ptr[a], hp.ib_idx[a], uc, bvar_of_pos[a][r - ni]); src = f < 0 ? -1 : o_ib + f; }
+                        } else {
+                            const int bc = bvar_of_pos[a][c - ni];
+                            if (r == nloc) src = o_bbv + bc;
+                            else src = o_bb + (int64_t)bvar_of_pos[a][r - ni] * nb + bc;
+                        }
+                        hp.gval_src[(size_t)dst] = src;
+                    }
             }
         } else {
             choose_chunks(hp.fronts[root_id], opt.tile_rows);

@@ -237,6 +237,14 @@ def objective(ms: MeasurementSet, state: StateVector) -> float:
         est.close()
 
 
+def assemble_boundary(schur_results, selectors, n_gamma) -> BoundarySystem:
+    """S_Gamma[sel, sel] += S_b, b_Gamma[sel] += b_hat, areas in ascending order (reference
+    solver.py:106-119), summed on the device (``gse_assemble_boundary``)."""
+    s_gamma, b_gamma = _native.assemble_boundary_device(
+        [r.s_b for r in schur_results], [r.b_hat for r in schur_results], selectors, int(n_gamma))
+    return BoundarySystem(s_gamma=s_gamma, b_gamma=b_gamma)
+
+
 def solve_multiarea(net, ms: MeasurementSet, part, maps=None, config: SolverConfig = None,
                     on_iteration=None):
     """Boundary-condensed multi-area WLS-GN; returns (estimate, report).
