@@ -26,8 +26,11 @@ struct GatherArgs {
     int p, ld, ldt, rp, Rp, ni, nj, diag, direct, warp, lane, nwarps;
 };
 
-// NB children of one batch, compile-time so that empty child slots cost no instructions
-template <int NB>
+// NB children of one batch, compile-time so that empty child slots cost no instructions.
+// G row groups per warp and sweep: G * 2 * NB independent loads per thread in flight (16 with the
+// usual two children and G = 4; G = 8 only for a single child: more would spill under the 128-register cap
+// of the persistent kernel).
+template <int NB, int G>
 __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec* __restrict__ crec) {
     const int p = a.p, ld = a.ld, ldt = a.ldt, rp = a.rp, Rp = a.Rp, ni = a.ni, nj = a.nj;
     const int warp = a.warp, lane = a.lane, nwarps = a.nwarps;
@@ -36,8 +39,8 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
     for (int c = 0; c < NB; ++c) Ub[c] = a.ubuf + crec[c].u_off;
     // panel rows [pivots | I | J] x pivot columns
     if (p) {
-        for (int Rb = warp; Rb < Rp; Rb += 4 * nwarps) {
-            double v[NB][8];
+        for (int Rb = warp; Rb < Rp; Rb += G * nwarps) {
+            double v[NB][2 * G];
 #pragma unroll
             for (int c = 0; c < NB; ++c) {
                 const int* inv = a.inv + c * kInvRows;
@@ -45,7 +48,7 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
 #pragma unroll
                 for (int cp = 0; cp < 2; ++cp) { const int C = lane + 32 * cp; ic[cp] = C < p ? inv[C] : -1; }
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < G; ++g) {
                     const int R = Rb + g * nwarps;
                     const int ir = R < Rp ? inv[R] : -1;
                     const int irc = ir > 0 ? ir : 0;
@@ -56,7 +59,7 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
                 }
             }
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 0; g < G; ++g) {
                 const int R = Rb + g * nwarps;
 #pragma unroll
                 for (int cp = 0; cp < 2; ++cp) {
@@ -75,8 +78,8 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
     if (!a.direct) {
         const int irow0 = rp, jrow0 = a.diag ? rp : rp + round8(ni);   // index of tile row / column 0 in inv
         for (int Cb = 0; Cb < nj; Cb += 64) {
-            for (int Rb = warp; Rb < ni; Rb += 4 * nwarps) {
-                double v[NB][8];
+            for (int Rb = warp; Rb < ni; Rb += G * nwarps) {
+                double v[NB][2 * G];
 #pragma unroll
                 for (int c = 0; c < NB; ++c) {
                     const int* inv = a.inv + c * kInvRows;
@@ -84,7 +87,7 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
 #pragma unroll
                     for (int cp = 0; cp < 2; ++cp) { const int C = Cb + lane + 32 * cp; ic[cp] = C < nj ? inv[jrow0 + C] : -1; }
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
+                    for (int g = 0; g < G; ++g) {
                         const int R = Rb + g * nwarps;
                         const int ir = R < ni ? inv[irow0 + R] : -1;
                         const int irc = ir > 0 ? ir : 0;
@@ -95,7 +98,7 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
                     }
                 }
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < G; ++g) {
                     const int R = Rb + g * nwarps;
 #pragma unroll
                     for (int cp = 0; cp < 2; ++cp) {
@@ -145,6 +148,8 @@ __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec*
 // Dependency hooks of a front task.  The level-launch kernels run a whole tree level per launch,
 // so their hooks are empty; the persistent kernel spins on completion counters here.
 struct NoWait {
+    __device__ __forceinline__ void factor(const BwdTask&) const {}
+    __device__ __forceinline__ void parent(const BwdTask&) const {}
     __device__ __forceinline__ void originals(const TaskRec&) const {}
     __device__ __forceinline__ void children(const TaskRec&, const ChildRec*) const {}
     __device__ __forceinline__ void panels(const TaskRec&) const {}
@@ -264,10 +269,10 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         GatherArgs ga{pan, tile, &s_inv[0][0], ubuf, pp, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
         const ChildRec* cb = crec + cbase;
         switch (nb) {
-            case 1: gather_batch<1>(ga, cb); break;
-            case 2: gather_batch<2>(ga, cb); break;
-            case 3: gather_batch<3>(ga, cb); break;
-            default: gather_batch<4>(ga, cb); break;
+            case 1: gather_batch<1, 8>(ga, cb); break;
+            case 2: gather_batch<2, 4>(ga, cb); break;
+            case 3: gather_batch<3, 4>(ga, cb); break;
+            default: gather_batch<4, 4>(ga, cb); break;
         }
     }
     __syncthreads();
@@ -503,8 +508,12 @@ struct __align__(16) BwdScratch {
 
 // One backward task, executed by the first 128 threads of the CTA (all threads must call it).
 // Returns true in the CTA that solved the front's pivots (the last split to finish).
+// wait.factor() precedes the first read of the front's own factor, wait.parent() the first read of
+// the solution of its ancestors: everything that only needs the factor (the pivot block, this
+// split's slice of L21, the row indices) is fetched BEFORE waiting for the parent.
+template <class Wait>
 __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, const FrontTab& ft, const double* lbuf,
-                                              double* xsol, double* bpart, int32_t* bcnt) {
+                                              double* xsol, double* bpart, int32_t* bcnt, const Wait& wait) {
     double* l11 = B.l11;
     double (*half)[64] = B.half;
     double* xs = B.xs;
@@ -516,6 +525,7 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
     const int32_t* rows = ft.rows + tk.rows_off;
     const int tid = threadIdx.x, k = tid & 63, h = tid >> 6;
     const int lo = tk.split * kBwdRows, n = min(kBwdRows, u - lo);
+    wait.factor(tk);
     // L11 is needed only by the CTA that finishes last; every CTA prefetches it asynchronously so
     // the copy overlaps the matrix-vector part instead of following the atomic hand-off
     // (l_off is even, so 16-byte cp.async.cg -- L2-coherent -- covers the block pairwise)
@@ -528,16 +538,20 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
         if ((p & 1) && tid == 0) l11[p * p - 1] = ldc(L + p * p - 1);
     }
     const double yk = (tid < p) ? ldc(L + (size_t)(p + u) * p + tid) : 0.0;
-    if (tid < kBwdRows) xs[tid] = tid < n ? ldc(xsol + rows[p + lo + tid]) : 0.0;
+    const int xrow = (tid < kBwdRows && tid < n) ? rows[p + lo + tid] : -1;
+    const int a = (h & 1) * (kBwdRows / 2), b = min(n, a + kBwdRows / 2);
+    double v[kBwdRows / 2];
+    {
+        const double* col = L + (size_t)(p + lo) * p + k;
+#pragma unroll
+        for (int i = 0; i < kBwdRows / 2; ++i) v[i] = (k < p && tid < 128 && a + i < b) ? ldc(col + (size_t)(a + i) * p) : 0.0;
+    }
+    wait.parent(tk);
+    if (tid < kBwdRows) xs[tid] = xrow >= 0 ? ldc(xsol + xrow) : 0.0;
     __syncthreads();
     {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         if (k < p && tid < 128) {
-            const double* col = L + (size_t)(p + lo) * p + k;
-            const int a = h * (kBwdRows / 2), b = min(n, a + kBwdRows / 2);
-            double v[kBwdRows / 2];
-#pragma unroll
-            for (int i = 0; i < kBwdRows / 2; ++i) v[i] = (a + i < b) ? ldc(col + (size_t)(a + i) * p) : 0.0;
 #pragma unroll
             for (int i = 0; i < kBwdRows / 2; i += 4) {
                 s0 = fma(v[i], xs[min(a + i, kBwdRows - 1)], s0);

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128) backward_kernel(FrontTab ft, const BwdTas
                                                        double* xsol, double* bpart, int32_t* bcnt) {
     __shared__ BwdScratch B;
     const BwdTask tk = tasks[blockIdx.x];
-    backward_body(B, tk, ft, lbuf, xsol, bpart, bcnt);
+    backward_body(B, tk, ft, lbuf, xsol, bpart, bcnt, NoWait{});
 }
 
 void launch_backward(const FrontTab& ft, const BwdTask* tasks, int ntasks, const double* lbuf,

@@ -55,6 +55,16 @@ struct SpinWait {
     unsigned acc_target;
     unsigned long long* tr;  // trace slots of this item (debug) or nullptr
     int n_fronts;
+    // backward tasks: own factor complete (all its panel-storing tasks), then the nearest ancestor solved
+    __device__ __forceinline__ void factor(const BwdTask& tk) const {
+        if (threadIdx.x == 0) wait_ge(ctr + CTR_FRONT0 + n_fronts + tk.front, (unsigned)tk.need * epoch);
+        __syncthreads();
+    }
+    __device__ __forceinline__ void parent(const BwdTask& tk) const {
+        if (tk.dep < 0) return;
+        if (threadIdx.x == 0) { wait_ge(ctr + CTR_FRONT0 + 2 * n_fronts + tk.dep, epoch); if (tr) tr[2] = globaltimer(); }
+        __syncthreads();
+    }
     __device__ __forceinline__ void originals(const TaskRec& hdr) const {
         if (!(hdr.flags & 2)) return;
         if (threadIdx.x == 0) { wait_ge(ctr + CTR_ACC, acc_target); if (tr) tr[1] = globaltimer(); }
@@ -172,13 +182,8 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
         } else if (loc < o_upd) {
             // ---- backward substitution task ---------------------------------------------------------
             const BwdTask tk = sp.btasks[loc - o_bwd];
-            if (tid == 0) {
-                wait_ge(pdone + tk.front, (unsigned)tk.need * epoch);
-                if (tk.dep >= 0) wait_ge(bdone + tk.dep, epoch);
-            }
-            __syncthreads();
-            if (tr && tid == 0) tr[2] = globaltimer();
-            const bool solved = backward_body(*reinterpret_cast<BwdScratch*>(sm), tk, ft, sp.lbuf, sp.xsol, sp.bpart, sp.bcnt);
+            const SpinWait w{ctr, epoch, 0u, tr, sp.n_fronts};
+            const bool solved = backward_body(*reinterpret_cast<BwdScratch*>(sm), tk, ft, sp.lbuf, sp.xsol, sp.bpart, sp.bcnt, w);
             if (solved && tid == 0) {
                 __threadfence();
                 atomicAdd(bdone + tk.front, 1u);
