@@ -289,7 +289,7 @@ def run_gpu(args):
         "time_to_converge_ms": {"warm_device": tot_dev / args.steps * 1e3, "warm_e2e": tot_e2e / args.steps * 1e3,
                                 "plan_build_s": plan_s},
         "objective": rep.objective,
-        "e2e": {"value": e2e_value, "unit": "GN iterations/s", "h2d_bytes_per_step": 16 * m + 16 * nb,
+        "e2e": {"value": e2e_value, "unit": "GN iterations/s", "h2d_bytes_per_step": 16 * m,
                 "d2h_bytes_per_step": 16 * nb + 16 * it_per_solve},
         "gpu_launches": int(est.launches_per_solve * args.steps * 2),
         "clocks": clocks.summary(),

@@ -56,7 +56,7 @@ struct gse_plan {
     // evaluation units
     DevBuf<int32_t> vm_bus, vm_row, vm_slot, fl_branch, fl_from, fl_to, fl_row, fl_slot;
     DevBuf<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq, inj_nth;
-    DevBuf<double> val;                       // [g | w*g | w*r]: template partials per slot, weighted residual per row
+    DevBuf<double> val;                       // [(g, w*g) per slot | w*r per row]: template partials, weighted residuals
     // accumulation programs
     DevBuf<int32_t> acc_ptr, acc_items, acc_uniq, racc_ptr, racc_a, racc_b;
     DevBuf<uint32_t> acc_pair;
@@ -77,6 +77,8 @@ struct gse_plan {
     DevBuf<int32_t> upd_bus, upd_quant, upd_pos;
     DevBuf<double> obj_partial, status;       // status: [delta bits as double slot, err as double] (MAX-reducible)
     DevBuf<unsigned long long> flags;         // [0] delta_inf bits, [1] failure code (min)
+    double* h_stage[2] = {nullptr, nullptr};  // pinned staging of new z / w
+    cudaEvent_t stage_done[2] = {nullptr, nullptr};
     unsigned long long* h_flags = nullptr;    // pinned
     double* h_obj = nullptr;                  // pinned
     std::vector<LevelLaunch> fwd;
@@ -206,6 +208,7 @@ gse_plan::~gse_plan() {
     if (h_flags) cudaFreeHost(h_flags);
     if (h_obj) cudaFreeHost(h_obj);
     if (h_blk) cudaFreeHost(h_blk);
+    for (int i = 0; i < 2; ++i) { if (h_stage[i]) cudaFreeHost(h_stage[i]); if (stage_done[i]) cudaEventDestroy(stage_done[i]); }
     syncblk.release(); trace.release();
     DevBuf<int32_t>* ib[] = {&y_ptr, &y_idx, &br_from, &br_to, &m_type, &m_target, &vm_bus, &vm_row, &vm_slot, &fl_branch,
                              &fl_from, &fl_to, &fl_row, &fl_slot, &inj_bus, &inj_rowp, &inj_rowq, &inj_slotp, &inj_slotq, &inj_nth,
@@ -255,6 +258,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     if (const char* e = getenv("GSE_GAMMA_LEAF")) { int v = atoi(e); if (v >= 1) bo.gamma_leaf_buses = v; }
     if (const char* e = getenv("GSE_MAX_PIVOTS")) { int v = atoi(e); if (v == 32 || v == 64) bo.max_pivots = v; }
     if (const char* e = getenv("GSE_LEAF_BUSES")) { int v = atoi(e); if (v >= 1) bo.leaf_buses = v; }
+    if (const char* e = getenv("GSE_SEPW")) bo.sep_weight = atof(e);
+    if (const char* e = getenv("GSE_GAMMA_SEPW")) bo.gamma_sep_weight = atof(e);
     if (const char* e = getenv("GSE_SPLIT_MIN")) { int v = atoi(e); if (v >= 1) bo.split_min_pivots = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;
@@ -304,7 +309,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     ep.fl_row = plan->fl_row.ptr; ep.fl_slot = plan->fl_slot.ptr;
     ep.inj_bus = plan->inj_bus.ptr; ep.inj_rowp = plan->inj_rowp.ptr; ep.inj_rowq = plan->inj_rowq.ptr;
     ep.inj_slotp = plan->inj_slotp.ptr; ep.inj_slotq = plan->inj_slotq.ptr; ep.inj_nth = plan->inj_nth.ptr;
-    ep.g = plan->val.ptr; ep.gw = plan->val.ptr + hp.n_slots; ep.wr = plan->val.ptr + 2 * hp.n_slots;
+    ep.g = plan->val.ptr; ep.wr = plan->val.ptr + 2 * hp.n_slots;
 
     // ---- front tables ----
     const size_t nf = hp.fronts.size();
@@ -495,16 +500,26 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
 
 void gse_plan_destroy(gse_plan* plan) { delete plan; }
 
-int gse_set_weights(gse_plan* plan, const double* w) {
+// New weights / values on the same rows: staged through plan-owned pinned memory and copied on the
+// plan's stream, so the call returns without waiting for the device and the next solve (same stream)
+// sees the data.  which: 0 = z, 1 = w.
+static int stage_rows(gse_plan* plan, int which, const double* src, double* dst_dev) {
     CU(cudaSetDevice(plan->device));
-    CU(cudaMemcpy(plan->w.ptr, w, sizeof(double) * plan->hp.n_rows, cudaMemcpyHostToDevice));
+    const size_t bytes = sizeof(double) * plan->hp.n_rows;
+    if (bytes == 0) return GSE_OK;
+    if (!plan->h_stage[which]) {
+        CU(cudaMallocHost(&plan->h_stage[which], bytes));
+        CU(cudaEventCreateWithFlags(&plan->stage_done[which], cudaEventDisableTiming));
+    } else {
+        CU(cudaEventSynchronize(plan->stage_done[which]));      // the previous copy out of this buffer
+    }
+    memcpy(plan->h_stage[which], src, bytes);
+    CU(cudaMemcpyAsync(dst_dev, plan->h_stage[which], bytes, cudaMemcpyHostToDevice, plan->stream));
+    CU(cudaEventRecord(plan->stage_done[which], plan->stream));
     return GSE_OK;
 }
-int gse_set_measurements(gse_plan* plan, const double* z) {
-    CU(cudaSetDevice(plan->device));
-    CU(cudaMemcpy(plan->z.ptr, z, sizeof(double) * plan->hp.n_rows, cudaMemcpyHostToDevice));
-    return GSE_OK;
-}
+int gse_set_weights(gse_plan* plan, const double* w) { return stage_rows(plan, 1, w, plan->w.ptr); }
+int gse_set_measurements(gse_plan* plan, const double* z) { return stage_rows(plan, 0, z, plan->z.ptr); }
 
 int gse_check(gse_plan* plan) {
     CU(cudaSetDevice(plan->device));

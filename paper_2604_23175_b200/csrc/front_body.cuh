@@ -280,7 +280,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
 
     // ---- blocked panel factorisation (block = 8 columns) ---------------------------------------
     // Per block: warp 0 brings the 8x8 diagonal tile up to date (rank-8 share of the previous block
-    // column; see diag_rank8), factors it in registers and publishes it while the other warps
+    // column; see diag_rank8), eliminates it across its lanes and publishes it while the other warps
     // update the remaining row tiles on the tensor pipe (left-looking, look-ahead); then every row
     // solves against the published block (independent FMAs).  Two barriers per 8 pivots.
     if (HAS_PIVOTS && pp) {
@@ -291,46 +291,66 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         for (int kb = 0; kb < rp; kb += 8) {
             const int t0 = kb >> 3;
             if (warp == 0) {
-                if (kb) { diag_rank8(pan, ld, t0, kb - 8, lane); __syncwarp(); }   // the last block column's share
+                // The 8x8 diagonal block lives in the MMA accumulator layout: lane (r = lane / 4, c = lane % 4)
+                // holds D[r][2c], D[r][2c + 1].  It is loaded with one 16-byte read, takes the last block
+                // column's share straight in registers, and is eliminated by all 32 lanes together.
+                const int r = lane >> 2, c2 = 2 * (lane & 3);
+                const double2 dt = *reinterpret_cast<const double2*>(pan + (size_t)(kb + r) * ld + kb + c2);
+                double x0 = dt.x, x1 = dt.y;
+                if (kb) {
+                    const double* ap = pan + (size_t)(kb + r) * ld + (kb - 8) + (lane & 3);
+                    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+                    dmma_m8n8k4(c0, c1, ap[0], ap[0]);
+                    dmma_m8n8k4(e0, e1, ap[4], ap[4]);
+                    x0 -= c0 + e0; x1 -= c1 + e1;
+                }
                 GSE_PC(0);
-                double d[36];   // lower triangle, row-major: d[i*(i+1)/2 + j]
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j <= i; ++j) d[i * (i + 1) / 2 + j] = pan[(kb + i) * ld + kb + j];
                 GSE_PC(1);
-                double rinv[8];
+                // Division-free elimination: step k cross-multiplies
+                //     a_ij <- (p_k a_ij - a_ik a_jk) * 2^-e,   p_k = a_kk,   2^e ~ p_k  (exact scaling),
+                // one multiply-add per lane, so the serial chain per pivot is shuffle -> multiply -> FMA
+                // instead of a reciprocal square root.  Stage-k entries equal c_k times the true Schur
+                // complement, c_{k+1} = c_k p_k 2^-e in [1, 2^k); hence L_ik = a_ik / sqrt(p_k c_k) and
+                // 1 / L_kk = c_k / sqrt(p_k c_k): the eight reciprocal square roots are independent and
+                // run after the chain, one per lane.
                 int badk = -1;
+                double cs = 1.0, mine = 1.0, myc = 1.0;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const double dk = d[k * (k + 1) / 2 + k];
-                    if (!(dk > 0.0) && badk < 0) badk = k;
-                    const double r = rsqrt(dk);
-                    rinv[k] = r;
-                    d[k * (k + 1) / 2 + k] = dk * r;
-#pragma unroll
-                    for (int i = k + 1; i < 8; ++i) d[i * (i + 1) / 2 + k] *= r;
-#pragma unroll
-                    for (int j = k + 1; j < 8; ++j)
-#pragma unroll
-                        for (int i = j; i < 8; ++i)
-                            d[i * (i + 1) / 2 + j] = fma(-d[i * (i + 1) / 2 + k], d[j * (j + 1) / 2 + k], d[i * (i + 1) / 2 + j]);
+                    const double src = (k & 1) ? x1 : x0;                                   // column k lives in lanes (*, k / 2)
+                    const double pv = __shfl_sync(0xffffffffu, src, 4 * k + (k >> 1));        // a_kk
+                    const double aik = __shfl_sync(0xffffffffu, src, (lane & ~3) | (k >> 1)); // a_rk
+                    const double aj0 = __shfl_sync(0xffffffffu, src, 4 * c2 + (k >> 1));      // a_{2c,k}
+                    const double aj1 = __shfl_sync(0xffffffffu, src, 4 * (c2 + 1) + (k >> 1));
+                    badk = (!(pv > 0.0) && badk < 0) ? k : badk;
+                    const bool own = (lane & 7) == k;
+                    mine = own ? pv * cs : mine;
+                    myc = own ? cs : myc;
+                    // exact power-of-two scaling through the exponent field (no floating-point latency):
+                    // ps = p_k 2^-e in [1, 2); the cross product a_ik a_jk is scaled the same way
+                    const int de = (((__double2hiint(pv) >> 20) & 0x7ff) - 1023) * 1048576;
+                    const double ps = __hiloint2double(__double2hiint(pv) - de, __double2loint(pv));
+                    cs *= ps;
+                    const double u0 = aik * aj0, u1 = aik * aj1;
+                    // (a product whose exponent would underflow under the scaling is flushed to zero: it is
+                    // below 2^-1022 relative to the pivot)
+                    const int h0 = __double2hiint(u0), h1 = __double2hiint(u1);
+                    const double s0 = ((h0 & 0x7ff00000) > de) ? __hiloint2double(h0 - de, __double2loint(u0)) : 0.0;
+                    const double s1 = ((h1 & 0x7ff00000) > de) ? __hiloint2double(h1 - de, __double2loint(u1)) : 0.0;
+                    const double n0 = fma(ps, x0, -s0), n1 = fma(ps, x1, -s1);
+                    x0 = (r > k && c2 > k) ? n0 : x0;
+                    x1 = (r > k && c2 + 1 > k) ? n1 : x1;
                 }
+                const double q = rsqrt(mine);                  // lane l: 1 / sqrt(p_k c_k) of pivot k = l % 8
+                const double rk = myc * q;                     // 1 / L_kk
+                x0 *= __shfl_sync(0xffffffffu, q, c2);
+                x1 *= __shfl_sync(0xffffffffu, q, c2 + 1);
                 GSE_PC(2);
-                // publish: every lane holds the same values; lane l writes entries l and l + 32
-                {
-                    if (lane == 0) {
-                        double2* o2 = reinterpret_cast<double2*>(s_ld);
-#pragma unroll
-                        for (int i = 0; i < 18; ++i) o2[i] = make_double2(d[2 * i], d[2 * i + 1]);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) o2[18 + k] = make_double2(rinv[2 * k], rinv[2 * k + 1]);
-                        double2* r2 = reinterpret_cast<double2*>(s_rinv + kb);     // (padded pivots: reciprocal 1)
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) r2[k] = make_double2(rinv[2 * k], rinv[2 * k + 1]);
-                        if (badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
-                    }
-                }
+                // publish the factor of the block (packed lower triangle) and the reciprocal pivots
+                if (c2 <= r) s_ld[r * (r + 1) / 2 + c2] = x0;
+                if (c2 + 1 <= r) s_ld[r * (r + 1) / 2 + c2 + 1] = x1;
+                if (lane < 8) { s_ld[36 + lane] = rk; s_rinv[kb + lane] = rk; }      // (padded pivots: reciprocal 1)
+                if (lane == 0 && badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
             } else if (kb) {
                 // later pivot tiles: their diagonal blocks take the last block column's share now
                 const int nw = nwarps - 1;

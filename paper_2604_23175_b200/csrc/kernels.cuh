@@ -16,9 +16,9 @@ struct EvalProg {
     const int32_t *vm_bus, *vm_row, *vm_slot;
     const int32_t *fl_branch, *fl_from, *fl_to, *fl_row, *fl_slot;
     const int32_t *inj_bus, *inj_rowp, *inj_rowq, *inj_slotp, *inj_slotq, *inj_nth;
-    // outputs = the unified value array val = [g | gw | wr]: per slot the partial and weight * partial,
-    // per measurement row weight * residual
-    double *g, *gw, *wr;
+    // outputs = the unified value array val = [(g, w*g) per slot, interleaved | wr]: per slot the partial
+    // and weight * partial, per measurement row weight * residual
+    double *g, *wr;
 };
 
 // One (front, row-chunk, col-chunk) task: everything the CTA needs, read with one coalesced load.

@@ -118,6 +118,9 @@ struct BuildOptions {
     int max_pivots = 64;
     int boundary_mode = 0;     // 0 auto (tree when n_Gamma > 192), 1 dense chain, 2 tree
     int gamma_leaf_buses = 16; // nested-dissection leaf of the boundary tree, in boundary buses
+    // nested dissection picks the BFS level minimising |left - right| + w * |separator|: a larger w trades
+    // balance for shorter chains of sequential pivots (the solve is latency-bound on that chain)
+    double sep_weight = 2.0, gamma_sep_weight = 2.0;
     // fronts with several row chunks and at least this many pivots run as panel + update tasks.  Measured on the
     // PEGASE-9241 shape (tools/gpu_sweep2.sh): the panel is bound by its serial 8x8 chain, not by its row count,
     // so the split only adds a hand-off (2.06 ms vs 2.03 ms per solve) -- off by default, kept for wide fronts.

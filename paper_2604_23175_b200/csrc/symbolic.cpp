@@ -50,6 +50,7 @@ struct NDGraph {
     std::vector<int> xadj, adj;
     std::vector<int> stamp, level;
     int cur = 0;
+    double sep_weight = 2.0;   // level-set choice: |left - right| + sep_weight * |separator|
 };
 
 void nd_recurse(NDGraph& g, std::vector<int>& verts, int leaf, std::vector<std::vector<int>>& out) {
@@ -131,7 +132,7 @@ void nd_recurse(NDGraph& g, std::vector<int>& verts, int leaf, std::vector<std::
     int best_j = 1; double best_cost = 1e300; int below = cnt[0];
     for (int j = 1; j <= depth - 1; ++j) {
         int above = n - below - cnt[j];
-        double cost = std::abs(below - above) + 2.0 * cnt[j];
+        double cost = std::abs(below - above) + g.sep_weight * cnt[j];
         if (cost < best_cost) { best_cost = cost; best_j = j; }
         below += cnt[j];
     }
@@ -302,6 +303,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         for (size_t i = 0; i < edges.size(); ++i) { g.xadj[edges[i] / nn + 1]++; g.adj[i] = (int)(edges[i] % nn); }
         for (int i = 0; i < nn; ++i) g.xadj[i + 1] += g.xadj[i];
         g.stamp.assign(nn, 0); g.level.assign(nn, 0);
+        g.sep_weight = opt.gamma_sep_weight;
         std::vector<int> all(nn); std::iota(all.begin(), all.end(), 0);
         std::vector<std::vector<int>> nodes;
         nd_recurse(g, all, std::max(1, opt.gamma_leaf_buses), nodes);
@@ -478,6 +480,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             for (size_t i = 0; i < edges.size(); ++i) { g.xadj[edges[i] / nib + 1]++; g.adj[i] = (int)(edges[i] % nib); }
             for (int i = 0; i < nib; ++i) g.xadj[i + 1] += g.xadj[i];
             g.stamp.assign(nib, 0); g.level.assign(nib, 0);
+            g.sep_weight = opt.sep_weight;
             std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
             nd_recurse(g, all, std::max(1, opt.leaf_buses), nodes);
         }
@@ -878,11 +881,11 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     lap("offsets, levels, tasks");
     // ---- solver-layout accumulation program ---------------------------------------------
     // Every contribution is a product val[a] * val[b] of the unified value array
-    // val = [g (n_slots) | w*g (n_slots) | w*r (n_rows)]: a indexes g, b indexes w*g (matrix
+    // val = [(g, w*g) per slot, interleaved | w*r (n_rows)]: a indexes g, b indexes w*g (matrix
     // entries) or w*r of the row (right-hand sides, collected above as -(row + 1)).
     hp.n_val = 2 * hp.n_slots + m;
     if (hp.n_val > 2147483647LL) return "value array exceeds int32 indexing";
-    auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(hp.n_slots + b) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
+    auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(2 * b + 1) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
     {
         std::vector<int64_t> dest; std::vector<int32_t> pa, pb;
         for (int a = 0; a < K; ++a) {
@@ -920,7 +923,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         for (int64_t i = 0; i < hp.n_gval; ++i) hp.acc_ptr[i + 1] += hp.acc_ptr[i];
         hp.acc_a.resize(dest.size()); hp.acc_b.resize(dest.size());
         std::vector<int32_t> cur(hp.acc_ptr.begin(), hp.acc_ptr.end() - 1);
-        for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = pa[i]; hp.acc_b[q] = val_index(pb[i]); }
+        for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = 2 * pa[i]; hp.acc_b[q] = val_index(pb[i]); }
     }
     lap("accumulation program (sort)");
     build_acc_items(hp);
@@ -982,13 +985,13 @@ void build_reference_program(HostProgram& hp) {
             }
         }
     }
-    auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(hp.n_slots + b) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
+    auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(2 * b + 1) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
     hp.racc_ptr.assign(hp.n_ref_vals + 1, 0);
     for (int64_t dd : rdest) hp.racc_ptr[dd + 1]++;
     for (int64_t i = 0; i < hp.n_ref_vals; ++i) hp.racc_ptr[i + 1] += hp.racc_ptr[i];
     hp.racc_a.resize(rdest.size()); hp.racc_b.resize(rdest.size());
     std::vector<int32_t> cur(hp.racc_ptr.begin(), hp.racc_ptr.end() - 1);
-    for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = ra[i]; hp.racc_b[q] = val_index(rb[i]); }
+    for (size_t i = 0; i < rdest.size(); ++i) { int32_t q = cur[rdest[i]]++; hp.racc_a[q] = 2 * ra[i]; hp.racc_b[q] = val_index(rb[i]); }
 }
 
 }  // namespace gse

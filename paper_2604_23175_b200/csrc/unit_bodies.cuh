@@ -13,8 +13,7 @@ namespace gse {
 __device__ __forceinline__ double ldc(const double* p) { return __ldcg(p); }
 
 __device__ __forceinline__ void put_slot(const EvalProg& ep, int s, double gv, double w) {
-    ep.g[s] = gv;
-    ep.gw[s] = w * gv;
+    reinterpret_cast<double2*>(ep.g)[s] = make_double2(gv, w * gv);      // (g, w*g) interleaved: one 16-byte store
 }
 
 __device__ __forceinline__ void flow_row(const EvalProg& ep, int row, int slot, bool f_slack,

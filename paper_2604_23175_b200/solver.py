@@ -126,13 +126,15 @@ class MultiAreaEstimator:
         self._flat = np.stack([StateVector.flat_start(net).va, np.ones(net.n_bus)])
         self._host = torch.empty((2, net.n_bus), dtype=torch.float64).pin_memory()
         self._state = torch.empty((2, net.n_bus), dtype=torch.float64, device=self.device)
+        self._flat_dev = torch.from_numpy(self._flat).to(self.device)      # the flat start is a constant of the plan
         self.setup_s = time.perf_counter() - t0
 
     # -- inputs ----------------------------------------------------------------------
     def update_measurements(self, ms: MeasurementSet):
         """New values / masks on the same rows: refresh z and w, no re-analysis."""
-        if ms.m != self.ms.m or not (np.array_equal(ms.mtype, self.ms.mtype)
-                                     and np.array_equal(ms.target, self.ms.target)):
+        same_rows = ms.m == self.ms.m and all(
+            a is b or np.array_equal(a, b) for a, b in ((ms.mtype, self.ms.mtype), (ms.target, self.ms.target)))
+        if not same_rows:
             raise ValueError("measurement rows differ from the analysed template set")
         self.plan.set_measurements(ms.z)
         self.plan.set_weights(ms.weight)
@@ -142,8 +144,7 @@ class MultiAreaEstimator:
         return self._state[0].data_ptr(), self._state[1].data_ptr()
 
     def _load_flat_start(self):
-        self._host.copy_(self.torch.from_numpy(self._flat))
-        self._state.copy_(self._host, non_blocking=True)
+        self._state.copy_(self._flat_dev, non_blocking=True)
 
     def _read_state(self):
         self._host.copy_(self._state)

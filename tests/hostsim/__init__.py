@@ -46,9 +46,9 @@ class HostSim:
         self.net, self.maps, self.n_gamma = net, maps, bord.n_gamma
 
     def stats(self):
-        out = np.zeros(10)
+        out = np.zeros(12)
         _lib().hostsim_stats(self.h, out.ctypes.data_as(C.POINTER(C.c_double)))
-        keys = ("fronts", "levels", "max_front", "lbuf", "ubuf", "pairs", "gval", "flops", "tasks", "bwd_levels")
+        keys = ("fronts", "levels", "max_front", "lbuf", "ubuf", "pairs", "gval", "flops", "tasks", "bwd_levels", "chain_pivots", "boundary_chain_pivots")
         return dict(zip(keys, out))
 
     def iterate(self, va, vm):

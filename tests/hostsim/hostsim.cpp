@@ -8,6 +8,7 @@
 // csrc/kernels.cu step for step.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -21,13 +22,13 @@ namespace {
 struct Sim {
     HostProgram hp;
     gse_problem_desc d;
-    std::vector<double> val, gval, lbuf, ubuf, xsol, w;   // val = [g | w*g | w*r]
+    std::vector<double> val, gval, lbuf, ubuf, xsol, w;   // val = [(g, w*g) per slot | w*r]
     long long fail_code = -1;
 };
 
 inline int pad_ld(int p) { return ((p + 11) / 16) * 16 + 4; }
 
-void put(Sim& s, int slot, double gv, double w, double) { s.val[slot] = gv; s.val[s.hp.n_slots + slot] = w * gv; }
+void put(Sim& s, int slot, double gv, double w, double) { s.val[2 * slot] = gv; s.val[2 * slot + 1] = w * gv; }
 void put_wr(Sim& s, int row, double wr) { if (row >= 0) s.val[2 * s.hp.n_slots + row] = wr; }
 
 void flow_row(Sim& s, int row, int slot, bool fs, bool ts, double h, double a, double b, double c, double e) {
@@ -174,6 +175,10 @@ void* hostsim_create(const gse_problem_desc* d, int dense, int leaf, int pmax, i
     Sim* s = new Sim(); s->d = *d;
     BuildOptions bo; bo.dense = dense != 0; if (leaf > 0) bo.leaf_buses = leaf; if (pmax == 32 || pmax == 64) bo.max_pivots = pmax;
     bo.rank = rank; bo.world = std::max(1, world); bo.boundary_mode = boundary_mode;
+    if (const char* e = getenv("GSE_SEPW")) bo.sep_weight = atof(e);
+    if (const char* e = getenv("GSE_GAMMA_SEPW")) bo.gamma_sep_weight = atof(e);
+    if (const char* e = getenv("GSE_GAMMA_LEAF")) bo.gamma_leaf_buses = atoi(e);
+    if (const char* e = getenv("GSE_LEAF_BUSES")) bo.leaf_buses = atoi(e);
     if (area_rank) bo.area_rank.assign(area_rank, area_rank + d->n_areas);
     std::string e = build_host_program(*d, bo, s->hp);
     if (!e.empty()) { snprintf(msg, msglen, "%s", e.c_str()); delete s; return nullptr; }
@@ -187,7 +192,19 @@ void hostsim_destroy(void* h) { delete (Sim*)h; }
 void hostsim_stats(void* h, double* out) { Sim* s = (Sim*)h; const HostProgram& hp = s->hp;
     out[0] = (double)hp.fronts.size(); out[1] = (double)hp.fwd_levels.size(); out[2] = hp.max_front; out[3] = (double)hp.n_lbuf;
     out[4] = (double)hp.n_ubuf; out[5] = (double)hp.n_pairs; out[6] = (double)hp.n_gval; out[7] = hp.dense_flops;
-    size_t nt = 0; for (auto& l : hp.fwd_levels) nt += l.size(); out[8] = (double)nt; out[9] = (double)hp.bwd_levels.size(); }
+    size_t nt = 0; for (auto& l : hp.fwd_levels) nt += l.size(); out[8] = (double)nt; out[9] = (double)hp.bwd_levels.size();
+    // sequential pivots on the longest leaf-to-root chain (total, and inside the boundary fronts)
+    std::vector<double> path(hp.fronts.size(), 0.0), gpath(hp.fronts.size(), 0.0);
+    double best = 0, gbest = 0;
+    for (size_t f = 0; f < hp.fronts.size(); ++f) {     // children precede parents in front order? not guaranteed: iterate by level
+    }
+    std::vector<int> order(hp.fronts.size()); for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return hp.fronts[a].level < hp.fronts[b].level; });
+    for (int f : order) { const Front& fr = hp.fronts[f];
+        double c = 0, gc = 0; for (int ch : fr.children) { c = std::max(c, path[ch]); gc = std::max(gc, gpath[ch]); }
+        path[f] = c + fr.p; gpath[f] = gc + (fr.kind == 3 ? fr.p : 0);
+        best = std::max(best, path[f]); gbest = std::max(gbest, gpath[f]); }
+    out[10] = best; out[11] = gbest; }
 // one outer iteration; returns failure code or -1
 long long hostsim_iterate(void* h, double* va, double* vm, double* delta_inf) {
     Sim* s = (Sim*)h; const HostProgram& hp = s->hp; s->fail_code = -1;
