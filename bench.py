@@ -170,6 +170,8 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     net, ms, part = build_workload(args.workload)
+    torch.zeros(1, device=dev)                       # CUDA context creation is not part of the plan build
+    torch.cuda.synchronize(dev)
 
     t0 = time.perf_counter()
     if world > 1:
