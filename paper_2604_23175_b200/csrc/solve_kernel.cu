@@ -36,7 +36,19 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 // barrier, which costs no issue slots); the back-off keeps a waiting CTA from stealing load/store
 // bandwidth from the CTA it shares the SM with -- often the very producer it is waiting for.
 __device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target) {
-    while (ld_acquire(p) < target) __nanosleep(40);
+    unsigned polls = 0;
+    unsigned long long t0 = 0;
+    while (ld_acquire(p) < target) {
+        __nanosleep(40);
+        // watchdog: a dependency that never completes would hang the device; after ~10 s of waiting
+        // the kernel aborts instead (the launch then fails with an error the host reports)
+        if ((++polls & 0xffffu) == 0) {
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 10000000000ull) __trap();
+        }
+    }
 }
 // called by one thread after a CTA barrier that follows the item's last global write
 __device__ __forceinline__ void signal(unsigned* p) {
