@@ -102,6 +102,7 @@ def lib():
     L.gse_solve.argtypes = [vp, C.POINTER(Config), vp, vp, C.POINTER(Report)]
     L.gse_iterate.argtypes = [vp, vp, vp, f64p]
     L.gse_inner_step.argtypes = [vp, vp, vp, f64p]
+    L.gse_set_rows_pinned.argtypes = [vp, vp, vp]
     L.gse_matrix_plan_create.argtypes = [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, C.POINTER(Options), C.POINTER(vp)]
     L.gse_matrix_set_values.argtypes = [vp, f64p, f64p, f64p, f64p, f64p]
     L.gse_matrix_condense.argtypes = [vp]
@@ -136,7 +137,7 @@ def lib():
 
 EXPORTED = [
     "gse_plan_create", "gse_plan_destroy", "gse_last_error", "gse_set_weights",
-    "gse_set_measurements", "gse_solve", "gse_iterate", "gse_inner_step", "gse_phase_assemble",
+    "gse_set_measurements", "gse_set_rows_pinned", "gse_solve", "gse_iterate", "gse_inner_step", "gse_phase_assemble",
     "gse_phase_condense", "gse_phase_boundary", "gse_phase_recover", "gse_check", "gse_objective",
     "gse_area_dims", "gse_area_pattern", "gse_area_blocks", "gse_area_schur", "gse_area_delta",
     "gse_boundary_system", "gse_set_boundary_delta", "gse_exchange_buffer_dev",
@@ -270,6 +271,10 @@ class Plan:
         w = np.ascontiguousarray(w, dtype=np.float64)
         assert w.shape == (self.n_rows,)
         self._call(lib().gse_set_weights(self._h, _fp(w)))
+
+    def set_rows_pinned(self, z_ptr, w_ptr):
+        """Async refresh from pinned host memory (raw addresses, 0 = skip)."""
+        self._call(lib().gse_set_rows_pinned(self._h, C.c_void_p(z_ptr or None), C.c_void_p(w_ptr or None)))
 
     def set_measurements(self, z):
         z = np.ascontiguousarray(z, dtype=np.float64)

@@ -518,6 +518,16 @@ static int stage_rows(gse_plan* plan, int which, const double* src, double* dst_
     CU(cudaEventRecord(plan->stage_done[which], plan->stream));
     return GSE_OK;
 }
+// Same refresh straight from caller-owned PINNED host memory (cudaHostAlloc / torch pin_memory): one
+// asynchronous copy per array on the plan's stream, no staging.  The buffers must stay unchanged until
+// the next solve / iterate call has returned.
+int gse_set_rows_pinned(gse_plan* plan, const double* z_pinned, const double* w_pinned) {
+    CU(cudaSetDevice(plan->device));
+    const size_t bytes = sizeof(double) * plan->hp.n_rows;
+    if (z_pinned && bytes) CU(cudaMemcpyAsync(plan->z.ptr, z_pinned, bytes, cudaMemcpyHostToDevice, plan->stream));
+    if (w_pinned && bytes) CU(cudaMemcpyAsync(plan->w.ptr, w_pinned, bytes, cudaMemcpyHostToDevice, plan->stream));
+    return GSE_OK;
+}
 int gse_set_weights(gse_plan* plan, const double* w) { return stage_rows(plan, 1, w, plan->w.ptr); }
 int gse_set_measurements(gse_plan* plan, const double* z) { return stage_rows(plan, 0, z, plan->z.ptr); }
 

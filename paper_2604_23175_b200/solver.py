@@ -140,6 +140,22 @@ class MultiAreaEstimator:
         self.plan.set_weights(ms.weight)
         self.ms = ms
 
+    def pinned_inputs(self):
+        """(z, w) numpy views of pinned host buffers owned by the estimator.  A data front end writes
+        the next scan's values / weights there in place; ``update_from_pinned`` then moves them to the
+        device with two asynchronous copies (no staging, no host synchronisation)."""
+        if getattr(self, "_pin", None) is None:
+            self._pin = self.torch.empty((2, self.ms.m), dtype=self.torch.float64).pin_memory()
+            self._pin[0].numpy()[:] = self.ms.z
+            self._pin[1].numpy()[:] = self.ms.weight
+        return self._pin[0].numpy(), self._pin[1].numpy()
+
+    def update_from_pinned(self):
+        """Refresh z and w on the device from ``pinned_inputs()`` (same rows, no re-analysis)."""
+        if getattr(self, "_pin", None) is None:
+            raise RuntimeError("pinned_inputs() must be called (and filled) first")
+        self.plan.set_rows_pinned(self._pin[0].data_ptr(), self._pin[1].data_ptr())
+
     def _ptrs(self):
         return self._state[0].data_ptr(), self._state[1].data_ptr()
 

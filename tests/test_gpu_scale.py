@@ -98,3 +98,24 @@ def test_persistent_kernel_iteration_cap_and_failure(G):
     only_vm = G.generate_measurements(net, G.MeasurementConfig(types=(G.MeasurementType.VM,)))
     with pytest.raises(G.SolverError, match="area"):
         G.solve_multiarea(net, only_vm, part)
+
+
+def test_pinned_input_refresh_matches_staged_refresh(G):
+    """update_from_pinned (async copies from caller-visible pinned buffers) == update_measurements."""
+    from conftest import build_case
+    net, ms, part, g = build_case("ieee118_k6")
+    est = G.MultiAreaEstimator(net, ms, part)
+    try:
+        masked = G.apply_mask(ms, G.MeasurementType.QF)
+        est.update_measurements(masked)
+        a, ra = est.estimate()
+        est.update_measurements(ms)
+        zv, wv = est.pinned_inputs()
+        zv[:] = masked.z
+        wv[:] = masked.weight
+        est.update_from_pinned()
+        b, rb = est.estimate()
+        assert ra.iterations == rb.iterations and np.array_equal(a.va, b.va) and np.array_equal(a.vm, b.vm)
+        assert ra.objective == rb.objective
+    finally:
+        est.close()
