@@ -138,6 +138,7 @@ struct __align__(16) FrontScratch {
     int inv[kGatherBatch][kInvRows];
     double ld8[48];            // published 8x8 diagonal factor (36) + reciprocal pivots (8)
     double rinv[64];           // reciprocal pivots of the whole front (stored for the backward pass)
+    double colbuf[2][16];      // two columns of the 8x8 pivot block being eliminated (double-buffered)
 };
 
 __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec* __restrict__ task) {
@@ -242,6 +243,35 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     // (the child list of a task is pruned on the host to the children that reach its regions)
     // (everything static -- child records, row maps -- is staged BEFORE waiting for the children, so
     // that only the loads of their update matrices follow the hand-off)
+    if (direct && nchild == 1) {
+        // Chain piece: the single child's update rows ARE this front's rows (identity map, no original
+        // entries).  The tile is read in place later; the panel rows are a plain copy of row prefixes
+        // of the child's packed update matrix -- coalesced, no index maps, twelve loads per lane in flight.
+        GSE_TICK(7);
+        wait.children(hdr, ft.crecs + hdr.child_off);
+        if (pp) {
+            const double* Uc = ubuf + crec[0].u_off;
+            const int Rn = p + ni + (diag ? 0 : nj);
+            for (int rb = warp; rb < Rn; rb += 6 * nwarps) {
+                double v[6][2];
+#pragma unroll
+                for (int g = 0; g < 6; ++g) {
+                    const int r = rb + g * nwarps;
+                    const int cr_ = r < p ? r : r < p + ni ? p + i0 + (r - p) : p + j0 + (r - p - ni);   // child row
+                    const double* src = Uc + (size_t)cr_ * (cr_ + 1) / 2;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) { const int C = lane + 32 * h; v[g][h] = (r < Rn && C < p && C <= cr_) ? ldc(src + C) : 0.0; }
+                }
+#pragma unroll
+                for (int g = 0; g < 6; ++g) {
+                    const int r = rb + g * nwarps;
+                    const int sr = r < p ? r : r < p + ni ? rp + (r - p) : rp + ri + (r - p - ni);      // panel row
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) { const int C = lane + 32 * h; if (r < Rn && C < p) pan[sr * ld + C] += v[g][h]; }
+                }
+            }
+        }
+    } else
     for (int cb0 = 0; cb0 < nchild; cb0 += kGatherBatch) {
         const int nb = min(kGatherBatch, nchild - cb0);
         const int Rp = rp + ri + rj;
@@ -315,31 +345,51 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                 // run after the chain, one per lane.
                 int badk = -1;
                 double cs = 1.0, mine = 1.0, myc = 1.0;
+                // two pivots per round: one exchange fetches what both elimination steps need
+                // (columns k and k + 1 of the block live in the same lanes), the stage k+1 values of
+                // column k + 1 are recomputed locally, and the serial chain per PAIR of pivots is one
+                // shared-memory exchange plus ~7 dependent FP64 operations.
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double src = (k & 1) ? x1 : x0;                                   // column k lives in lanes (*, k / 2)
-                    const double pv = __shfl_sync(0xffffffffu, src, 4 * k + (k >> 1));        // a_kk
-                    const double aik = __shfl_sync(0xffffffffu, src, (lane & ~3) | (k >> 1)); // a_rk
-                    const double aj0 = __shfl_sync(0xffffffffu, src, 4 * c2 + (k >> 1));      // a_{2c,k}
-                    const double aj1 = __shfl_sync(0xffffffffu, src, 4 * (c2 + 1) + (k >> 1));
+                for (int k = 0; k < 8; k += 2) {
+                    const int kh = k >> 1;
+                    // columns k, k + 1 of the block go through a 16-double shared buffer: one 16-byte store by
+                    // the eight lanes that hold them, then broadcast / quad-uniform 16-byte reads -- a third
+                    // of the load/store-pipe traffic the equivalent nine 64-bit shuffles would need
+                    double2* cb = reinterpret_cast<double2*>(S.colbuf[kh & 1]);
+                    if ((lane & 3) == kh) cb[r] = make_double2(x0, x1);
+                    __syncwarp();
+                    const double pv = cb[k].x;                                               // a[k][k]
+                    const double2 bc = cb[k + 1];                                            // a[k+1][k], a[k+1][k+1]
+                    const double2 ai = cb[r], aj0 = cb[c2], aj1 = cb[c2 + 1];
+                    const double bv = bc.x, cv = bc.y;
+                    const double ai0 = ai.x, ai1 = ai.y;                                     // a[r][k], a[r][k+1]
+                    const double aj00 = aj0.x, aj01 = aj0.y;                                 // a[2c][k], a[2c][k+1]
+                    const double aj10 = aj1.x, aj11 = aj1.y;                                 // a[2c+1][k], a[2c+1][k+1]
+                    // ---- stage k -> k + 1: pivot p_k, exact scale s1 = 2^-(exponent of p_k)
                     badk = (!(pv > 0.0) && badk < 0) ? k : badk;
-                    const bool own = (lane & 7) == k;
-                    mine = own ? pv * cs : mine;
-                    myc = own ? cs : myc;
-                    // exact power-of-two scaling through the exponent field (no floating-point latency):
-                    // ps = p_k 2^-e in [1, 2); the cross product a_ik a_jk is scaled the same way
-                    const int de = (((__double2hiint(pv) >> 20) & 0x7ff) - 1023) * 1048576;
-                    const double ps = __hiloint2double(__double2hiint(pv) - de, __double2loint(pv));
-                    cs *= ps;
-                    const double u0 = aik * aj0, u1 = aik * aj1;
-                    // (a product whose exponent would underflow under the scaling is flushed to zero: it is
-                    // below 2^-1022 relative to the pivot)
-                    const int h0 = __double2hiint(u0), h1 = __double2hiint(u1);
-                    const double s0 = ((h0 & 0x7ff00000) > de) ? __hiloint2double(h0 - de, __double2loint(u0)) : 0.0;
-                    const double s1 = ((h1 & 0x7ff00000) > de) ? __hiloint2double(h1 - de, __double2loint(u1)) : 0.0;
-                    const double n0 = fma(ps, x0, -s0), n1 = fma(ps, x1, -s1);
-                    x0 = (r > k && c2 > k) ? n0 : x0;
-                    x1 = (r > k && c2 + 1 > k) ? n1 : x1;
+                    const double s1 = __hiloint2double((2046 - ((__double2hiint(pv) >> 20) & 0x7ff)) << 20, 0);
+                    const double ps = pv * s1;
+                    const double p1 = fma(ps, cv, -((bv * bv) * s1));                       // a'[k+1][k+1]
+                    const double ui = fma(ps, ai1, -((ai0 * bv) * s1));                     // a'[r][k+1]
+                    const double uj0 = fma(ps, aj01, -((aj00 * bv) * s1));                  // a'[2c][k+1]
+                    const double uj1 = fma(ps, aj11, -((aj10 * bv) * s1));                  // a'[2c+1][k+1]
+                    const double y0 = fma(ps, x0, -((ai0 * aj00) * s1));                    // a'[r][2c]
+                    const double y1 = fma(ps, x1, -((ai0 * aj10) * s1));                    // a'[r][2c+1]
+                    // ---- stage k + 1 -> k + 2: pivot p'_{k+1}
+                    badk = (!(p1 > 0.0) && badk < 0) ? k + 1 : badk;
+                    const double s2 = __hiloint2double((2046 - ((__double2hiint(p1) >> 20) & 0x7ff)) << 20, 0);
+                    const double p1s = p1 * s2;
+                    const double z0 = fma(p1s, y0, -((ui * uj0) * s2));
+                    const double z1 = fma(p1s, y1, -((ui * uj1) * s2));
+                    // reciprocal-square-root arguments and scales of the two pivots (lane l keeps pivot l % 8)
+                    const double cs1 = cs * ps;
+                    const int own = lane & 7;
+                    mine = own == k ? pv * cs : own == k + 1 ? p1 * cs1 : mine;
+                    myc = own == k ? cs : own == k + 1 ? cs1 : myc;
+                    cs = cs1 * p1s;
+                    // own entries: both steps below / right of the pair, the first step only in column k + 1
+                    x0 = (r > k + 1 && c2 > k + 1) ? z0 : x0;
+                    x1 = (r > k + 1 && c2 + 1 > k + 1) ? z1 : ((c2 == k && r > k) ? y1 : x1);
                 }
                 const double q = rsqrt(mine);                  // lane l: 1 / sqrt(p_k c_k) of pivot k = l % 8
                 const double rk = myc * q;                     // 1 / L_kk
