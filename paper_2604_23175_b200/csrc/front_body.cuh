@@ -438,9 +438,12 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
 #pragma unroll
                     for (int j = 0; j < 8; ++j) myrow[j] = j <= i ? s_ld[i * (i + 1) / 2 + j] : 0.0;
                 } else {
+                    // (16-byte accesses: the row stride maps eight rows onto four bank groups, so 8-byte
+                    // accesses of one row per thread would be 8-way bank conflicted)
                     double y[8];
+                    double2* my2 = reinterpret_cast<double2*>(myrow);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) y[j] = myrow[j];
+                    for (int j = 0; j < 4; ++j) { const double2 t2 = my2[j]; y[2 * j] = t2.x; y[2 * j + 1] = t2.y; }
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         y[k] *= s_ld[36 + k];
@@ -448,7 +451,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                         for (int j = k + 1; j < 8; ++j) y[j] = fma(-y[k], s_ld[j * (j + 1) / 2 + k], y[j]);
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) myrow[j] = y[j];
+                    for (int j = 0; j < 4; ++j) my2[j] = make_double2(y[2 * j], y[2 * j + 1]);
                 }
             }
             GSE_PC(5);
@@ -457,6 +460,22 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         }
 #undef GSE_PC
         if (tb && tid == 0) for (int k = 0; k < 7; ++k) tb[8 + k] = pc[k];
+    }
+    // ---- factor panel to global (diagonal tasks own their row chunk): one TMA bulk store per row,
+    // issued as soon as the panel is final so that the copies overlap the trailing update
+    const bool bulk_panel = HAS_PIVOTS && pp && diag && (p & 1) == 0;
+    if (bulk_panel) {
+        fence_proxy_async();            // the rows were written with ordinary shared-memory stores
+        __syncthreads();
+        double* L = lbuf + hdr.l_off;
+        const int n0 = ci == 0 ? p : 0;                       // pivot rows (first chunk only), then the rows of chunk I
+        if (tid < n0 + ni) {
+            const int r = tid < n0 ? tid : tid - n0;
+            const double* src = tid < n0 ? pan + (size_t)r * ld : pan + (size_t)(rp + r) * ld;
+            double* dst = tid < n0 ? L + (size_t)r * p : L + (size_t)(p + i0 + r) * p;
+            tma_store_1d(dst, src, (unsigned)(p * sizeof(double)));
+            tma_store_commit();
+        }
     }
     GSE_TICK(4);
 
@@ -546,14 +565,17 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         // ---- factor panel to global (diagonal tasks own their row chunk) ----------------------
         if (HAS_PIVOTS && pp && diag) {
             double* L = lbuf + hdr.l_off;
-            if (ci == 0) {
-                for (int r = warp; r < p; r += nwarps)
-                    for (int k = lane; k < p; k += 32) L[(size_t)r * p + k] = pan[r * ld + k];
-                if (tid < p) dinv[hdr.dinv_off + tid] = s_rinv[tid];
+            if (ci == 0 && tid < p) dinv[hdr.dinv_off + tid] = s_rinv[tid];
+            if (bulk_panel) {
+                tma_store_wait_all();            // (threads without a pending group return at once)
+            } else {                            // odd pivot count: rows are not 16-byte multiples
+                if (ci == 0)
+                    for (int r = warp; r < p; r += nwarps)
+                        for (int k = lane; k < p; k += 32) L[(size_t)r * p + k] = pan[r * ld + k];
+                double* Li = L + (size_t)(p + i0) * p;
+                for (int r = warp; r < ni; r += nwarps)
+                    for (int k = lane; k < p; k += 32) Li[(size_t)r * p + k] = Pi[r * ld + k];
             }
-            double* Li = L + (size_t)(p + i0) * p;
-            for (int r = warp; r < ni; r += nwarps)
-                for (int k = lane; k < p; k += 32) Li[(size_t)r * p + k] = Pi[r * ld + k];
         }
         GSE_TICK(6);
     }

@@ -165,6 +165,15 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// shared -> global bulk copy (TMA store); bytes and both addresses are multiples of 16.  The issuing
+// thread commits and, before the data may be signalled to other CTAs, waits for the group.
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // One staged accumulation item (symbolic.cpp: build_acc_items), entirely out of shared memory:
 // one thread starts two TMA bulk copies (contribution pairs, item-local pointers) while all
 // threads gather the item's distinct values (independent loads, eight in flight per thread);
