@@ -139,6 +139,7 @@ struct __align__(16) FrontScratch {
     double ld8[48];            // published 8x8 diagonal factor (36) + reciprocal pivots (8)
     double rinv[64];           // reciprocal pivots of the whole front (stored for the backward pass)
     double colbuf[2][16];      // two columns of the 8x8 pivot block being eliminated (double-buffered)
+    int nready;                // children of the current gather batch that are complete
 };
 
 __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec* __restrict__ task) {
@@ -153,6 +154,7 @@ struct NoWait {
     __device__ __forceinline__ void parent(const BwdTask&) const {}
     __device__ __forceinline__ void originals(const TaskRec&) const {}
     __device__ __forceinline__ void children(const TaskRec&, const ChildRec*) const {}
+    __device__ __forceinline__ int ready_children(const TaskRec&, const ChildRec*, int c, int nb, int*) const { return nb - c; }
     __device__ __forceinline__ void panels(const TaskRec&) const {}
 };
 
@@ -164,8 +166,8 @@ struct NoWait {
 //                its slice of the factor panel (ci == cj on the host side; no tile);
 //   2 update  -- assemble the tile, then read the finished panels L_I, L_J of the front back from
 //                the factor storage and run the trailing update (no pivot rows in shared memory).
-// wait.originals() runs before the first read of gval, wait.children() before the first read of a
-// child's update matrix (it ends with a CTA barrier when it waited), wait.panels() before
+// wait.originals() runs before the first read of gval, wait.children() / wait.ready_children() before
+// the first read of a child's update matrix (they end with a CTA barrier when they waited), wait.panels() before
 // the first read of the front's own factor panels (kind 2).
 template <int HAS_PIVOTS, class Wait>
 __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, const FrontTab& ft, const double* gval,
@@ -295,14 +297,21 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
             }
         }
         __syncthreads();
-        if (cb0 == 0) { GSE_TICK(7); wait.children(hdr, ft.crecs + hdr.child_off); }
-        GatherArgs ga{pan, tile, &s_inv[0][0], ubuf, pp, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
-        const ChildRec* cb = crec + cbase;
-        switch (nb) {
-            case 1: gather_batch<1, 8>(ga, cb); break;
-            case 2: gather_batch<2, 4>(ga, cb); break;
-            case 3: gather_batch<3, 4>(ga, cb); break;
-            default: gather_batch<4, 4>(ga, cb); break;
+        if (cb0 == 0) GSE_TICK(7);
+        // children are taken in order, as many at a time as are already complete: the contributions of a
+        // child that finished early are folded in while the task still waits for its slower sibling
+        // (the sums are sequential per child either way, so the grouping does not change a bit)
+        for (int c = 0; c < nb;) {
+            const int ready = wait.ready_children(hdr, ft.crecs + hdr.child_off + cb0, c, nb, &S.nready);
+            GatherArgs ga{pan, tile, &s_inv[c][0], ubuf, pp, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
+            const ChildRec* cb = crec + cbase + c;
+            switch (ready) {
+                case 1: gather_batch<1, 8>(ga, cb); break;
+                case 2: gather_batch<2, 4>(ga, cb); break;
+                case 3: gather_batch<3, 4>(ga, cb); break;
+                default: gather_batch<4, 4>(ga, cb); break;
+            }
+            c += ready;
         }
     }
     __syncthreads();

@@ -96,6 +96,21 @@ struct SpinWait {
         }
         __syncthreads();
     }
+    // Blocks until child c of the batch is complete, then counts how many of the following children
+    // of the batch are complete as well (without waiting for them).  cr = records of the batch.
+    __device__ __forceinline__ int ready_children(const TaskRec&, const ChildRec* cr, int c, int nb, int* s_n) const {
+        if (threadIdx.x == 0) {
+            wait_ge(ctr + CTR_FRONT0 + cr[c].front, (unsigned)cr[c].need * epoch);
+            int n = 1;
+            while (c + n < nb && ld_acquire(ctr + CTR_FRONT0 + cr[c + n].front) >= (unsigned)cr[c + n].need * epoch) ++n;
+            *s_n = n;
+            if (tr) tr[2] = globaltimer();
+        }
+        __syncthreads();
+        const int n = *s_n;
+        __syncthreads();
+        return n;
+    }
 };
 
 }  // namespace

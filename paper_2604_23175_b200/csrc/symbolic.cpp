@@ -848,6 +848,26 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         for (int c : f.children) lv = std::max(lv, hp.fronts[c].level + 1);
         f.level = lv; n_levels = std::max(n_levels, lv + 1);
     }
+    // Child order = summation order of the extend-add.  The dataflow kernel folds a child's update
+    // matrix in as soon as that child is complete while it still waits for the next one, so children
+    // are ordered by the length of the pivot chain below them (the proxy for when they finish): the
+    // slowest subtree comes last.  Area roots stay first and in area order (assemble_boundary's order).
+    {
+        std::vector<int> by_level(hp.fronts.size());
+        std::iota(by_level.begin(), by_level.end(), 0);
+        std::stable_sort(by_level.begin(), by_level.end(), [&](int a, int b) { return hp.fronts[a].level < hp.fronts[b].level; });
+        std::vector<int64_t> chain(hp.fronts.size(), 0);
+        for (int fi : by_level) {
+            Front& f = hp.fronts[fi];
+            if ((f.kind == 0 || f.kind == 3) && f.child_rel.empty())
+                std::stable_sort(f.children.begin(), f.children.end(), [&](int a, int b) {
+                    const int64_t ka = hp.fronts[a].kind == 1 ? -1 : chain[a], kb = hp.fronts[b].kind == 1 ? -1 : chain[b];
+                    return ka < kb; });
+            int64_t c = 0;
+            for (int ch : f.children) c = std::max(c, chain[ch]);
+            chain[fi] = c + f.p + 8;       // + a per-front overhead (hand-off, gather) in pivot units
+        }
+    }
     hp.fwd_levels.assign(n_levels, {}); hp.level_phase.assign(n_levels, 1);
     for (size_t fi = 0; fi < hp.fronts.size(); ++fi) {
         Front& f = hp.fronts[fi];
