@@ -228,6 +228,19 @@ void build_acc_items(HostProgram& hp) {
     if (getenv("GSE_DEBUG_ACC")) {
         int n_items = (int)(hp.acc_items.size() / 8), max_nd = 0, max_np = hp.acc_pair_max; double sum_nu = 0;
         for (int i = 0; i < n_items; ++i) { max_nd = std::max(max_nd, hp.acc_items[8 * i + 1]); sum_nu += hp.acc_items[8 * i + 3]; }
+        {   // contribution-list lengths: the longest list of an item bounds its sequential rounds
+            int64_t sum_max = 0, sum_w0 = 0; int gmax = 0;
+            for (int i = 0; i < n_items; ++i) {
+                const int l0 = hp.acc_items[8 * i + 6], nd = hp.acc_items[8 * i + 1];
+                const int32_t* ord = &hp.acc_lptr[l0 + nd + 1];
+                auto len = [&](int d) { return hp.acc_lptr[l0 + d + 1] - hp.acc_lptr[l0 + d]; };
+                const int mx = nd ? len(ord[0]) : 0; gmax = std::max(gmax, mx); sum_max += mx;
+                int w0 = 0; for (int g = 0; g * 256 < nd; ++g) w0 += len(ord[g * 256]);   // rounds of thread 0 over its groups
+                sum_w0 += w0;
+            }
+            fprintf(stderr, "acc lists: longest %d, mean longest per item %.1f, mean rounds of the slowest thread %.1f\n",
+                    gmax, (double)sum_max / std::max(n_items, 1), (double)sum_w0 / std::max(n_items, 1));
+        }
         fprintf(stderr, "acc items %d (dmax %lld): max dests %d, max pairs %d, max values %d, mean values %.0f, n_val %lld, n_gval %lld, pairs %zu\n",
                 n_items, (long long)dmax, max_nd, max_np, hp.acc_stage_max, sum_nu / std::max(n_items, 1), (long long)hp.n_val, (long long)n, hp.acc_a.size());
     }
