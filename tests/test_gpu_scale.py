@@ -119,3 +119,71 @@ def test_pinned_input_refresh_matches_staged_refresh(G):
         assert ra.objective == rb.objective
     finally:
         est.close()
+
+
+@pytest.mark.parametrize("name,world", [("ieee118_k6", 2), ("pegase2869_k8", 3)])
+def test_rank_sharded_plans_on_one_device_match_single_plan_bitwise(G, name, world):
+    """The multi-rank device path without a cluster: ``world`` rank plans (each owning a block of
+    areas) live on the one GPU and exchange their packed (S_b | b_hat) segments and delta_x_Gamma
+    with device copies -- exactly what the NCCL send/recv + broadcast of distributed.py move.  The
+    result must equal the single-plan solve bit for bit (blocks are summed on the coordinator in
+    area order)."""
+    import torch
+    from conftest import build_case
+    from paper_2604_23175_b200.distributed import CudaEngine, area_work_estimate, assign_areas
+    net, ms, part, g = build_case(name)
+    bord, maps = G.build_variable_maps(net, part)
+    cfg = G.SolverConfig()
+    ref, rref = G.solve_multiarea(net, ms, part, maps=(bord, maps), config=cfg)
+    area_rank = assign_areas(area_work_estimate(maps), world)
+    assert len(set(area_rank.tolist())) == world
+    engines = [CudaEngine(net, ms, part, bord, maps, cfg, r, world, area_rank, 0) for r in range(world)]
+    try:
+        flat = G.StateVector.flat_start(net)
+        for e in engines:
+            e.load_state(flat.va, flat.vm)
+        off = engines[0].offsets
+        iterations = 0
+        for it in range(1, cfg.max_outer_iterations + 1):
+            for e in engines:
+                e.phase_local()
+                e.sync()
+            for r in range(1, world):                       # the variable-size gather to the coordinator
+                mine = np.flatnonzero(area_rank == r)
+                lo, hi = int(off[mine[0]]), int(off[mine[-1] + 1])
+                engines[0].exchange[lo:hi].copy_(engines[r].exchange[lo:hi])
+            torch.cuda.synchronize()
+            engines[0].phase_boundary()
+            engines[0].sync()
+            for r in range(1, world):                       # the broadcast of delta_x_Gamma
+                engines[r].delta.copy_(engines[0].delta)
+            torch.cuda.synchronize()
+            delta = max(e.phase_recover() for e in engines)
+            iterations = it
+            if delta < cfg.convergence_tol:
+                break
+        assert iterations == rref.iterations
+        state = engines[0].state.clone()
+        for r in range(1, world):                           # interiors of the other ranks' areas
+            m = engines[r].owned_mask
+            state[:, m] = engines[r].state[:, m]
+        out = state.cpu().numpy()
+        assert np.array_equal(out[0], ref.va) and np.array_equal(out[1], ref.vm)
+    finally:
+        for e in engines:
+            e.close()
+
+
+def test_distributed_estimator_single_rank_on_device(G):
+    """DistributedEstimator with its product engine (CudaEngine) on one rank == MultiAreaEstimator."""
+    from conftest import build_case
+    from paper_2604_23175_b200.distributed import DistributedEstimator
+    net, ms, part, g = build_case("ieee118_k6")
+    est = DistributedEstimator(net, ms, part)
+    try:
+        st, rep = est.estimate()
+    finally:
+        est.close()
+    ref, rref = G.solve_multiarea(net, ms, part)
+    assert rep.iterations == rref.iterations and rep.converged
+    assert np.array_equal(st.va, ref.va) and np.array_equal(st.vm, ref.vm) and rep.objective == rref.objective
