@@ -43,14 +43,14 @@ d = np.diff(clk[:, :7], axis=1)   # zero, orig, children, panel, dmma, store
 labels = ["zero", "orig", "extend-add", "panel", "dmma", "Lstore"]
 # tasks are laid out launch by launch in the same order as the front launches above
 pos = 0
-print("per-launch front task phases (cycles, max over the launch's CTAs of total; phases of that slowest CTA)")
+print("per-launch front task phases (globaltimer ns, max over the launch's CTAs of total; phases of that slowest CTA)")
 for i in range(n):
     if kind[i] != 2:
         continue
     blk = d[pos:pos + ct[i]]
     tot = blk.sum(axis=1)
     w = int(np.argmax(tot))
-    print(f"launch {i:2d} ctas {ct[i]:4d} slowest {tot[w]:7d} cyc: " + " ".join(f"{l}={v}" for l, v in zip(labels, blk[w])) + f" | median total {int(np.median(tot))}")
+    print(f"launch {i:2d} ctas {ct[i]:4d} slowest {tot[w]:7d} ns: " + " ".join(f"{l}={v}" for l, v in zip(labels, blk[w])) + f" | median total {int(np.median(tot))}")
     row = clk[pos + w]
     if row[24] > 0:
         print("      last panel block: diag-dmma=%d load-d=%d factor=%d publish=%d sync1=%d trsm=%d sync2=%d" % tuple(int(row[k + 1] - row[k]) for k in range(24, 31)))
