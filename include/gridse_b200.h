@@ -73,6 +73,7 @@ typedef struct {
                               * 1 persistent, 2 level launches captured in a CUDA graph             */
     int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default 48) */
     int32_t boundary_mode;   /* boundary factorisation: 0 auto, 1 dense chain (dense_cholesky_solve), 2 block-sparse tree */
+    void *stream;            /* cudaStream_t every kernel / copy of the plan is enqueued on; NULL = a stream of its own */
 } gse_options;
 
 typedef struct {
@@ -139,6 +140,13 @@ int gse_phase_boundary(gse_plan *plan);
 /* interior_recover + apply_interior_delta + BoundaryOrdering.apply_delta + the
  * stacked infinity norm (linalg.py:427-434, partition.py:59-62,113-116, solver.py:328-333). */
 int gse_phase_recover(gse_plan *plan, double *va_dev, double *vm_dev, double *delta_inf);
+/* The same phases, enqueue-only (no host synchronisation, no failure check): with gse_options.stream set
+ * to the caller's stream, collectives enqueued there between the calls are ordered by the stream.
+ * gse_phase_recover_async leaves [max |dx|, failed ? 1 : 0] in gse_status_dev for one MAX all-reduce;
+ * after a reduced failure flag, gse_check on the owning rank names the area / pivot. */
+int gse_phase_local_async(gse_plan *plan, const double *va_dev, const double *vm_dev);
+int gse_phase_boundary_async(gse_plan *plan);
+int gse_phase_recover_async(gse_plan *plan, double *va_dev, double *vm_dev);
 /* Poll the device failure flag after a phase: 0 or GSE_E_NOT_SPD_*. */
 int gse_check(gse_plan *plan);
 /* objective(ms, state) (solver.py:100-103). */

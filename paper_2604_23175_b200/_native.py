@@ -48,6 +48,7 @@ class Options(C.Structure):
         ("max_pivots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("area_rank", i32p), ("persistent", C.c_int32), ("tile_rows", C.c_int32),
         ("boundary_mode", C.c_int32),
+        ("stream", C.c_void_p),
     ]
 
 
@@ -102,6 +103,9 @@ def lib():
     L.gse_solve.argtypes = [vp, C.POINTER(Config), vp, vp, C.POINTER(Report)]
     L.gse_iterate.argtypes = [vp, vp, vp, f64p]
     L.gse_inner_step.argtypes = [vp, vp, vp, f64p]
+    L.gse_phase_local_async.argtypes = [vp, vp, vp]
+    L.gse_phase_boundary_async.argtypes = [vp]
+    L.gse_phase_recover_async.argtypes = [vp, vp, vp]
     L.gse_set_rows_pinned.argtypes = [vp, vp, vp]
     L.gse_matrix_plan_create.argtypes = [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, C.POINTER(Options), C.POINTER(vp)]
     L.gse_matrix_set_values.argtypes = [vp, f64p, f64p, f64p, f64p, f64p]
@@ -143,7 +147,8 @@ EXPORTED = [
     "gse_boundary_system", "gse_set_boundary_delta", "gse_exchange_buffer_dev",
     "gse_exchange_offsets", "gse_boundary_delta_dev", "gse_status_dev", "gse_plan_stats",
     "gse_version", "gse_stream", "gse_matrix_plan_create", "gse_matrix_set_values", "gse_matrix_condense",
-    "gse_matrix_recover", "gse_assemble_boundary", "gse_debug_trace", "gse_solve_layout",
+    "gse_matrix_recover", "gse_assemble_boundary", "gse_phase_local_async", "gse_phase_boundary_async",
+    "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout",
 ]
 
 
@@ -224,7 +229,7 @@ class Plan:
     """Owner of one ``gse_plan`` (analysis + device program of one problem)."""
 
     def __init__(self, net, ms, part, bord, maps, *, device=0, dense=False, leaf_buses=0,
-                 max_pivots=0, rank=0, world=1, area_rank=None, tile_rows=0, boundary_mode=0):
+                 max_pivots=0, rank=0, world=1, area_rank=None, tile_rows=0, boundary_mode=0, stream=None):
         L = lib()
         self._desc, self._keep = make_desc(net, ms, part, bord, maps)
         opt = Options()
@@ -233,6 +238,7 @@ class Plan:
         opt.rank, opt.world = int(rank), int(world)
         opt.tile_rows = int(tile_rows)
         opt.boundary_mode = int(boundary_mode)
+        opt.stream = int(stream) if stream else None      # cudaStream_t of the caller (e.g. torch's current stream)
         if area_rank is not None:
             self._keep["area_rank"] = np.ascontiguousarray(area_rank, dtype=np.int32)
             opt.area_rank = _ip(self._keep["area_rank"])
@@ -302,6 +308,19 @@ class Plan:
         j = C.c_double()
         self._call(lib().gse_objective(self._h, va_ptr, vm_ptr, C.byref(j)))
         return j.value
+
+    # -- phases, enqueue-only (multi-GPU driver) ------------------------------------
+    def phase_local_async(self, va_ptr, vm_ptr):
+        self._call(lib().gse_phase_local_async(self._h, va_ptr, vm_ptr))
+
+    def phase_boundary_async(self):
+        self._call(lib().gse_phase_boundary_async(self._h))
+
+    def phase_recover_async(self, va_ptr, vm_ptr):
+        self._call(lib().gse_phase_recover_async(self._h, va_ptr, vm_ptr))
+
+    def check(self):
+        self._call(lib().gse_check(self._h))
 
     # -- phases ----------------------------------------------------------------------
     def phase_assemble(self, va_ptr, vm_ptr):
@@ -385,6 +404,9 @@ class Plan:
 
     def boundary_delta_ptr(self):
         return lib().gse_boundary_delta_dev(self._h)
+
+    def status_ptr(self):
+        return lib().gse_status_dev(self._h)
 
     def stats(self):
         s = np.zeros(16)

@@ -48,6 +48,7 @@ struct gse_plan {
     gse_error err{};
     int device = 0;
     cudaStream_t stream = nullptr;
+    bool own_stream = true;                   // false: the caller's stream (gse_options.stream)
     bool coordinator = true;
 
     // network + measurements
@@ -204,7 +205,7 @@ gse_plan::~gse_plan() {
     cudaSetDevice(device);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
-    if (stream) cudaStreamDestroy(stream);
+    if (stream && own_stream) cudaStreamDestroy(stream);
     if (h_flags) cudaFreeHost(h_flags);
     if (h_obj) cudaFreeHost(h_obj);
     if (h_blk) cudaFreeHost(h_blk);
@@ -267,7 +268,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     if (!msg.empty()) return fail(plan, GSE_E_INVALID, msg);
     if (hp.max_front >= 65535) return fail(plan, GSE_E_INVALID, "front order exceeds 65534");
 
-    CU(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
+    if (opt && opt->stream) { plan->stream = (cudaStream_t)opt->stream; plan->own_stream = false; }
+    else CU(cudaStreamCreateWithFlags(&plan->stream, cudaStreamNonBlocking));
     CU(configure_kernels());
     CU(configure_unit_kernels());
     for (auto& e : plan->ev) CU(cudaEventCreate(&e));
@@ -833,6 +835,33 @@ int gse_phase_recover(gse_plan* plan, double* va, double* vm, double* delta_inf)
     double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
     if (delta_inf) *delta_inf = dv;
     CU(cudaMemcpy(plan->status.ptr, &dv, sizeof dv, cudaMemcpyHostToDevice));
+    return GSE_OK;
+}
+
+// ---- asynchronous phases (multi-GPU driver): enqueue only, no host synchronisation ----------------
+// With gse_options.stream = the caller's stream, the collectives the caller enqueues on that stream
+// (NCCL send/recv of the exchange segments, broadcast of delta_x_Gamma, MAX all-reduce of the status)
+// are ordered with the phases by the stream itself; the host synchronises once per iteration, when it
+// reads the reduced status.
+int gse_phase_local_async(gse_plan* plan, const double* va, const double* vm) {
+    CU(cudaSetDevice(plan->device));
+    plan->launches_last = enqueue_phase_assemble(plan, va, vm);      // launches of this iteration (gse_plan_stats[0])
+    plan->launches_last += enqueue_fwd(plan, 1);
+    return GSE_OK;
+}
+int gse_phase_boundary_async(gse_plan* plan) {
+    CU(cudaSetDevice(plan->device));
+    if (!plan->coordinator) return GSE_OK;
+    plan->launches_last += enqueue_fwd(plan, 2) + enqueue_fwd(plan, 3) + enqueue_bwd(plan, 3);
+    return GSE_OK;
+}
+// interiors + state update; then status[0] = max |dx| of this rank, status[1] = 1 if any factorisation of
+// this rank failed since the last gse_check (else 0) -- two doubles for one MAX all-reduce
+int gse_phase_recover_async(gse_plan* plan, double* va, double* vm) {
+    CU(cudaSetDevice(plan->device));
+    CU(cudaMemsetAsync(plan->flags.ptr, 0, sizeof(unsigned long long), plan->stream));
+    plan->launches_last += enqueue_bwd(plan, 4) + enqueue_update(plan, va, vm) + 1;
+    launch_status(plan->flags.ptr, plan->status.ptr, plan->stream);
     return GSE_OK;
 }
 

@@ -132,6 +132,13 @@ void launch_assemble_boundary(int n_gamma, int n_areas, const int32_t* inv, cons
     assemble_boundary_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n_gamma, n_areas, inv, off, sel_ptr, s_b, b_hat, s_gamma, b_gamma);
 }
 
+// flags = [|dx| max as ordered bits, failure code (~0 = none)] -> status = [max |dx|, failed ? 1 : 0]
+__global__ void status_kernel(const unsigned long long* __restrict__ flags, double* __restrict__ status) {
+    status[0] = __longlong_as_double((long long)flags[0]);
+    status[1] = flags[1] != ~0ull ? 1.0 : 0.0;
+}
+void launch_status(const unsigned long long* flags, double* status, cudaStream_t s) { status_kernel<<<1, 1, 0, s>>>(flags, status); }
+
 cudaError_t configure_unit_kernels() {
     return cudaFuncSetAttribute(accumulate_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccSmemBytes);
 }

@@ -94,6 +94,7 @@ void launch_objective(const EvalProg& ep, const int32_t* m_type, const int32_t* 
                       const int32_t* br_from, const int32_t* br_to, int n_rows, const double* va,
                       const double* vm, double* partial, double* out, cudaStream_t s);
 int objective_blocks(int n_rows);
+void launch_status(const unsigned long long* flags, double* status, cudaStream_t s);
 void launch_assemble_boundary(int n_gamma, int n_areas, const int32_t* inv, const int64_t* off, const int32_t* sel_ptr,
                               const double* s_b, const double* b_hat, double* s_gamma, double* b_gamma, cudaStream_t s);
 cudaError_t configure_kernels();

@@ -59,21 +59,30 @@ def assign_areas(work, world):
 class CudaEngine:
     """Phase engine over the C-ABI plan (``libgridse_b200.so``)."""
 
-    def __init__(self, net, ms, part, bord, maps, cfg, rank, world, area_rank, device):
+    # the plan enqueues on torch's current stream, so the NCCL collectives torch orders against that
+    # stream need no host synchronisation between the phases (one per iteration: the status read)
+    async_phases = True
+
+    def __init__(self, net, ms, part, bord, maps, cfg, rank, world, area_rank, device, stream=None):
         import torch
         from . import _native
         self.torch = torch
         self.dev = torch.device("cuda", device)
+        # a stream of the engine's own (the legacy default stream cannot be handed over as "the caller's
+        # stream"); the driver makes it torch's current stream around every phase and collective
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.dev)
         self.plan = _native.Plan(net, ms, part, bord, maps, device=device,
                                  dense=cfg.backend == "dense", rank=rank, world=world,
-                                 area_rank=area_rank,
+                                 area_rank=area_rank, stream=self.stream.cuda_stream,
                                  boundary_mode={"auto": 0, "dense": 1, "sparse": 2}[cfg.boundary])
+        self.net, self.bord = net, bord
         self.n_bus, self.n_gamma = net.n_bus, bord.n_gamma
         self.state = torch.empty((2, net.n_bus), dtype=torch.float64, device=self.dev)
         ptr, n, off = self.plan.exchange_buffer()
         self.offsets = off
         self.exchange = self._view(ptr, n)
         self.delta = self._view(self.plan.boundary_delta_ptr(), max(self.n_gamma, 1))[: self.n_gamma]
+        self.status = self._view(self.plan.status_ptr(), 2)      # [max |dx|, failed ? 1 : 0] after recover_async
         owned = np.zeros(net.n_bus, dtype=bool)
         for a, m in enumerate(maps):
             if area_rank[a] == rank:
@@ -88,20 +97,51 @@ class CudaEngine:
                                            "data": (int(ptr), False), "version": 3}
         return self.torch.as_tensor(holder, device=self.dev)
 
+    def stream_ctx(self):
+        """Context in which torch ops and collectives are ordered with the plan's kernels."""
+        return self.torch.cuda.stream(self.stream)
+
     def load_state(self, va, vm):
-        self.state.copy_(self.torch.from_numpy(np.stack([va, vm])))
+        with self.stream_ctx():
+            self.state.copy_(self.torch.from_numpy(np.stack([va, vm])))
         self.torch.cuda.synchronize(self.dev)
+
+    def _translated(self, fn, *args):
+        from . import _native
+        from .solver import raise_solver_error
+        try:
+            return fn(*args)
+        except _native.NativeError as exc:
+            raise_solver_error(exc, self.net, self.bord)
 
     def phase_local(self):
         va, vm = self.state[0].data_ptr(), self.state[1].data_ptr()
         self.plan.phase_assemble(va, vm)
-        self.plan.phase_condense()
+        self._translated(self.plan.phase_condense)
 
     def phase_boundary(self):
-        self.plan.phase_boundary()
+        self._translated(self.plan.phase_boundary)
 
     def phase_recover(self):
         return self.plan.phase_recover(self.state[0].data_ptr(), self.state[1].data_ptr())
+
+    # enqueue-only variants (same kernels; no host synchronisation, failures surface in status[1])
+    def phase_local_async(self):
+        self.plan.phase_local_async(self.state[0].data_ptr(), self.state[1].data_ptr())
+
+    def phase_boundary_async(self):
+        self.plan.phase_boundary_async()
+
+    def phase_recover_async(self):
+        self.plan.phase_recover_async(self.state[0].data_ptr(), self.state[1].data_ptr())
+
+    def check(self):
+        """Raise the precise error of a failed factorisation owned by this rank (synchronises)."""
+        self._translated(self.plan.check)
+
+    def launches_last(self):
+        """Kernels this rank's plan enqueued in the iteration just finished."""
+        return int(self.plan.stats()["launches_last"])
 
     def sync(self):
         self.torch.cuda.synchronize(self.dev)
@@ -174,13 +214,49 @@ class DistributedEstimator:
         self.ms = ms
 
     def estimate(self, on_iteration=None):
+        ctx = getattr(self.engine, "stream_ctx", None)
+        if ctx is None:
+            return self._estimate(on_iteration)
+        with ctx():
+            return self._estimate(on_iteration)
+
+    def _estimate(self, on_iteration=None):
         cfg, eng = self.cfg, self.engine
         t_start = time.perf_counter()
         flat = StateVector.flat_start(self.net)
         eng.load_state(flat.va, flat.vm)
         iterations, converged, deltas = 0, False, []
+        self.launches_per_solve = 0
         t_loop = time.perf_counter()
+        use_async = bool(getattr(eng, "async_phases", False))
         for it in range(1, cfg.max_outer_iterations + 1):
+            if use_async:
+                # one pipeline per iteration on the engine's stream: local condensation -> gather of the
+                # (S_b | b_hat) segments -> boundary solve on the coordinator -> broadcast of delta_x_Gamma
+                # -> recovery -> MAX all-reduce of [delta, failed]; the host waits once, for that pair
+                eng.phase_local_async()
+                self._gather_blocks()
+                if self.rank == 0 and self.n_gamma:
+                    eng.phase_boundary_async()
+                if self.world > 1 and self.n_gamma:
+                    self.dist.broadcast(eng.delta, src=0, group=self.group)
+                eng.phase_recover_async()
+                if self.world > 1:
+                    self.dist.all_reduce(eng.status, op=self.dist.ReduceOp.MAX, group=self.group)
+                delta, failed = (float(v) for v in eng.status.cpu())
+                self.launches_per_solve += eng.launches_last()
+                if failed:
+                    eng.check()        # the owning rank raises the precise error ...
+                    raise SolverError("a factorisation on another rank is not positive definite; "
+                                      "the area it belongs to is likely locally unobservable")
+                iterations = it
+                deltas.append(delta)
+                if on_iteration is not None:
+                    on_iteration(it, self._full_state(), delta)
+                if delta < cfg.convergence_tol:
+                    converged = True
+                    break
+                continue
             failure = None
             try:
                 eng.phase_local()

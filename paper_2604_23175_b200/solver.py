@@ -105,6 +105,24 @@ def _torch():
     return torch
 
 
+def raise_solver_error(exc, net, bord, method="multiarea"):
+    """Re-raise a ``NativeError`` of the C ABI with the reference's texts (solver.py:250-251,304-309)."""
+    if exc.code == _native.GSE_E_NOT_SPD_AREA:
+        ctx = f"area {exc.area} interior block"
+        inner = NotPositiveDefiniteError(exc.pivot, ctx)
+        if method == "centralized":
+            raise SolverError(
+                f"gain matrix {inner}: system unobservable or ill-conditioned") from inner
+        raise SolverError(f"{inner}; area {exc.area} is likely locally unobservable") from inner
+    if exc.code == _native.GSE_E_NOT_SPD_BOUNDARY:
+        inner = NotPositiveDefiniteError(exc.pivot, "boundary system")
+        bus, quant = bord.entries[exc.pivot]
+        raise SolverError(
+            f"boundary system not positive definite at pivot {exc.pivot} "
+            f"(bus {net.buses[bus].id}, {quant})") from inner
+    raise exc
+
+
 class MultiAreaEstimator:
     """Plan once, estimate many times (device-resident Gauss-Newton loop)."""
 
@@ -168,20 +186,7 @@ class MultiAreaEstimator:
         return StateVector(va=arr[0].copy(), vm=arr[1].copy())
 
     def _raise(self, exc):
-        if exc.code == _native.GSE_E_NOT_SPD_AREA:
-            ctx = f"area {exc.area} interior block"
-            inner = NotPositiveDefiniteError(exc.pivot, ctx)
-            if self.method == "centralized":
-                raise SolverError(
-                    f"gain matrix {inner}: system unobservable or ill-conditioned") from inner
-            raise SolverError(f"{inner}; area {exc.area} is likely locally unobservable") from inner
-        if exc.code == _native.GSE_E_NOT_SPD_BOUNDARY:
-            inner = NotPositiveDefiniteError(exc.pivot, "boundary system")
-            bus, quant = self.bord.entries[exc.pivot]
-            raise SolverError(
-                f"boundary system not positive definite at pivot {exc.pivot} "
-                f"(bus {self.net.buses[bus].id}, {quant})") from inner
-        raise exc
+        raise_solver_error(exc, self.net, self.bord, self.method)
 
     # -- the solve -----------------------------------------------------------------------
     def estimate(self, on_iteration=None, t_start=None):

@@ -85,20 +85,61 @@ class OracleEngine:
         pass
 
 
+class AsyncOracleEngine(OracleEngine):
+    """The same engine behind the enqueue-only phase interface (CudaEngine.async_phases): exercises the
+    pipelined driver path -- failures and the norm travel in ``status`` through one MAX all-reduce."""
+
+    async_phases = True
+
+    def __init__(self, *a, **k):
+        import torch
+        super().__init__(*a, **k)
+        self.status = torch.zeros(2, dtype=torch.float64)
+        self.failed = None
+
+    def phase_local_async(self):
+        try:
+            self.phase_local()
+        except Exception as exc:              # a device plan records the failure and keeps going
+            self.failed = exc
+
+    def phase_boundary_async(self):
+        try:
+            self.phase_boundary()
+        except Exception as exc:
+            self.failed = exc
+
+    def phase_recover_async(self):
+        d = 0.0
+        if self.failed is None:
+            try:
+                d = self.phase_recover()
+            except Exception as exc:
+                self.failed = exc
+        self.status[0], self.status[1] = d, 1.0 if self.failed is not None else 0.0
+
+    def check(self):
+        if self.failed is not None:
+            raise self.failed
+
+    def launches_last(self):
+        return 0
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, out_dir):
+def _worker(rank, world, port, name, out_dir, async_phases=False):
     import torch.distributed as dist
     from conftest import build_case
     from paper_2604_23175_b200.distributed import DistributedEstimator
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         net, ms, part, g = build_case(name)
-        est = DistributedEstimator(net, ms, part, engine_factory=OracleEngine)
+        est = DistributedEstimator(net, ms, part, engine_factory=AsyncOracleEngine if async_phases else OracleEngine)
         trace = []
         state, rep = est.estimate(on_iteration=lambda it, s, d: trace.append(d))
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), va=state.va, vm=state.vm,
@@ -108,13 +149,14 @@ def _worker(rank, world, port, name, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("ieee118_k6", 2), ("rand120_k4", 3), ("ieee14_k2", 2)])
-def test_sharded_solve_is_bit_identical_to_single_process(tmp_path, name, world):
+@pytest.mark.parametrize("name,world,async_phases", [("ieee118_k6", 2, False), ("rand120_k4", 3, False), ("ieee14_k2", 2, False),
+                                                     ("ieee118_k6", 2, True), ("rand120_k4", 3, True)])
+def test_sharded_solve_is_bit_identical_to_single_process(tmp_path, name, world, async_phases):
     import torch.multiprocessing as mp
     from conftest import build_case
     from oracle.mase_oracle import Oracle
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, name, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, name, str(tmp_path), async_phases), nprocs=world, join=True)
     net, ms, part, g = build_case(name)
     ref = Oracle(net, ms, part.area_of_bus).solve()
     outs = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]

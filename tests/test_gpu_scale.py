@@ -174,6 +174,74 @@ def test_rank_sharded_plans_on_one_device_match_single_plan_bitwise(G, name, wor
             e.close()
 
 
+@pytest.mark.parametrize("name,world", [("ieee118_k6", 2), ("pegase2869_k8", 3)])
+def test_rank_sharded_plans_enqueue_only_pipeline_matches_single_plan_bitwise(G, name, world):
+    """The pipelined multi-rank iteration (gse_phase_*_async on one shared stream): no host
+    synchronisation between the phases and the exchanges, one status read per iteration.  Device
+    copies on that stream stand in for the NCCL send/recv, broadcast and MAX all-reduce."""
+    import torch
+    from conftest import build_case
+    from paper_2604_23175_b200.distributed import CudaEngine, area_work_estimate, assign_areas
+    net, ms, part, g = build_case(name)
+    bord, maps = G.build_variable_maps(net, part)
+    cfg = G.SolverConfig()
+    ref, rref = G.solve_multiarea(net, ms, part, maps=(bord, maps), config=cfg)
+    area_rank = assign_areas(area_work_estimate(maps), world)
+    stream = torch.cuda.Stream(torch.device("cuda", 0))
+    engines = [CudaEngine(net, ms, part, bord, maps, cfg, r, world, area_rank, 0, stream=stream) for r in range(world)]
+    try:
+        flat = G.StateVector.flat_start(net)
+        for e in engines:
+            e.load_state(flat.va, flat.vm)
+        off = engines[0].offsets
+        iterations, deltas = 0, []
+        with torch.cuda.stream(stream):
+            for it in range(1, cfg.max_outer_iterations + 1):
+                for e in engines:
+                    e.phase_local_async()
+                for r in range(1, world):
+                    mine = np.flatnonzero(area_rank == r)
+                    lo, hi = int(off[mine[0]]), int(off[mine[-1] + 1])
+                    engines[0].exchange[lo:hi].copy_(engines[r].exchange[lo:hi], non_blocking=True)
+                engines[0].phase_boundary_async()
+                for r in range(1, world):
+                    engines[r].delta.copy_(engines[0].delta, non_blocking=True)
+                for e in engines:
+                    e.phase_recover_async()
+                status = torch.stack([e.status for e in engines]).amax(dim=0)      # the MAX all-reduce
+                delta, failed = (float(v) for v in status.cpu())                    # the one host wait
+                assert failed == 0.0
+                iterations = it
+                deltas.append(delta)
+                if delta < cfg.convergence_tol:
+                    break
+        assert iterations == rref.iterations
+        state = engines[0].state.clone()
+        for r in range(1, world):
+            m = engines[r].owned_mask
+            state[:, m] = engines[r].state[:, m]
+        out = state.cpu().numpy()
+        assert np.array_equal(out[0], ref.va) and np.array_equal(out[1], ref.vm)
+    finally:
+        for e in engines:
+            e.close()
+
+
+def test_distributed_estimator_reports_unobservable_area_through_status(G):
+    """Enqueue-only phases cannot raise: the failure flag rides in status[1] and the owning rank's
+    gse_check names the area (reference solver.py:250-251)."""
+    from conftest import build_case
+    from paper_2604_23175_b200.distributed import DistributedEstimator
+    net, ms, part, g = build_case("ieee14_k2")
+    vm_only = G.apply_mask(ms, lambda t, tg: t != G.MeasurementType.VM)   # reference test_solver.py:335-342
+    est = DistributedEstimator(net, vm_only, part)
+    try:
+        with pytest.raises(G.SolverError, match="likely locally unobservable"):
+            est.estimate()
+    finally:
+        est.close()
+
+
 def test_distributed_estimator_single_rank_on_device(G):
     """DistributedEstimator with its product engine (CudaEngine) on one rank == MultiAreaEstimator."""
     from conftest import build_case
