@@ -38,7 +38,7 @@ def build(force=False, verbose=False):
         subprocess.run(cmd, check=True)
         objs.append(obj)
     subprocess.run([nvcc, "-shared", "-o", LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a",
-                    "-lcudart"], check=True)
+                    "-lcudart", "-lpthread"], check=True)
     return LIB
 
 

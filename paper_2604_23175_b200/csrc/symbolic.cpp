@@ -24,11 +24,30 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <thread>
 
 #include "plan.hpp"
 
 namespace gse {
 namespace {
+
+// Plan-time work that splits by area / by item runs on a few host threads (GSE_BUILD_THREADS
+// overrides the count; 1 = serial).  Every piece writes its own output, merged in index order:
+// the program does not depend on the thread count.
+int build_threads() {
+    if (const char* e = getenv("GSE_BUILD_THREADS")) return std::max(1, atoi(e));
+    const unsigned hw = std::thread::hardware_concurrency();
+    return (int)std::min(16u, std::max(1u, hw));
+}
+template <class F>
+void parallel_for(int n, int nthreads, F&& fn) {
+    nthreads = std::min(nthreads, n);
+    if (nthreads <= 1) { for (int i = 0; i < n; ++i) fn(i); return; }
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nthreads; ++t)
+        pool.emplace_back([&, t] { for (int i = t; i < n; i += nthreads) fn(i); });
+    for (auto& th : pool) th.join();
+}
 
 struct AreaSym {
     int ni = 0, nb = 0;
@@ -180,52 +199,107 @@ void build_acc_items(HostProgram& hp) {
     const int64_t target_items = 280;
     int64_t dmax = (n + target_items - 1) / target_items;
     dmax = std::min<int64_t>(std::max<int64_t>((dmax + 255) / 256 * 256, 256), kAccItemDestMax);
-    std::vector<int32_t> stamp((size_t)hp.n_val, -1), local((size_t)hp.n_val, 0), uniq;
     auto pad4 = [](auto& v) { while (v.size() % 4) v.push_back(0); };
-    int64_t d0 = 0;
-    while (d0 < n) {
-        const int item = (int)(hp.acc_items.size() / 8);
-        uniq.clear();
-        int64_t d1 = d0;
-        while (d1 < n && d1 - d0 < dmax) {
-            // distinct values / pairs the next destination would add
-            const size_t before = uniq.size();
-            for (int q = hp.acc_ptr[d1]; q < hp.acc_ptr[d1 + 1]; ++q)
-                for (int32_t v : {hp.acc_a[q], hp.acc_b[q]})
-                    if (stamp[v] != item) { stamp[v] = item; uniq.push_back(v); }
-            if (((int)uniq.size() > kAccStageMax || hp.acc_ptr[d1 + 1] - hp.acc_ptr[d0] > kAccPairMax) && d1 > d0) {
-                for (size_t i = before; i < uniq.size(); ++i) stamp[uniq[i]] = -1;
-                uniq.resize(before);
-                break;
+    // The destination range is cut into kSeg fixed segments (multiples of dmax; the count does not
+    // depend on the machine), each cut greedily into items on its own thread with private scratch;
+    // the pieces are concatenated in segment order.
+    constexpr int kSeg = 8;
+    struct Piece { std::vector<int32_t> items, uniq, lptr; std::vector<uint32_t> pair; int stage_max = 0, pair_max = 0; };
+    const int64_t chunks = (n + dmax - 1) / dmax;
+    const int nseg = (int)std::min<int64_t>(kSeg, chunks);
+    std::vector<Piece> pieces(nseg);
+    int nthreads = build_threads();
+    nthreads = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads, (1024LL << 20) / (8 * std::max<int64_t>(hp.n_val, 1))));
+    nthreads = std::min(nthreads, nseg);
+    std::vector<std::vector<int32_t>> stamps(nthreads), locals(nthreads);
+    auto cut_segment = [&](int sg, std::vector<int32_t>& stamp, std::vector<int32_t>& local) {
+        Piece& P = pieces[sg];
+        const int64_t lo = chunks * sg / nseg * dmax, hi = std::min<int64_t>(n, chunks * (sg + 1) / nseg * dmax);
+        std::vector<int32_t> uniq;
+        int64_t d0 = lo;
+        while (d0 < hi) {
+            const int item = (int)(P.items.size() / 8) + sg * (1 << 24);      // stamp value: unique per (segment, item)
+            uniq.clear();
+            int64_t d1 = d0;
+            while (d1 < hi && d1 - d0 < dmax) {
+                // distinct values / pairs the next destination would add
+                const size_t before = uniq.size();
+                for (int q = hp.acc_ptr[d1]; q < hp.acc_ptr[d1 + 1]; ++q)
+                    for (int32_t v : {hp.acc_a[q], hp.acc_b[q]})
+                        if (stamp[v] != item) { stamp[v] = item; uniq.push_back(v); }
+                if (((int)uniq.size() > kAccStageMax || hp.acc_ptr[d1 + 1] - hp.acc_ptr[d0] > kAccPairMax) && d1 > d0) {
+                    for (size_t i = before; i < uniq.size(); ++i) stamp[uniq[i]] = -1;
+                    uniq.resize(before);
+                    break;
+                }
+                ++d1;
             }
-            ++d1;
+            std::sort(uniq.begin(), uniq.end());
+            for (size_t i = 0; i < uniq.size(); ++i) local[uniq[i]] = (int32_t)i;
+            const int32_t q0 = hp.acc_ptr[d0], np = hp.acc_ptr[d1] - q0;
+            const int32_t pair_off = (int32_t)P.pair.size(), ptr_off = (int32_t)P.lptr.size(), uniq_off = (int32_t)P.uniq.size();
+            for (int q = q0; q < q0 + np; ++q) P.pair.push_back(((uint32_t)local[hp.acc_b[q]] << 16) | (uint32_t)local[hp.acc_a[q]]);
+            pad4(P.pair);
+            for (int64_t dd = d0; dd <= d1; ++dd) P.lptr.push_back(hp.acc_ptr[dd] - q0);
+            // processing order: destinations by decreasing contribution count, so that the threads of a
+            // warp (consecutive ranks) walk lists of similar length
+            {
+                std::vector<int32_t> ord((size_t)(d1 - d0));
+                std::iota(ord.begin(), ord.end(), 0);
+                std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+                    return hp.acc_ptr[d0 + x + 1] - hp.acc_ptr[d0 + x] > hp.acc_ptr[d0 + y + 1] - hp.acc_ptr[d0 + y]; });
+                P.lptr.insert(P.lptr.end(), ord.begin(), ord.end());
+            }
+            pad4(P.lptr);
+            P.uniq.insert(P.uniq.end(), uniq.begin(), uniq.end());
+            pad4(P.uniq);
+            const int32_t rec[8] = {(int32_t)d0, (int32_t)(d1 - d0), uniq_off, (int32_t)uniq.size(), pair_off, np, ptr_off, 0};
+            P.items.insert(P.items.end(), rec, rec + 8);
+            P.stage_max = std::max(P.stage_max, (int)uniq.size());
+            P.pair_max = std::max(P.pair_max, (int)np);
+            d0 = d1;
         }
-        std::sort(uniq.begin(), uniq.end());
-        for (size_t i = 0; i < uniq.size(); ++i) local[uniq[i]] = (int32_t)i;
-        const int32_t q0 = hp.acc_ptr[d0], np = hp.acc_ptr[d1] - q0;
-        const int32_t pair_off = (int32_t)hp.acc_pair.size(), ptr_off = (int32_t)hp.acc_lptr.size(), uniq_off = (int32_t)hp.acc_uniq.size();
-        for (int q = q0; q < q0 + np; ++q) hp.acc_pair.push_back(((uint32_t)local[hp.acc_b[q]] << 16) | (uint32_t)local[hp.acc_a[q]]);
-        pad4(hp.acc_pair);
-        for (int64_t dd = d0; dd <= d1; ++dd) hp.acc_lptr.push_back(hp.acc_ptr[dd] - q0);
-        // processing order: destinations by decreasing contribution count, so that the threads of a
-        // warp (consecutive ranks) walk lists of similar length
-        {
-            std::vector<int32_t> ord((size_t)(d1 - d0));
-            std::iota(ord.begin(), ord.end(), 0);
-            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
-                return hp.acc_ptr[d0 + x + 1] - hp.acc_ptr[d0 + x] > hp.acc_ptr[d0 + y + 1] - hp.acc_ptr[d0 + y]; });
-            hp.acc_lptr.insert(hp.acc_lptr.end(), ord.begin(), ord.end());
-        }
-        pad4(hp.acc_lptr);
-        hp.acc_uniq.insert(hp.acc_uniq.end(), uniq.begin(), uniq.end());
-        pad4(hp.acc_uniq);
-        const int32_t rec[8] = {(int32_t)d0, (int32_t)(d1 - d0), uniq_off, (int32_t)uniq.size(), pair_off, np, ptr_off, 0};
-        hp.acc_items.insert(hp.acc_items.end(), rec, rec + 8);
-        hp.acc_stage_max = std::max(hp.acc_stage_max, (int)uniq.size());
-        hp.acc_pair_max = std::max(hp.acc_pair_max, (int)np);
-        d0 = d1;
+    };
+    const bool dbg_time = getenv("GSE_DEBUG_TIME") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* w) { if (!dbg_time) return; auto now = std::chrono::steady_clock::now(); fprintf(stderr, "    acc items: %-22s %.3f s\n", w, std::chrono::duration<double>(now - t0).count()); t0 = now; };
+    {
+        std::vector<std::thread> pool;
+        auto work = [&](int t) {
+            stamps[t].assign((size_t)hp.n_val, -1); locals[t].assign((size_t)hp.n_val, 0);
+            for (int sg = t; sg < nseg; sg += nthreads) cut_segment(sg, stamps[t], locals[t]);
+        };
+        for (int t = 1; t < nthreads; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
     }
+    lap("segments (threads)");
+    {
+        size_t ni = 0, nu = 0, npr = 0, nl = 0;
+        for (const Piece& P : pieces) { ni += P.items.size(); nu += P.uniq.size(); npr += P.pair.size(); nl += P.lptr.size(); }
+        hp.acc_items.reserve(ni); hp.acc_uniq.reserve(nu); hp.acc_pair.reserve(npr); hp.acc_lptr.reserve(nl);
+    }
+    for (const Piece& P : pieces) {
+        const int32_t uo = (int32_t)hp.acc_uniq.size(), po = (int32_t)hp.acc_pair.size(), lo = (int32_t)hp.acc_lptr.size();
+        for (size_t i = 0; i < P.items.size(); i += 8) {
+            int32_t rec[8]; std::copy(P.items.begin() + i, P.items.begin() + i + 8, rec);
+            rec[2] += uo; rec[4] += po; rec[6] += lo;
+            hp.acc_items.insert(hp.acc_items.end(), rec, rec + 8);
+        }
+        hp.acc_uniq.insert(hp.acc_uniq.end(), P.uniq.begin(), P.uniq.end());
+        hp.acc_pair.insert(hp.acc_pair.end(), P.pair.begin(), P.pair.end());
+        hp.acc_lptr.insert(hp.acc_lptr.end(), P.lptr.begin(), P.lptr.end());
+        hp.acc_stage_max = std::max(hp.acc_stage_max, P.stage_max);
+        hp.acc_pair_max = std::max(hp.acc_pair_max, P.pair_max);
+    }
+    lap("merge");
     if (getenv("GSE_DEBUG_ACC")) {
+        auto fnv = [](const void* p, size_t bytes) { uint64_t h = 1469598103934665603ull; const unsigned char* c = (const unsigned char*)p; for (size_t i = 0; i < bytes; ++i) { h ^= c[i]; h *= 1099511628211ull; } return h; };
+        fprintf(stderr, "acc program checksums: items %016llx pair %016llx lptr %016llx uniq %016llx a %016llx b %016llx ptr %016llx\n",
+                (unsigned long long)fnv(hp.acc_items.data(), hp.acc_items.size() * 4), (unsigned long long)fnv(hp.acc_pair.data(), hp.acc_pair.size() * 4),
+                (unsigned long long)fnv(hp.acc_lptr.data(), hp.acc_lptr.size() * 4), (unsigned long long)fnv(hp.acc_uniq.data(), hp.acc_uniq.size() * 4),
+                (unsigned long long)fnv(hp.acc_a.data(), hp.acc_a.size() * 4), (unsigned long long)fnv(hp.acc_b.data(), hp.acc_b.size() * 4),
+                (unsigned long long)fnv(hp.acc_ptr.data(), hp.acc_ptr.size() * sizeof(hp.acc_ptr[0])));
         int n_items = (int)(hp.acc_items.size() / 8), max_nd = 0, max_np = hp.acc_pair_max; double sum_nu = 0;
         for (int i = 0; i < n_items; ++i) { max_nd = std::max(max_nd, hp.acc_items[8 * i + 1]); sum_nu += hp.acc_items[8 * i + 3]; }
         {   // contribution-list lengths: the longest list of an item bounds its sequential rounds
@@ -432,50 +506,57 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         }
         if (!closure_ok) return "measurement row references a bus outside its area's variable map";
         slot_cursor += (int64_t)A.slot_var.size();
-
+        for (int b : touched) { loc_va[b] = -1; loc_vm[b] = -1; }
         sec(0);
+    }
+
+    // ---- per area, on a few threads: reference-layout patterns and the nested dissection ----
+    // (both read only the area's own template layout and write only the area's own outputs)
+    std::vector<std::vector<std::vector<int>>> nodes_of(K);   // per area: tree nodes, each a list of interior bus indices
+    parallel_for(K, build_threads(), [&](int a) {
+        AreaSym& A = as[a];
+        const int ni = A.ni, nb = A.nb;
+        const int nib = d.im_ptr[a + 1] - d.im_ptr[a];
         // ---- reference-layout CSR patterns of G_ii, G_ib ------------------------------
         // (per interior variable: the sorted, de-duplicated columns its rows reach)
         if (opt.ext_pattern) {      // generic matrix plan: the caller supplies the patterns
             hp.ii_ptr[a] = opt.ext_ii_ptr; hp.ii_idx[a] = opt.ext_ii_idx;
             hp.ib_ptr[a] = opt.ext_ib_ptr; hp.ib_idx[a] = opt.ext_ib_idx;
         } else {
-            std::vector<std::vector<int>> cols_ii(ni), cols_ib(ni);
-            for (size_t k = 0; k < A.rows.size(); ++k)
-                for (int x = A.slot_ptr[k]; x < A.slot_ptr[k + 1]; ++x) {
-                    int va = A.slot_var[x]; if (va >= ni) continue;
-                    for (int y = A.slot_ptr[k]; y < A.slot_ptr[k + 1]; ++y) {
-                        int vb = A.slot_var[y];
-                        if (vb < ni) cols_ii[va].push_back(vb); else cols_ib[va].push_back(vb - ni);
-                    }
-                }
+            // rows of every interior variable (CSR), then per variable one stamped sweep over the
+            // slots of its rows: each distinct column is collected once, and only those are sorted
+            std::vector<int> vr_ptr(ni + 1, 0), vr_row;
+            for (int x : A.slot_var) if (x < ni) vr_ptr[x + 1]++;
+            for (int v = 0; v < ni; ++v) vr_ptr[v + 1] += vr_ptr[v];
+            vr_row.resize(vr_ptr[ni]);
+            {
+                std::vector<int> cur(vr_ptr.begin(), vr_ptr.end() - 1);
+                for (size_t k = 0; k < A.rows.size(); ++k)
+                    for (int x = A.slot_ptr[k]; x < A.slot_ptr[k + 1]; ++x)
+                        if (A.slot_var[x] < ni) vr_row[cur[A.slot_var[x]]++] = (int)k;
+            }
+            std::vector<int> mark(ni + nb, -1), cols;
             hp.ii_ptr[a].assign(ni + 1, 0); hp.ib_ptr[a].assign(ni + 1, 0);
             for (int v = 0; v < ni; ++v) {
-                for (auto* c : {&cols_ii[v], &cols_ib[v]}) { std::sort(c->begin(), c->end()); c->erase(std::unique(c->begin(), c->end()), c->end()); }
-                hp.ii_ptr[a][v + 1] = hp.ii_ptr[a][v] + (int32_t)cols_ii[v].size();
-                hp.ib_ptr[a][v + 1] = hp.ib_ptr[a][v] + (int32_t)cols_ib[v].size();
-                hp.ii_idx[a].insert(hp.ii_idx[a].end(), cols_ii[v].begin(), cols_ii[v].end());
-                hp.ib_idx[a].insert(hp.ib_idx[a].end(), cols_ib[v].begin(), cols_ib[v].end());
+                cols.clear();
+                for (int q = vr_ptr[v]; q < vr_ptr[v + 1]; ++q) {
+                    const int k = vr_row[q];
+                    for (int y = A.slot_ptr[k]; y < A.slot_ptr[k + 1]; ++y) {
+                        const int vb = A.slot_var[y];
+                        if (mark[vb] != v) { mark[vb] = v; cols.push_back(vb); }
+                    }
+                }
+                std::sort(cols.begin(), cols.end());
+                const auto mid = std::lower_bound(cols.begin(), cols.end(), ni);
+                hp.ii_idx[a].insert(hp.ii_idx[a].end(), cols.begin(), mid);
+                for (auto it = mid; it != cols.end(); ++it) hp.ib_idx[a].push_back(*it - ni);
+                hp.ii_ptr[a][v + 1] = (int32_t)hp.ii_idx[a].size();
+                hp.ib_ptr[a][v + 1] = (int32_t)hp.ib_idx[a].size();
             }
         }
-        // ref value layout of the area: [data_ii | data_ib | g_bb | b_i | b_b]
-        hp.ref_off[a + 1] = hp.ref_off[a] + (int64_t)hp.ii_idx[a].size() + (int64_t)hp.ib_idx[a].size() + (int64_t)nb * nb + ni + nb;
-        nnz_total += (double)hp.ii_idx[a].size() + (double)hp.ib_idx[a].size() + (double)nb * nb; rhs_total += ni + nb;
-        // template layout kept for the (lazily built) reference-layout program
-        hp.tmpl_rows.push_back(A.rows); hp.tmpl_slot_ptr.push_back(A.slot_ptr); hp.tmpl_slot_var.push_back(A.slot_var);
-        hp.tmpl_slot_base.push_back(A.slot_base);
-
-        sec(1);
-        // ---- ordering of the interior --------------------------------------------------
-        A.epos.assign(ni, -1); A.order.assign(ni, -1);
-        int ep = 0;
-        A.first_front = (int)hp.fronts.size();
-        A.front_of_pos.assign(ni, -1);
-        if (!hp.owned[a]) {
-            for (int v = 0; v < ni; ++v) { A.epos[v] = v; A.order[v] = v; }
-            ep = ni;
-        } else {
-        std::vector<std::vector<int>> nodes;   // each: interior bus indices, in elimination order
+        // ---- ordering of the interior: nested dissection on the bus graph ----------------
+        std::vector<std::vector<int>>& nodes = nodes_of[a];   // each: interior bus indices, in elimination order
+        if (!hp.owned[a]) return;
         if (opt.dense || ni <= PMAX) {
             std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
             if (nib) nodes.push_back(all);
@@ -497,6 +578,33 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
             nd_recurse(g, all, std::max(1, opt.leaf_buses), nodes);
         }
+    });
+    sec(1);
+
+    for (int a = 0; a < K; ++a) {
+        AreaSym& A = as[a];
+        const int ni = A.ni, nb = A.nb;
+        const int n_ia = d.ia_ptr[a + 1] - d.ia_ptr[a];
+        const int n_ba = d.ba_ptr[a + 1] - d.ba_ptr[a];
+        const int nib = d.im_ptr[a + 1] - d.im_ptr[a];
+        (void)n_ia; (void)n_ba; (void)nib;
+        // ref value layout of the area: [data_ii | data_ib | g_bb | b_i | b_b]
+        hp.ref_off[a + 1] = hp.ref_off[a] + (int64_t)hp.ii_idx[a].size() + (int64_t)hp.ib_idx[a].size() + (int64_t)nb * nb + ni + nb;
+        nnz_total += (double)hp.ii_idx[a].size() + (double)hp.ib_idx[a].size() + (double)nb * nb; rhs_total += ni + nb;
+        // template layout kept for the (lazily built) reference-layout program
+        hp.tmpl_rows.push_back(A.rows); hp.tmpl_slot_ptr.push_back(A.slot_ptr); hp.tmpl_slot_var.push_back(A.slot_var);
+        hp.tmpl_slot_base.push_back(A.slot_base);
+
+        // ---- fronts of the interior, in the order found above ----------------------------
+        A.epos.assign(ni, -1); A.order.assign(ni, -1);
+        int ep = 0;
+        A.first_front = (int)hp.fronts.size();
+        A.front_of_pos.assign(ni, -1);
+        if (!hp.owned[a]) {
+            for (int v = 0; v < ni; ++v) { A.epos[v] = v; A.order[v] = v; }
+            ep = ni;
+        } else {
+        std::vector<std::vector<int>>& nodes = nodes_of[a];
         // nodes -> fronts of at most PMAX pivots
         for (auto& node : nodes) {
             std::vector<int> vars;
@@ -688,11 +796,10 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         } else {
             choose_chunks(hp.fronts[root_id], opt.tile_rows);
         }
-        for (int b : touched) { loc_va[b] = -1; loc_vm[b] = -1; }
         sec(4);
     }
     hp.n_slots = slot_cursor;
-    if (dbg_time) fprintf(stderr, "  plan build (areas): slots/units %.3f  ref patterns+program %.3f  ordering %.3f  lower pattern %.3f  fronts+entries %.3f\n",
+    if (dbg_time) fprintf(stderr, "  plan build (areas): slots/units %.3f  patterns+dissection (threads) %.3f  fronts %.3f  lower pattern %.3f  update sets+entries %.3f\n",
                           t_sec[0], t_sec[1], t_sec[2], t_sec[3], t_sec[4]);
 
     lap("areas: slots, patterns, fronts");
@@ -920,10 +1027,14 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     if (hp.n_val > 2147483647LL) return "value array exceeds int32 indexing";
     auto val_index = [&](int32_t b) { return b >= 0 ? (int32_t)(2 * b + 1) : (int32_t)(2 * hp.n_slots + (-b - 1)); };
     {
-        std::vector<int64_t> dest; std::vector<int32_t> pa, pb;
-        for (int a = 0; a < K; ++a) {
-            if (!hp.owned[a]) continue;
-            AreaSym& A = as[a];
+        // pairs of every area on its own thread (read-only plan data, private output), in area order below
+        struct AreaPairs { std::vector<int64_t> dest; std::vector<int32_t> pa, pb; bool bad = false; int64_t lo = INT64_MAX, hi = -1; };
+        std::vector<AreaPairs> ap(K);
+        const int nthreads = build_threads();
+        parallel_for(K, nthreads, [&](int a) {
+            if (!hp.owned[a]) return;
+            const AreaSym& A = as[a];
+            AreaPairs& out = ap[a];
             const int ni = A.ni, nloc = A.ni + A.nb;
             auto lp = [&](int v) { return v < ni ? A.epos[v] : ni + hp.area_bpos[a][v - ni]; };
             auto find = [&](int c, int r) -> int64_t {
@@ -931,32 +1042,57 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 auto it = std::lower_bound(b, e, r);
                 return (it == e || *it != r) ? -1 : A.col_dest[it - A.col_row.begin()];
             };
+            size_t np = 0;
+            for (size_t k = 0; k < A.rows.size(); ++k) { const size_t sl = A.slot_ptr[k + 1] - A.slot_ptr[k]; np += sl * (sl + 1) / 2 + sl; }
+            out.dest.reserve(np); out.pa.reserve(np); out.pb.reserve(np);
+            std::vector<int> pos;
             for (size_t k = 0; k < A.rows.size(); ++k) {
                 int s0 = A.slot_ptr[k], s1 = A.slot_ptr[k + 1];
+                pos.resize(s1 - s0);
+                for (int x = s0; x < s1; ++x) pos[x - s0] = lp(A.slot_var[x]);
                 for (int x = s0; x < s1; ++x) {
-                    int ra_ = lp(A.slot_var[x]);
+                    int ra_ = pos[x - s0];
                     for (int y = s0; y < s1; ++y) {
-                        int cb = lp(A.slot_var[y]);
+                        int cb = pos[y - s0];
                         if (ra_ < cb) continue;
                         int64_t dd = find(cb, ra_);
-                        if (dd < 0) return "internal: pair without a destination";
-                        dest.push_back(dd); pa.push_back((int32_t)(A.slot_base + x)); pb.push_back((int32_t)(A.slot_base + y));
+                        if (dd < 0) { out.bad = true; return; }
+                        out.dest.push_back(dd); out.pa.push_back((int32_t)(A.slot_base + x)); out.pb.push_back((int32_t)(A.slot_base + y));
                     }
                 }
                 for (int x = s0; x < s1; ++x) {
-                    int64_t dd = find(lp(A.slot_var[x]), nloc);
-                    dest.push_back(dd); pa.push_back((int32_t)(A.slot_base + x)); pb.push_back(-(A.rows[k] + 1));
+                    int64_t dd = find(pos[x - s0], nloc);
+                    if (dd < 0) { out.bad = true; return; }
+                    out.dest.push_back(dd); out.pa.push_back((int32_t)(A.slot_base + x)); out.pb.push_back(-(A.rows[k] + 1));
                 }
             }
-        }
-        hp.n_pairs = (int64_t)dest.size();
-        // stable counting sort by destination keeps ascending-row order per slot
+            for (int64_t dd : out.dest) { out.lo = std::min(out.lo, dd); out.hi = std::max(out.hi, dd); }
+        });
+        lap("  acc program: pairs per area (threads)");
+        int64_t n_pairs = 0;
+        for (int a = 0; a < K; ++a) { if (ap[a].bad) return "internal: pair without a destination"; n_pairs += (int64_t)ap[a].dest.size(); }
+        if (n_pairs > 2147483647LL) return "contribution program exceeds int32 indexing";
+        hp.n_pairs = n_pairs;
+        // stable counting sort by destination keeps ascending-row order per slot (areas in order)
         hp.acc_ptr.assign(hp.n_gval + 1, 0);
-        for (int64_t dd : dest) hp.acc_ptr[dd + 1]++;
+        for (int a = 0; a < K; ++a) for (int64_t dd : ap[a].dest) hp.acc_ptr[dd + 1]++;
         for (int64_t i = 0; i < hp.n_gval; ++i) hp.acc_ptr[i + 1] += hp.acc_ptr[i];
-        hp.acc_a.resize(dest.size()); hp.acc_b.resize(dest.size());
+        hp.acc_a.resize((size_t)n_pairs); hp.acc_b.resize((size_t)n_pairs);
         std::vector<int32_t> cur(hp.acc_ptr.begin(), hp.acc_ptr.end() - 1);
-        for (size_t i = 0; i < dest.size(); ++i) { int32_t q = cur[dest[i]]++; hp.acc_a[q] = 2 * pa[i]; hp.acc_b[q] = val_index(pb[i]); }
+        // the destination ranges of distinct areas are disjoint (every entry lives in a front of its
+        // area), so the scatter of an area touches only its own cursors; checked, serial otherwise
+        lap("  acc program: count + prefix");
+        bool disjoint = true;
+        {
+            std::vector<std::pair<int64_t, int64_t>> rg;
+            for (int a = 0; a < K; ++a) if (ap[a].hi >= 0) rg.push_back({ap[a].lo, ap[a].hi});
+            std::sort(rg.begin(), rg.end());
+            for (size_t i = 1; i < rg.size(); ++i) if (rg[i].first <= rg[i - 1].second) disjoint = false;
+        }
+        parallel_for(K, disjoint ? nthreads : 1, [&](int a) {
+            const AreaPairs& in = ap[a];
+            for (size_t i = 0; i < in.dest.size(); ++i) { int32_t q = cur[in.dest[i]]++; hp.acc_a[q] = 2 * in.pa[i]; hp.acc_b[q] = val_index(in.pb[i]); }
+        });
     }
     lap("accumulation program (sort)");
     build_acc_items(hp);

@@ -19,7 +19,7 @@ def _lib():
                 os.path.join(_ROOT, "paper_2604_23175_b200", "csrc", "symbolic.cpp")]
         deps = srcs + [os.path.join(_ROOT, "paper_2604_23175_b200", "csrc", "plan.hpp")]
         if not os.path.exists(_SO) or any(os.path.getmtime(s) > os.path.getmtime(_SO) for s in deps):
-            subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", "-ffp-contract=off", "-shared", "-fPIC",
+            subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", "-ffp-contract=off", "-shared", "-fPIC", "-pthread",
                             "-o", _SO, *srcs], check=True)
         L = C.CDLL(_SO)
         L.hostsim_create.restype = C.c_void_p

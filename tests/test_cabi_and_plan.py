@@ -99,3 +99,22 @@ def test_reference_layout_program_reproduces_oracle_blocks():
         flat = np.concatenate([b["data_ii"], b["data_ib"], b["g_bb"].ravel(), b["b_i"], b["b_b"]])
         mine = vals[off[a]:off[a + 1]]
         assert np.max(np.abs(mine - flat) / (1 + np.abs(flat))) < 5e-13
+
+
+def test_plan_build_does_not_depend_on_the_host_thread_count(monkeypatch):
+    """symbolic.cpp runs the per-area / per-segment parts of the analysis on a few host threads;
+    the program (and hence every bit of the solve) must be the same for any thread count."""
+    from hostsim import HostSim
+    net, ms, part, g = build_case("pegase2869_k8")
+    bord, maps = G.build_variable_maps(net, part)
+    outs = []
+    for threads in ("1", "3", "16"):
+        monkeypatch.setenv("GSE_BUILD_THREADS", threads)
+        sim = HostSim(net, ms, part, bord, maps)
+        va, vm, it, conv, deltas = sim.solve()
+        vals, off = sim.ref_blocks()
+        outs.append((sim.stats(), va, vm, it, np.array(deltas), vals))
+    for st, va, vm, it, deltas, vals in outs[1:]:
+        assert st == outs[0][0] and it == outs[0][3]
+        assert np.array_equal(va, outs[0][1]) and np.array_equal(vm, outs[0][2])
+        assert np.array_equal(deltas, outs[0][4]) and np.array_equal(vals, outs[0][5])
