@@ -8,6 +8,10 @@
 
 namespace gse {
 
+#ifndef GSE_PANEL_QUIET
+#define GSE_PANEL_QUIET 1
+#endif
+
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
@@ -136,7 +140,7 @@ struct __align__(16) FrontScratch {
     TaskRec hdr;
     ChildRec crec[kChildBatch];
     int inv[kGatherBatch][kInvRows];
-    double ld8[48];            // published 8x8 diagonal factor (36) + reciprocal pivots (8)
+    double ld8[2][48];         // published 8x8 diagonal factor (36) + reciprocal pivots (8), double-buffered
     double rinv[64];           // reciprocal pivots of the whole front (stored for the backward pass)
     double colbuf[2][16];      // two columns of the 8x8 pivot block being eliminated (double-buffered)
     int nready;                // children of the current gather batch that are complete
@@ -177,7 +181,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     const TaskRec& hdr = S.hdr;
     ChildRec* crec = S.crec;
     int (*s_inv)[kInvRows] = S.inv;
-    double* s_ld = S.ld8;
+    double* s_ld = &S.ld8[0][0];
     double* s_rinv = S.rinv;
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
@@ -317,24 +321,52 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     __syncthreads();
     GSE_TICK(3);
 
-    // ---- blocked panel factorisation (block = 8 columns) ---------------------------------------
-    // Per block: warp 0 brings the 8x8 diagonal tile up to date (rank-8 share of the previous block
-    // column; see diag_rank8), eliminates it across its lanes and publishes it while the other warps
-    // update the remaining row tiles on the tensor pipe (left-looking, look-ahead); then every row
-    // solves against the published block (independent FMAs).  Two barriers per 8 pivots.
+    // ---- blocked panel factorisation (block = 8 columns), software-pipelined -------------------
+    // Warp 0 owns the serial chain: per block k it brings the 8x8 diagonal tile up to date (rank-8 share of
+    // the previous block column), eliminates it across its lanes, publishes the factor, solves the NEXT
+    // pivot tile's eight rows against it -- and goes straight on to block k + 1.  The other warps trail one
+    // step behind: they solve the remaining rows against block k, then run the right-looking diagonal
+    // updates and the left-looking DMMA update of block column k + 1 while warp 0 already eliminates
+    // block k + 1.  Per block: one CTA barrier (factor published / column k + 1 current) and one named
+    // barrier that warp 0 only arrives at (its tile solve is done) -- the chain never waits for the bulk
+    // row solves.  The published factor is double-buffered for the same reason.
     if (HAS_PIVOTS && pp) {
         const int R = rp + ri + rj;                 // padded rows: [pivots | chunk I | chunk J]
         const int ntile = R >> 3;
         long long pc[7] = {0, 0, 0, 0, 0, 0, 0}, pt = tb ? clock64() : 0;   // debug: cycles per panel sub-phase (thread 0)
 #define GSE_PC(k) do { if (tb) { const long long now = clock64(); pc[k] += now - pt; pt = now; } } while (0)
+        // one row of the panel against the published 8x8 factor (16-byte accesses: the row stride maps eight
+        // rows onto four bank groups, so 8-byte accesses of one row per thread would be 8-way bank conflicted)
+        auto solve_row = [&](int row, int kb, const double* sl) {
+            double y[8];
+            double2* my2 = reinterpret_cast<double2*>(pan + (size_t)row * ld + kb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { const double2 t2 = my2[j]; y[2 * j] = t2.x; y[2 * j + 1] = t2.y; }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                y[k] *= sl[36 + k];
+#pragma unroll
+                for (int j = k + 1; j < 8; ++j) y[j] = fma(-y[k], sl[j * (j + 1) / 2 + k], y[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) my2[j] = make_double2(y[2 * j], y[2 * j + 1]);
+        };
+        // helper warps of the tensor-pipe work: the warps that share warp 0's scheduler (and with it its FP64 /
+        // tensor issue port: an m8n8k4 DMMA holds the port for ~16 cycles, profiles/r01_microbench_b200.txt)
+        // stay off the pipe, so the serial chain is not queued behind their MMAs
+        const bool helper = warp != 0 && (GSE_PANEL_QUIET == 0 || (warp & 3) != 0);
+        const int nw = GSE_PANEL_QUIET ? nwarps - (nwarps >> 2) : nwarps - 1;
+        const int wi = GSE_PANEL_QUIET ? warp - 1 - (warp >> 2) : warp - 1;
         for (int kb = 0; kb < rp; kb += 8) {
             const int t0 = kb >> 3;
+            double* sl = s_ld + (t0 & 1) * 48;
             if (warp == 0) {
                 // The 8x8 diagonal block lives in the MMA accumulator layout: lane (r = lane / 4, c = lane % 4)
                 // holds D[r][2c], D[r][2c + 1].  It is loaded with one 16-byte read, takes the last block
                 // column's share straight in registers, and is eliminated by all 32 lanes together.
                 const int r = lane >> 2, c2 = 2 * (lane & 3);
-                const double2 dt = *reinterpret_cast<const double2*>(pan + (size_t)(kb + r) * ld + kb + c2);
+                double2* dptr = reinterpret_cast<double2*>(pan + (size_t)(kb + r) * ld + kb + c2);
+                const double2 dt = *dptr;
                 double x0 = dt.x, x1 = dt.y;
                 if (kb) {
                     const double* ap = pan + (size_t)(kb + r) * ld + (kb - 8) + (lane & 3);
@@ -344,7 +376,6 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                     x0 -= c0 + e0; x1 -= c1 + e1;
                 }
                 GSE_PC(0);
-                GSE_PC(1);
                 // Division-free elimination: step k cross-multiplies
                 //     a_ij <- (p_k a_ij - a_ik a_jk) * 2^-e,   p_k = a_kk,   2^e ~ p_k  (exact scaling),
                 // one multiply-add per lane, so the serial chain per pivot is shuffle -> multiply -> FMA
@@ -405,68 +436,60 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                 x0 *= __shfl_sync(0xffffffffu, q, c2);
                 x1 *= __shfl_sync(0xffffffffu, q, c2 + 1);
                 GSE_PC(2);
-                // publish the factor of the block (packed lower triangle) and the reciprocal pivots
-                if (c2 <= r) s_ld[r * (r + 1) / 2 + c2] = x0;
-                if (c2 + 1 <= r) s_ld[r * (r + 1) / 2 + c2 + 1] = x1;
-                if (lane < 8) { s_ld[36 + lane] = rk; s_rinv[kb + lane] = rk; }      // (padded pivots: reciprocal 1)
+                // publish the factor of the block (packed lower triangle, reciprocal pivots) for the row solves
+                // and put it in its place in the panel (zeros above the diagonal)
+                if (c2 <= r) sl[r * (r + 1) / 2 + c2] = x0;
+                if (c2 + 1 <= r) sl[r * (r + 1) / 2 + c2 + 1] = x1;
+                *dptr = make_double2(c2 <= r ? x0 : 0.0, c2 + 1 <= r ? x1 : 0.0);
+                if (lane < 8) { sl[36 + lane] = rk; s_rinv[kb + lane] = rk; }      // (padded pivots: reciprocal 1)
                 if (lane == 0 && badk >= 0 && kb + badk < p) atomicMin(err, ((unsigned long long)f << 32) | (unsigned long long)(kb + badk));
-            } else if (kb) {
-                // later pivot tiles: their diagonal blocks take the last block column's share now
-                const int nw = nwarps - 1;
-                for (int t = t0 + warp; t < (rp >> 3); t += nw) diag_rank8(pan, ld, t, kb - 8, lane);
-                // rows below the diagonal tile: block column kb -= A[rows, 0:kb] * A[kb:kb+8, 0:kb]^T
-                for (int tb2 = t0 + 1 + (warp - 1); tb2 < ntile; tb2 += 2 * nw) {
-                    const int ta = tb2, tc2 = tb2 + nw;
-                    const bool two = tc2 < ntile;
-                    const double* a0p = pan + (size_t)(ta * 8 + (lane >> 2)) * ld + (lane & 3);
-                    const double* a1p = pan + (size_t)((two ? tc2 : ta) * 8 + (lane >> 2)) * ld + (lane & 3);
-                    const double* bp = pan + (size_t)(kb + (lane >> 2)) * ld + (lane & 3);
-                    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
-#pragma unroll 2
-                    for (int kk = 0; kk < kb; kk += 4) {
-                        const double b = bp[kk];
-                        dmma_m8n8k4(c00, c01, a0p[kk], b);
-                        dmma_m8n8k4(c10, c11, a1p[kk], b);
-                    }
-                    double* o0 = pan + (size_t)(ta * 8 + (lane >> 2)) * ld + kb + 2 * (lane & 3);
-                    o0[0] -= c00; o0[1] -= c01;
-                    if (two) {
-                        double* o1 = pan + (size_t)(tc2 * 8 + (lane >> 2)) * ld + kb + 2 * (lane & 3);
-                        o1[0] -= c10; o1[1] -= c11;
-                    }
-                }
+                GSE_PC(3);
             }
-            GSE_PC(3);
+            // the factor of block k is published; block column k of every row below it is current
+            // (left-looking share applied by the helper warps during the previous step)
             __syncthreads();
             GSE_PC(4);
-            // every row at or below the block solves against the published 8x8 factor
-            if (tid >= kb && tid < R) {
-                double* myrow = pan + (size_t)tid * ld + kb;
-                if (tid < kb + 8) {
-                    const int i = tid - kb;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) myrow[j] = j <= i ? s_ld[i * (i + 1) / 2 + j] : 0.0;
-                } else {
-                    // (16-byte accesses: the row stride maps eight rows onto four bank groups, so 8-byte
-                    // accesses of one row per thread would be 8-way bank conflicted)
-                    double y[8];
-                    double2* my2 = reinterpret_cast<double2*>(myrow);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) { const double2 t2 = my2[j]; y[2 * j] = t2.x; y[2 * j + 1] = t2.y; }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        y[k] *= s_ld[36 + k];
-#pragma unroll
-                        for (int j = k + 1; j < 8; ++j) y[j] = fma(-y[k], s_ld[j * (j + 1) / 2 + k], y[j]);
+            if (warp == 0) {
+                // the next pivot tile (or, after the last block, the first eight update rows)
+                if (lane < 8 && kb + 8 + lane < R) solve_row(kb + 8 + lane, kb, sl);
+                __syncwarp();
+                __threadfence_block();
+                asm volatile("bar.arrive 1, %0;" :: "r"(nth) : "memory");
+                GSE_PC(5);
+            } else {
+                for (int row = kb + 16 + (tid - 32); row < R; row += nth - 32) solve_row(row, kb, sl);
+                asm volatile("bar.sync 1, %0;" :: "r"(nth) : "memory");      // + warp 0's tile
+                if (helper && kb + 8 < rp) {
+                    // later pivot tiles: their diagonal blocks take this block column's share now (tile k + 1
+                    // takes it in warp 0's registers)
+                    for (int t = t0 + 2 + wi; t < (rp >> 3); t += nw) diag_rank8(pan, ld, t, kb, lane);
+                    // rows below the next diagonal tile: block column kn -= A[rows, 0:kn] * A[kn:kn+8, 0:kn]^T
+                    const int kn = kb + 8;
+                    for (int tb2 = t0 + 2 + wi; tb2 < ntile; tb2 += 2 * nw) {
+                        const int ta = tb2, tc2 = tb2 + nw;
+                        const bool two = tc2 < ntile;
+                        const double* a0p = pan + (size_t)(ta * 8 + (lane >> 2)) * ld + (lane & 3);
+                        const double* a1p = pan + (size_t)((two ? tc2 : ta) * 8 + (lane >> 2)) * ld + (lane & 3);
+                        const double* bp = pan + (size_t)(kn + (lane >> 2)) * ld + (lane & 3);
+                        double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll 2
+                        for (int kk = 0; kk < kn; kk += 4) {
+                            const double b = bp[kk];
+                            dmma_m8n8k4(c00, c01, a0p[kk], b);
+                            dmma_m8n8k4(c10, c11, a1p[kk], b);
+                        }
+                        double* o0 = pan + (size_t)(ta * 8 + (lane >> 2)) * ld + kn + 2 * (lane & 3);
+                        o0[0] -= c00; o0[1] -= c01;
+                        if (two) {
+                            double* o1 = pan + (size_t)(tc2 * 8 + (lane >> 2)) * ld + kn + 2 * (lane & 3);
+                            o1[0] -= c10; o1[1] -= c11;
+                        }
                     }
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) my2[j] = make_double2(y[2 * j], y[2 * j + 1]);
                 }
             }
-            GSE_PC(5);
-            __syncthreads();
-            GSE_PC(6);
         }
+        __syncthreads();
+        GSE_PC(6);
 #undef GSE_PC
         if (tb && tid == 0) for (int k = 0; k < 7; ++k) tb[8 + k] = pc[k];
     }

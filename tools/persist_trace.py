@@ -89,7 +89,7 @@ for it in range(rep.iterations):
                 pw = b[i, 5] if kind == 2 else st[4]
                 print(f"     {f:5d} k{kind} {ci},{cj} | {(st[1]-st[0])/1e3:5.1f} {(st[2]-st[1])/1e3:5.1f} {(st[7]-st[2])/1e3:5.1f} [{(cw-st[7])/1e3:5.1f}] "
                       f"{(st[3]-cw)/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} [{(pw-st[4])/1e3:5.1f}] {(st[5]-pw)/1e3:5.1f} {(st[6]-st[5])/1e3:5.1f} {(b[i,3]-st[6])/1e3:5.1f}"
-                      + ("   panel cyc: diagupd %d lds %d factor %d publish %d sync %d rowsolve %d sync %d" % tuple(b[i, 16:23]) if kind != 2 else ""))
+                      + ("   panel cyc: diagupd %d - %d factor %d publish %d barrier %d tile solve %d tail %d" % tuple(b[i, 16:23]) if kind != 2 else ""))
         b = blk[bounds[3]:bounds[4]]
         step = max(1, len(b) // 25)
         print("   backward wavefront:")
