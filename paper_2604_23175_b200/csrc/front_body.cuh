@@ -453,11 +453,11 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
                 // the next pivot tile (or, after the last block, the first eight update rows)
                 if (lane < 8 && kb + 8 + lane < R) solve_row(kb + 8 + lane, kb, sl);
                 __syncwarp();
-                __threadfence_block();
                 asm volatile("bar.arrive 1, %0;" :: "r"(nth) : "memory");
                 GSE_PC(5);
             } else {
-                for (int row = kb + 16 + (tid - 32); row < R; row += nth - 32) solve_row(row, kb, sl);
+                // the bulk rows, on the helper warps only (warp 0's scheduler stays free for its tile solve)
+                if (helper) for (int row = kb + 16 + wi * 32 + lane; row < R; row += nw * 32) solve_row(row, kb, sl);
                 asm volatile("bar.sync 1, %0;" :: "r"(nth) : "memory");      // + warp 0's tile
                 if (helper && kb + 8 < rp) {
                     // later pivot tiles: their diagonal blocks take this block column's share now (tile k + 1
@@ -718,11 +718,16 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
         double t0 = tv[tid], t1 = tv[tid + 32];
         const double* di = ft.dinv + tk.dinv_off;
         const double r0 = tid < p ? ldc(di + tid) : 0.0, r1 = tid + 32 < p ? ldc(di + tid + 32) : 0.0;
+        // the lanes carry s_i = t_i / L_ii, so the serial chain per pivot is one shuffle and one FMA:
+        // x_c = s_c, then s_i -= (L_ci / L_ii) x_c with the scaled factor entry formed off the chain
+        t0 *= r0; t1 *= r1;
+#pragma unroll 4
         for (int c = p - 1; c >= 0; --c) {
-            const double xc = __shfl_sync(0xffffffffu, c < 32 ? t0 * r0 : t1 * r1, c & 31);
-            if (tid == (c & 31)) { if (c < 32) t0 = xc; else t1 = xc; }
-            if (tid < c) t0 = fma(-l11[c * p + tid], xc, t0);
-            if (tid + 32 < c) t1 = fma(-l11[c * p + tid + 32], xc, t1);
+            const double lc0 = tid < c ? l11[c * p + tid] * r0 : 0.0;
+            const double lc1 = tid + 32 < c ? l11[c * p + tid + 32] * r1 : 0.0;
+            const double xc = __shfl_sync(0xffffffffu, c < 32 ? t0 : t1, c & 31);
+            t0 = fma(-lc0, xc, t0);
+            t1 = fma(-lc1, xc, t1);
         }
         if (tid < p) xsol[rows[tid]] = t0;
         if (tid + 32 < p) xsol[rows[tid + 32]] = t1;
