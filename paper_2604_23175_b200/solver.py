@@ -287,9 +287,64 @@ def solve_centralized(net, ms: MeasurementSet, config: SolverConfig = None, on_i
     """Single-area GN on the device: the k = 1 path of the same plan (one area,
     empty boundary), i.e. the paper's "centralized GPU" baseline."""
     t_start = time.perf_counter()
+    if config is not None and config.iterative_refinement:
+        return _solve_centralized_refined(net, ms, config, on_iteration, t_start)
     est = MultiAreaEstimator(net, ms, partition_network(net, 1), config=config,
                              method="centralized")
     try:
         return est.estimate(on_iteration=on_iteration, t_start=t_start)
     finally:
         est.close()
+
+
+def _solve_centralized_refined(net, ms, cfg, on_iteration, t_start):
+    """``iterative_refinement=True`` (read only by ``solve_centralized`` in the reference,
+    solver.py:181-183): the reference's own loop on the device components -- ``fused_accumulate``
+    for the gain matrix and right-hand side, ``numeric_refactor`` and ``cache.solve(b,
+    refine_with=G)`` (one residual correction, linalg.py:385-392) on the device factorisation."""
+    from .assembly import build_patterns, fused_accumulate
+    from .linalg import numeric_refactor, symbolic_analyze
+    timings = {p: 0.0 for p in PHASES}
+    part = partition_network(net, 1)
+    _, maps = build_variable_maps(net, part)
+    vmap = maps[0]
+    pattern = build_patterns(vmap, ms)
+    cache = symbolic_analyze(pattern.gii_pattern(), dense_threshold=cfg.effective_dense_threshold,
+                             context="gain matrix")
+    try:
+        state = StateVector.flat_start(net)
+        empty = np.zeros(0)
+        iterations, converged = 0, False
+        for it in range(1, cfg.max_outer_iterations + 1):
+            t0 = time.perf_counter()
+            x_i = vmap.gather_interior(state.va, state.vm)
+            blocks = fused_accumulate(vmap, ms, x_i, empty, pattern=pattern)
+            t1 = time.perf_counter()
+            try:
+                numeric_refactor(cache, blocks.g_ii)
+            except NotPositiveDefiniteError as exc:
+                raise SolverError(
+                    f"gain matrix {exc}: system unobservable or ill-conditioned") from exc
+            t2 = time.perf_counter()
+            delta = cache.solve(blocks.b_i, refine_with=blocks.g_ii)
+            vmap.apply_interior_delta(state.va, state.vm, delta)
+            t3 = time.perf_counter()
+            timings["assembly"] += t1 - t0
+            timings["local_condense"] += t2 - t1
+            timings["recovery"] += t3 - t2
+            iterations = it
+            delta_inf = float(np.max(np.abs(delta))) if delta.size else 0.0
+            if on_iteration is not None:
+                on_iteration(it, state.copy(), delta_inf)
+            if delta_inf < cfg.convergence_tol:
+                converged = True
+                break
+        j = objective(ms, state)
+    finally:
+        cache.close()
+        pattern.plan.close()
+    timings["total"] = time.perf_counter() - t_start
+    report = SolveReport(method="centralized", iterations=iterations, converged=converged,
+                         objective=float(j), weighted_residual_norm=float(np.sqrt(j)), n_gamma=0,
+                         timings=timings)
+    return state, report

@@ -142,6 +142,22 @@ def main(which):
                          cfg=R.SolverConfig(inner_gn_steps=3),
                          recipe={"gen": "random_network(120, 3, 0.3)", "meas_seed": 2, "k": 4,
                                  "part_seed": 1, "inner": 3})
+    if "refined" in which:
+        # solve_centralized with iterative_refinement=True (reference solver.py:181-183, linalg.py:385-392)
+        for case, tag in (("ieee14.m", "ieee14"), ("ieee118.m", "ieee118")):
+            net = R.load_case(f"/root/reference/pkg/cases/{case}")
+            ms = R.generate_measurements(net, R.MeasurementConfig(seed=0))
+            trace = []
+            est, rep = R.solve_centralized(net, ms, config=R.SolverConfig(iterative_refinement=True),
+                                           on_iteration=lambda it, s, d: trace.append((s, d)))
+            np.savez_compressed(
+                os.path.join(HERE, f"{tag}_centralized_refined.npz"),
+                recipe=json.dumps({"case": case, "meas_seed": 0, "refined": True}),
+                area_of_bus=np.zeros(net.n_bus, dtype=np.int32), n_gamma=0,
+                iterations=rep.iterations, converged=rep.converged, objective=rep.objective,
+                deltas=np.array([d for _, d in trace]), va=est.va, vm=est.vm,
+                trace_va=np.array([s.va for s, _ in trace]), trace_vm=np.array([s.vm for s, _ in trace]))
+            print(f"{tag}_centralized_refined: iters {rep.iterations} J {rep.objective!r}", flush=True)
     for shape in ("pegase2869", "pegase9241", "activsg10k"):
         if shape not in which:
             continue
@@ -161,4 +177,4 @@ def main(which):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["small", "pegase2869", "pegase9241", "activsg10k"])
+    main(sys.argv[1:] or ["small", "inner", "refined", "pegase2869", "pegase9241", "activsg10k"])

@@ -256,6 +256,26 @@ def test_centralized_k1_and_every_bus_its_own_area(G):
     assert rm.iterations == int(g["iterations"]) and _state_err(em.va, em.vm, g["va"], g["vm"]) < 1e-8
 
 
+@pytest.mark.parametrize("name", ["ieee14_centralized_refined", "ieee118_centralized_refined"])
+def test_centralized_with_iterative_refinement_matches_reference(G, name):
+    """SolverConfig(iterative_refinement=True) -- read by solve_centralized only (reference
+    solver.py:181-183): same iteration count, per-iteration norms and iterates as the reference's run."""
+    net, ms, part, g = build_case(name)
+    trace = []
+    est, rep = G.solve_centralized(net, ms, config=G.SolverConfig(iterative_refinement=True),
+                                   on_iteration=lambda it, s, d: trace.append((s, d)))
+    assert rep.method == "centralized" and rep.n_gamma == 0
+    assert rep.iterations == int(g["iterations"]) and rep.converged == bool(g["converged"])
+    assert _state_err(est.va, est.vm, g["va"], g["vm"]) < 1e-8          # north_star tolerance
+    assert abs(rep.objective - float(g["objective"])) <= 1e-10 * float(g["objective"])
+    for (s, d), va, vm, dref in zip(trace, g["trace_va"], g["trace_vm"], g["deltas"]):
+        assert _state_err(s.va, s.vm, va, vm) < 1e-9 and abs(d - dref) <= 1e-9 * (1 + dref)
+    assert set(rep.timings) == {"assembly", "local_condense", "boundary_assemble", "boundary_solve", "recovery", "total"}
+    # and the plain centralized solve agrees with it to rounding (the refinement only polishes)
+    plain, rplain = G.solve_centralized(net, ms)
+    assert rplain.iterations == rep.iterations and _state_err(plain.va, plain.vm, est.va, est.vm) < 1e-10
+
+
 def test_unobservable_raises_solver_error(G):
     # reference test_solver.py:335-342
     net, ms, part, _ = build_case("ieee14_k2")

@@ -94,3 +94,16 @@ def test_unobservable_area_reports_area():
     with pytest.raises(OracleError) as exc:
         Oracle(net, ms2, part.area_of_bus).solve()
     assert exc.value.kind == 1 and exc.value.area == 1
+
+
+@pytest.mark.parametrize("name", ["ieee14_centralized_refined", "ieee118_centralized_refined"])
+def test_refined_centralized_fixture_is_the_plain_solve_to_rounding(name):
+    # reference solve_centralized(iterative_refinement=True) (solver.py:181-183): one residual correction per
+    # solve only polishes the iterate, so the oracle's plain k = 1 solve pins the fixture to 1e-9
+    net, ms, part, g = build_case(name)
+    assert part.k == 1 and int(g["n_gamma"]) == 0
+    res = Oracle(net, ms, part.area_of_bus).solve(trace=True)
+    assert res["iterations"] == int(g["iterations"]) and res["converged"] == bool(g["converged"])
+    assert np.max(np.abs(res["trace_va"] - g["trace_va"])) < 1e-9
+    assert np.max(np.abs(res["trace_vm"] - g["trace_vm"])) < 1e-9
+    assert abs(res["objective"] - float(g["objective"])) <= 1e-10 * float(g["objective"])
