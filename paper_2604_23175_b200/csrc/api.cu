@@ -75,7 +75,7 @@ struct gse_plan {
     DevBuf<ChildRec> crecs;
     DevBuf<int32_t> bwd_fronts;
     DevBuf<double> lbuf, ubuf, xsol;
-    DevBuf<int32_t> upd_bus, upd_quant, upd_pos;
+    DevBuf<int32_t> upd_bus, upd_quant, upd_pos, pos_bq;
     DevBuf<double> obj_partial, status;       // status: [delta bits as double slot, err as double] (MAX-reducible)
     DevBuf<unsigned long long> flags;         // [0] delta_inf bits, [1] failure code (min)
     double* h_stage[2] = {nullptr, nullptr};  // pinned staging of new z / w
@@ -464,7 +464,13 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         sp.n_tasks = n_solve_tasks;
         sp.n_btasks = (int)btasks.size();
         sp.n_upd = (int)hp.upd_bus.size();
-        sp.n_upd_items = (sp.n_upd + kUpdPerItem - 1) / kUpdPerItem;
+        sp.n_upd_items = 0;           // the state update rides on the backward tasks (every variable is the pivot of one front)
+        {
+            std::vector<int32_t> bq((size_t)hp.n_pos, -1);
+            for (size_t v = 0; v < hp.upd_bus.size(); ++v) bq[hp.upd_pos[v]] = 2 * hp.upd_bus[v] + hp.upd_quant[v];
+            CU(plan->pos_bq.upload(bq));
+            sp.pos_bq = plan->pos_bq.ptr;
+        }
         sp.items_per_it = sp.n_eval_items + sp.n_acc_items + sp.n_tasks + sp.n_btasks + sp.n_upd_items;
         sp.n_bwd_fronts = 0;
         for (auto& lv : hp.bwd_levels) sp.n_bwd_fronts += (int)lv.size();

@@ -120,6 +120,7 @@ struct SolveProg {
     const uint32_t* acc_pair;
     const double* val;
     const int32_t *upd_bus, *upd_quant, *upd_pos;
+    const int32_t* pos_bq;        // elimination position -> 2 * bus + (0 angle | 1 magnitude): state update fused into the backward tasks
     const int32_t *m_type, *m_target, *br_from, *br_to;
     double *gval, *lbuf, *ubuf, *xsol, *bpart, *obj_partial;   // obj_partial[nblocks] then the total
     int32_t* bcnt;
