@@ -48,6 +48,11 @@ for it in range(rep.iterations):
               f"wait mean {np.mean(ready - pull) / 1e3:6.2f} max {np.max(ready - pull) / 1e3:6.2f}  "
               f"exec mean {np.mean(end - ready) / 1e3:6.2f} max {np.max(end - ready) / 1e3:6.2f} us")
     if it == 1:
+        b = blk[bounds[0]:bounds[1]]
+        ex = (b[:, 3] - b[:, 0]) / 1e3
+        q = len(ex) // 8 or 1
+        print("   eval exec by item index (mean us per eighth: flow units first, then injection, then VM): "
+              + " ".join(f"{ex[i:i + q].mean():.1f}" for i in range(0, len(ex), q)))
         b = blk[bounds[1]:bounds[2]]
         rdy = np.maximum(b[:, 2], b[:, 0])
         print(f"   acc detail (mean us): gather {np.mean(b[:,5]-rdy)/1e3:.2f}  tma wait {np.mean(b[:,6]-b[:,5])/1e3:.2f}  "
