@@ -464,7 +464,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         sp.n_tasks = n_solve_tasks;
         sp.n_btasks = (int)btasks.size();
         sp.n_upd = (int)hp.upd_bus.size();
-        sp.n_upd_items = 0;           // the state update rides on the backward tasks (every variable is the pivot of one front)
+        sp.n_upd_items = (sp.n_upd + kUpdPerItem - 1) / kUpdPerItem;
         {
             std::vector<int32_t> bq((size_t)hp.n_pos, -1);
             for (size_t v = 0; v < hp.upd_bus.size(); ++v) bq[hp.upd_pos[v]] = 2 * hp.upd_bus[v] + hp.upd_quant[v];
@@ -497,6 +497,12 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         if (mode != 2 && bo.world == 1 && sp.items_per_it > 0) {
             const int cap = solve_kernel_max_ctas(plan->solve_smem, plan->device);
             if (cap <= 0) return fail(plan, GSE_E_CUDA, "persistent solve kernel does not fit this device");
+            // Latency-bound plans (a few backward tasks per resident CTA): the state update and the norm ride on
+            // the backward tasks (every variable is the pivot of exactly one front) and the update items go.
+            // Throughput-bound plans keep them: ~1.5 us more per backward task would cost more than the hop saves.
+            bool fuse = sp.n_btasks < 4 * cap;
+            if (const char* e = getenv("GSE_FUSED_UPDATE")) fuse = atoi(e) != 0;
+            if (fuse) { sp.items_per_it -= sp.n_upd_items; sp.n_upd_items = 0; }
             plan->solve_grid = std::min(cap, sp.items_per_it);
             plan->persistent = true;
         }

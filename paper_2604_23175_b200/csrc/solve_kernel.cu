@@ -5,8 +5,9 @@
 // update, convergence test -- and the final objective (solver.py:100-103) run inside a single
 // cooperative launch.  One CTA slot per SM-resident block; CTAs pull work items from a global
 // counter in topological order
-//     [eval blocks | accumulate blocks | front tasks (level order) | backward tasks]
-// (the state update and the norm of a front's pivots ride on its backward task) and spin on per-front completion counters instead of waiting for a kernel boundary: a front
+//     [eval blocks | accumulate blocks | front tasks (level order) | backward tasks | update blocks]
+// (latency-bound plans have no update blocks: the state update and the norm of a front's pivots ride
+// on its backward task) and spin on per-front completion counters instead of waiting for a kernel boundary: a front
 // starts the moment its own children are done, areas progress independently, and nothing returns
 // to the host until the loop has converged (the host then reads iterations, the per-iteration
 // norms, the failure code and J in one copy).
@@ -130,7 +131,9 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
     unsigned* fdone = ctr + CTR_FRONT0;
     unsigned* pdone = fdone + sp.n_fronts;
     unsigned* bdone = pdone + sp.n_fronts;
-    const int o_acc = sp.n_eval_items, o_front = o_acc + sp.n_acc_items, o_bwd = o_front + sp.n_tasks;
+    const int o_acc = sp.n_eval_items, o_front = o_acc + sp.n_acc_items, o_bwd = o_front + sp.n_tasks,
+              o_upd = o_bwd + sp.n_btasks;
+    const bool fused_update = sp.n_upd_items == 0;      // latency-bound plans: the update rides on the backward tasks
     if (sp.stamps && blockIdx.x == 0 && tid == 0) sp.stamps[0] = globaltimer();
 #define GSE_STAMP(it, k) do { if (sp.stamps) atomicMax(sp.stamps + 1 + 8 * (it) + (k), globaltimer()); } while (0)
 
@@ -148,8 +151,10 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             if (tid == 0) {
                 int stop = 0;
                 for (int j = known + 1; j <= it && !stop; ++j) {
-                    wait_ge(ctr + CTR_BWD, (unsigned)sp.n_bwd_fronts * (unsigned)j);     // every front solved, state updated
-                    wait_ge(ctr + CTR_FWD, (unsigned)sp.n_tasks * (unsigned)j);
+                    if (fused_update) {
+                        wait_ge(ctr + CTR_BWD, (unsigned)sp.n_bwd_fronts * (unsigned)j);     // every front solved, state updated
+                        wait_ge(ctr + CTR_FWD, (unsigned)sp.n_tasks * (unsigned)j);
+                    } else wait_ge(ctr + CTR_UPD, (unsigned)sp.n_upd_items * (unsigned)j);
                     const unsigned long long e = ld_acquire64(sp.err);
                     const double dv = __longlong_as_double((long long)ld_acquire64(sp.delta + (j - 1)));
                     if (e != ~0ull) stop = 2 * 65536 + j;
@@ -206,12 +211,19 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
                 atomicAdd(ctr + CTR_FWD, 1u);
                 GSE_STAMP(it, 1 + S.hdr.phase);
             }
-        } else {
+        } else if (loc < o_upd) {
             // ---- backward substitution task ---------------------------------------------------------
             const BwdTask tk = sp.btasks[loc - o_bwd];
             const SpinWait w{ctr, epoch, 0u, tr, sp.n_fronts};
             const bool solved = backward_body(*reinterpret_cast<BwdScratch*>(sm), tk, ft, sp.lbuf, sp.xsol, sp.bpart, sp.bcnt, w);
-            if (solved) {
+            if (solved && !fused_update) {
+                if (tid == 0) {
+                    __threadfence();
+                    atomicAdd(bdone + tk.front, 1u);
+                    atomicAdd(ctr + CTR_BWD, 1u);
+                    GSE_STAMP(it, tk.phase == 3 ? 5 : 6);
+                }
+            } else if (solved) {
                 // the children only need x: release them first, then fold the state update and the stacked
                 // infinity norm of this front's pivots in (reference partition.py:59-62,113-116, solver.py:328-333)
                 if (tid == 0) { __threadfence(); atomicAdd(bdone + tk.front, 1u); }
@@ -239,6 +251,32 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
                     GSE_STAMP(it, tk.phase == 3 ? 5 : 6);
                     GSE_STAMP(it, 7);
                 }
+            }
+        } else {
+            // ---- state update + stacked infinity norm (throughput-bound plans: separate items) --------
+            if (tid == 0) {
+                wait_ge(ctr + CTR_BWD, (unsigned)sp.n_bwd_fronts * epoch);
+                wait_ge(ctr + CTR_FWD, (unsigned)sp.n_tasks * epoch);
+                if (tr) tr[2] = globaltimer();
+            }
+            __syncthreads();
+            unsigned long long bits = 0ull;
+#pragma unroll
+            for (int k = 0; k < kUpdPerItem / kSolveThreads; ++k) {
+                const int v = (loc - o_upd) * kUpdPerItem + k * kSolveThreads + tid;
+                if (v < sp.n_upd) {
+                    const unsigned long long b = update_var(sp.upd_bus, sp.upd_quant, sp.upd_pos, v, sp.xsol, va, vm);
+                    bits = b > bits ? b : bits;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) { const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o); bits = other > bits ? other : bits; }
+            if ((tid & 31) == 0) s_red[tid >> 5] = bits;
+            __syncthreads();
+            if (tid == 0) {
+                for (int k = 1; k < kSolveThreads / 32; ++k) bits = s_red[k] > bits ? s_red[k] : bits;
+                if (bits) atomicMax(sp.delta + it, bits);
+                signal(ctr + CTR_UPD);
+                GSE_STAMP(it, 7);
             }
         }
         if (tr && tid == 0) tr[3] = globaltimer();
