@@ -354,9 +354,10 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         // helper warps of the tensor-pipe work: the warps that share warp 0's scheduler (and with it its FP64 /
         // tensor issue port: an m8n8k4 DMMA holds the port for ~16 cycles, profiles/r01_microbench_b200.txt)
         // stay off the pipe, so the serial chain is not queued behind their MMAs
-        const bool helper = warp != 0 && (GSE_PANEL_QUIET == 0 || (warp & 3) != 0);
-        const int nw = GSE_PANEL_QUIET ? nwarps - (nwarps >> 2) : nwarps - 1;
-        const int wi = GSE_PANEL_QUIET ? warp - 1 - (warp >> 2) : warp - 1;
+        const bool quiet = GSE_PANEL_QUIET && nwarps >= 8 && (nwarps & 3) == 0;
+        const bool helper = warp != 0 && (!quiet || (warp & 3) != 0);
+        const int nw = quiet ? nwarps - (nwarps >> 2) : nwarps - 1;
+        const int wi = quiet ? warp - 1 - (warp >> 2) : warp - 1;
         for (int kb = 0; kb < rp; kb += 8) {
             const int t0 = kb >> 3;
             double* sl = s_ld + (t0 & 1) * 48;
