@@ -208,6 +208,19 @@ double *gse_boundary_delta_dev(gse_plan *plan);
 /* Device pointer to [delta_inf, failure code] as two doubles for a MAX all-reduce. */
 double *gse_status_dev(gse_plan *plan);
 
+/* ---- partitioner passes on the host (no device involved) ---------------------------------
+ * One attempt of partition_network (reference partition.py:373-403; passes partition.py:198-365:
+ * farthest-point seeds, multi-source growth, re-centring, balance moves, cascade, cut thinning) on the
+ * bus graph given as the CSR of net.neighbors(u) (same neighbor order) and the branch end arrays.
+ * first_seed is the bus numpy's default_rng(seed).integers(n) drew.  Returns 0 and area_out[n], or 1
+ * with info = {starved area, its size, buses left unassigned} (the caller raises PartitionError). */
+int gse_partition_attempt(int32_t n_bus, const int32_t *nbr_ptr, const int32_t *nbr_idx, int32_t n_branch,
+                          const int32_t *br_from, const int32_t *br_to, int32_t k, int32_t first_seed,
+                          int32_t *area_out, int32_t *info);
+/* The cut-thinning pass alone, in place (merged variants of a finer attempt). */
+int gse_partition_thin_cuts(int32_t n_bus, const int32_t *nbr_ptr, const int32_t *nbr_idx, int32_t n_branch,
+                            const int32_t *br_from, const int32_t *br_to, int32_t k, int32_t *area_inout);
+
 /* ---- introspection ------------------------------------------------------------------ */
 /* stats[0]=kernel launches of the last gse_solve/gse_iterate, [1]=fronts, [2]=levels,
  * [3]=tasks, [4]=max front order, [5]=factor doubles, [6]=update doubles,

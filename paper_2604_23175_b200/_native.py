@@ -106,6 +106,8 @@ def lib():
     L.gse_phase_local_async.argtypes = [vp, vp, vp]
     L.gse_phase_boundary_async.argtypes = [vp]
     L.gse_phase_recover_async.argtypes = [vp, vp, vp]
+    L.gse_partition_attempt.argtypes = [C.c_int32, i32p, i32p, C.c_int32, i32p, i32p, C.c_int32, C.c_int32, i32p, i32p]
+    L.gse_partition_thin_cuts.argtypes = [C.c_int32, i32p, i32p, C.c_int32, i32p, i32p, C.c_int32, i32p]
     L.gse_set_rows_pinned.argtypes = [vp, vp, vp]
     L.gse_matrix_plan_create.argtypes = [C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, C.POINTER(Options), C.POINTER(vp)]
     L.gse_matrix_set_values.argtypes = [vp, f64p, f64p, f64p, f64p, f64p]
@@ -148,7 +150,7 @@ EXPORTED = [
     "gse_exchange_offsets", "gse_boundary_delta_dev", "gse_status_dev", "gse_plan_stats",
     "gse_version", "gse_stream", "gse_matrix_plan_create", "gse_matrix_set_values", "gse_matrix_condense",
     "gse_matrix_recover", "gse_assemble_boundary", "gse_phase_local_async", "gse_phase_boundary_async",
-    "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout",
+    "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout", "gse_partition_attempt", "gse_partition_thin_cuts",
 ]
 
 

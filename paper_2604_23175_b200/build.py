@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgridse_b200.so")
-SOURCES = ["symbolic.cpp", "kernels.cu", "front_kernels.cu", "solve_kernel.cu", "api.cu"]
+SOURCES = ["symbolic.cpp", "partition.cpp", "kernels.cu", "front_kernels.cu", "solve_kernel.cu", "api.cu"]
 HEADERS = ["plan.hpp", "kernels.cuh", "unit_bodies.cuh", "front_body.cuh", os.path.join("..", "..", "include", "gridse_b200.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

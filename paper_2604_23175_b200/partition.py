@@ -141,6 +141,17 @@ class _Grid:
                 shape=(self.n, self.n))
         else:
             self.csr = sp.csr_matrix((self.n, self.n))
+        self._flat = None
+
+    def flat(self):
+        """int32 CSR of ``nbrs`` (same neighbor order) + branch ends, for the native passes."""
+        if self._flat is None:
+            ptr = np.zeros(self.n + 1, dtype=np.int32)
+            ptr[1:] = np.cumsum([len(x) for x in self.nbrs])
+            idx = np.fromiter((v for x in self.nbrs for v in x), dtype=np.int32, count=int(ptr[-1]))
+            self._flat = (ptr, idx, np.ascontiguousarray(self.f, dtype=np.int32),
+                          np.ascontiguousarray(self.t, dtype=np.int32))
+        return self._flat
 
     def hop_distance(self, sources):
         dist = np.full(self.n, -1, dtype=int)
@@ -322,7 +333,7 @@ def _cascade(g, area, k, target_ratio=2.0):
     return area
 
 
-def _thin_cuts(g, area, k, max_passes=6):
+def _thin_cuts_py(g, area, k, max_passes=6):
     size = np.bincount(area, minlength=k).astype(int)
     cap = 2 * int(size.min())
     for _ in range(max_passes):
@@ -350,7 +361,7 @@ def _thin_cuts(g, area, k, max_passes=6):
     return area
 
 
-def _attempt(g, k, seed):
+def _attempt_py(g, k, seed):
     seeds = _seed_buses(g, k, seed)
     area = _grow(g, seeds)
     for _ in range(3):
@@ -362,7 +373,49 @@ def _attempt(g, k, seed):
     area = _balance_pass(g, area, k)
     area = _cascade(g, area, k)
     area = _balance_pass(g, area, k)
-    return _thin_cuts(g, area, k)
+    return _thin_cuts_py(g, area, k)
+
+
+def _native_passes():
+    """The C++ restatement of the passes (csrc/partition.cpp) when the library is built; the Python
+    passes above are the executable specification it is tested against and the fallback without it."""
+    try:
+        from . import _native
+        return _native.lib()
+    except Exception:
+        return None
+
+
+def _i32p(a):
+    import ctypes as C
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _attempt(g, k, seed):
+    L = _native_passes()
+    if L is None:
+        return _attempt_py(g, k, seed)
+    ptr, idx, f, t = g.flat()
+    first = int(np.random.default_rng(seed).integers(g.n))       # the one random draw (as in _seed_buses)
+    area = np.zeros(g.n, dtype=np.int32)
+    info = np.zeros(3, dtype=np.int32)
+    rc = L.gse_partition_attempt(g.n, _i32p(ptr), _i32p(idx), len(f), _i32p(f), _i32p(t), int(k), first,
+                                 _i32p(area), _i32p(info))
+    if rc:
+        raise PartitionError(
+            f"partition infeasible: area {int(info[0])} starved with {int(info[1])} bus(es) "
+            f"while {int(info[2])} remain unassigned")
+    return area.astype(int)
+
+
+def _thin_cuts(g, area, k, max_passes=6):
+    L = _native_passes()
+    if L is None or max_passes != 6:
+        return _thin_cuts_py(g, area, k, max_passes)
+    ptr, idx, f, t = g.flat()
+    out = np.ascontiguousarray(area, dtype=np.int32)
+    L.gse_partition_thin_cuts(g.n, _i32p(ptr), _i32p(idx), len(f), _i32p(f), _i32p(t), int(k), _i32p(out))
+    return out.astype(int)
 
 
 def _merged_variants(g, area, k_fine):

@@ -83,6 +83,31 @@ def test_partition_goldens(cases_dir):
         G.load_partition(p4, [0, 1, 0, 1])
 
 
+def test_native_partition_passes_equal_the_python_passes():
+    """csrc/partition.cpp restates the passes of one attempt; the Python passes are its executable
+    specification: same areas bus for bus (or the same PartitionError) on random grids, and the big
+    shapes reproduce the partitions the reference partitioner itself produced (hundreds of seconds there)."""
+    from paper_2604_23175_b200 import partition as P, synth
+    assert P._native_passes() is not None, "libgridse_b200.so must be built (python -c 'import __graft_entry__ as g; g.build()')"
+    for n, seed, k in [(30, 1, 3), (60, 2, 4), (120, 3, 5), (200, 4, 7), (333, 5, 6), (50, 6, 10), (90, 7, 2), (40, 9, 39)]:
+        net = synth.random_network(n, seed, 0.3)
+        g = P._Grid(net)
+        for s in (0, 1, 7919):
+            outs = []
+            for fn in (P._attempt, P._attempt_py):
+                try:
+                    outs.append(fn(g, k, s).tolist())
+                except P.PartitionError as exc:
+                    outs.append(str(exc))
+            assert outs[0] == outs[1], (n, seed, k, s)
+            if not isinstance(outs[0], str) and k > 2:
+                merged = np.array(outs[0])
+                merged[merged == k - 1] = k - 2          # not necessarily connected: the pass only needs sizes >= 1
+                assert np.array_equal(P._thin_cuts(g, merged.copy(), k - 1), P._thin_cuts_py(g, merged.copy(), k - 1))
+    net = synth.shaped_network("pegase2869")
+    assert np.array_equal(G.partition_network(net, 8, seed=0).area_of_bus, synth.golden_partition("pegase2869"))
+
+
 def test_variable_map_layouts():
     # reference tests/test_partition.py:98-121
     p4 = make_path4()
