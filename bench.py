@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 WORKLOADS = {"pegase2869_k8": "pegase2869", "pegase9241_k16": "pegase9241", "activsg10k_k32": "activsg10k",
-             "tiled101k_k176": "tiled"}
+             "tiled101k_k176": "tiled", "tiled101k_k128": "tiled"}
 
 
 def build_workload(name):
@@ -41,7 +41,11 @@ def build_workload(name):
         # its committed 16-area partition each: 101,651 buses, 176 areas, n_Gamma = 7996)
         net, _ = synth.tiled_network(synth.shaped_network("pegase9241"), 11)
         ms = G.generate_measurements(net, G.MeasurementConfig(seed=0))
-        part = G.load_partition(net, synth.tile_partition(synth.golden_partition("pegase9241"), 11))
+        if name == "tiled101k_k128":
+            # the 128 areas BASELINE.json names: partition_network of this package on the tiled grid (committed; 34 s)
+            part = G.load_partition(net, synth.golden_partition("tiled101k_k128"))
+        else:
+            part = G.load_partition(net, synth.tile_partition(synth.golden_partition("pegase9241"), 11))
         return net, ms, part
     net = synth.shaped_network(shape)
     ms = G.generate_measurements(net, G.MeasurementConfig(seed=0))

@@ -118,8 +118,13 @@ int center_of(const Grid& g, const std::vector<int>& area, int a) {
 bool stays_connected(const Grid& g, const std::vector<int>& area, const std::vector<int>& size, int a, int without) {
     const int members = size[a] - ((without >= 0 && area[without] == a) ? 1 : 0);
     if (members <= 0) return false;
+    // (the answer does not depend on where the walk starts: a neighbor of the removed bus saves the scan)
     int start = -1;
-    for (int u = 0; u < g.n; ++u) if (area[u] == a && u != without) { start = u; break; }
+    if (without >= 0)
+        for (int p = g.ptr[without]; p < g.ptr[without + 1] && start < 0; ++p)
+            if (area[g.idx[p]] == a && g.idx[p] != without) start = g.idx[p];
+    if (start < 0)
+        for (int u = 0; u < g.n; ++u) if (area[u] == a && u != without) { start = u; break; }
     if ((int)g.mark.size() != g.n) { g.mark.assign(g.n, 0); g.stamp = 0; }
     const int st = ++g.stamp;
     std::vector<int> todo{start};

@@ -75,6 +75,33 @@ def test_tiled_100k_bitwise_repeatable_and_scheduler_independent(G, tiled):
     assert 10.5 * 73721.5 < r1.objective < 11.5 * 73721.5
 
 
+def test_tiled_100k_in_128_areas_gives_the_same_estimate(G, tiled):
+    """BASELINE.json's ~100k-bus configuration names 128 areas: the committed partition_network result of
+    this package on the tiled grid (cases/part_tiled101k_k128.json).  The WLS optimum does not depend on
+    the partition: same iteration count, same state (to solver accuracy) and objective as with 176 areas;
+    noiseless measurements return the truth."""
+    from paper_2604_23175_b200 import synth
+    net, part176, noisy, exact, est176 = tiled
+    part = G.load_partition(net, synth.golden_partition("tiled101k_k128"))
+    assert part.k == 128
+    est = G.MultiAreaEstimator(net, noisy, part)
+    try:
+        est176.update_measurements(noisy)
+        s176, r176 = est176.estimate()
+        s128, r128 = est.estimate()
+        assert r128.converged and r128.iterations == r176.iterations
+        assert np.max(np.abs(s128.va - s176.va)) < 1e-9 and np.max(np.abs(s128.vm - s176.vm)) < 1e-9
+        assert abs(r128.objective - r176.objective) <= 1e-10 * r176.objective
+        again, r2 = est.estimate()
+        assert np.array_equal(again.va, s128.va) and np.array_equal(again.vm, s128.vm)
+        est.update_measurements(exact)
+        st, rep = est.estimate()
+        va_true = np.array([b.va_true for b in net.buses]); vm_true = np.array([b.vm_true for b in net.buses])
+        assert rep.converged and np.max(np.abs(st.va - va_true)) < 1e-8 and np.max(np.abs(st.vm - vm_true) / vm_true) < 1e-8
+    finally:
+        est.close()
+
+
 @pytest.mark.parametrize("name", ["ieee14_k2", "ieee118_k6", "pegase2869_k8", "pegase9241_k16", "activsg10k_k32"])
 def test_persistent_kernel_matches_level_path_bitwise(G, name):
     from conftest import build_case
