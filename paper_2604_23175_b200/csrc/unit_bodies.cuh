@@ -186,6 +186,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// Rounds of K interleaved contribution lists, until list K - 1 (the shortest of them) is exhausted; every
+// list sums in its own pair order with separately rounded multiply / add (the bincount arithmetic).
+template <int K>
+__device__ __forceinline__ void acc_rounds(const double* sv, const uint32_t* spair, int (&q)[4], const int (&qe)[4],
+                                           uint32_t (&pr)[4], double (&s)[4]) {
+    while (q[K - 1] < qe[K - 1]) {
+        double x[K], y[K];
+        uint32_t nx[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) { x[k] = sv[pr[k] & 0xffffu]; y[k] = sv[pr[k] >> 16]; }
+#pragma unroll
+        for (int k = 0; k < K; ++k) nx[k] = q[k] + 1 < qe[k] ? spair[q[k] + 1] : 0u;     // next round's pairs
+#pragma unroll
+        for (int k = 0; k < K; ++k) { s[k] = __dadd_rn(s[k], __dmul_rn(x[k], y[k])); ++q[k]; pr[k] = nx[k]; }
+    }
+}
+
 __device__ __forceinline__ void acc_item_staged(const AccProg& ap, int item, double* stage, unsigned long long* bar,
                                                 unsigned& parity, unsigned long long* tr = nullptr) {
     const int4 r0 = reinterpret_cast<const int4*>(ap.items)[2 * item];       // first dest, dests, value offset, values
@@ -229,20 +246,13 @@ __device__ __forceinline__ void acc_item_staged(const AccProg& ap, int item, dou
             q[k] = od[k] >= 0 ? sptr[od[k]] : 0; qe[k] = od[k] >= 0 ? sptr[od[k] + 1] : 0; s[k] = 0.0;
             pr[k] = q[k] < qe[k] ? spair[q[k]] : 0u;
         }
-        // ranks db, db + nth, ... are in decreasing length order: lane 0 of the interleave is the longest
-        while (q[0] < qe[0]) {
-            double x[4], y[4];
-            uint32_t nx[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) { x[k] = sv[pr[k] & 0xffffu]; y[k] = sv[pr[k] >> 16]; }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) nx[k] = q[k] + 1 < qe[k] ? spair[q[k] + 1] : 0u;     // next round's pairs
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (q[k] < qe[k]) { s[k] = __dadd_rn(s[k], __dmul_rn(x[k], y[k])); ++q[k]; }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) pr[k] = nx[k];
-        }
+        // ranks db, db + nth, ... are in decreasing length order: list 0 of the interleave is the longest, list 3
+        // the shortest.  The interleave narrows as the short lists run out (4, 3, 2, then 1 list per round), so
+        // the long tail of list 0 does not keep issuing the (predicated-off) shared-memory loads of the others.
+        acc_rounds<4>(sv, spair, q, qe, pr, s);
+        acc_rounds<3>(sv, spair, q, qe, pr, s);
+        acc_rounds<2>(sv, spair, q, qe, pr, s);
+        acc_rounds<1>(sv, spair, q, qe, pr, s);
 #pragma unroll
         for (int k = 0; k < 4; ++k) if (od[k] >= 0) ap.out[r0.x + od[k]] = s[k];
     }
