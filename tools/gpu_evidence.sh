@@ -3,7 +3,7 @@
 # persistent-kernel timeline + sanitizer + ncu launch lists / full captures.  Outputs in gpurun_out/.
 mkdir -p gpurun_out
 bash tools/gpu_check.sh > gpurun_out/check.log 2>&1
-for W in pegase2869_k8 activsg10k_k32 tiled101k_k176; do
+for W in pegase2869_k8 activsg10k_k32 tiled101k_k176 tiled101k_k128; do
   timeout 900 python bench.py --workload $W --steps 20 > gpurun_out/bench_$W.json 2> gpurun_out/bench_$W.err
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
@@ -13,4 +13,4 @@ bash tools/gpu_sanitize.sh > /dev/null 2>&1
 bash tools/gpu_ncu.sh pegase9241_k16 > gpurun_out/ncu.log 2>&1
 for f in gpurun_out/launches_persistent_pegase9241_k16.csv gpurun_out/launches_levels_pegase9241_k16.csv; do python tools/summarize_launches.py $f second-half > ${f%.csv}.txt 2>&1; done
 tail -4 gpurun_out/check.log | cut -c1-300; head -3 gpurun_out/trace.txt; tail -3 gpurun_out/sanitizer.txt; ls -la gpurun_out/*.ncu-rep
-for W in pegase2869_k8 activsg10k_k32 tiled101k_k176 reference; do cut -c1-220 gpurun_out/bench_$W.json; done
+for W in pegase2869_k8 activsg10k_k32 tiled101k_k176 tiled101k_k128 reference; do cut -c1-220 gpurun_out/bench_$W.json; done
