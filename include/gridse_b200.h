@@ -71,7 +71,7 @@ typedef struct {
     const int32_t *area_rank;/* [n_areas] owner rank per area, NULL = all on rank 0          */
     int32_t persistent;      /* gse_solve scheduler: 0 auto (persistent dataflow kernel on single-rank plans),
                               * 1 persistent, 2 level launches captured in a CUDA graph             */
-    int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default 48) */
+    int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default: 32 up to 30k buses, else 48) */
     int32_t boundary_mode;   /* boundary factorisation: 0 auto, 1 dense chain (dense_cholesky_solve), 2 block-sparse tree */
     void *stream;            /* cudaStream_t every kernel / copy of the plan is enqueued on; NULL = a stream of its own */
 } gse_options;

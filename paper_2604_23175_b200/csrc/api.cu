@@ -245,6 +245,11 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         return fail(plan, GSE_E_NO_DEVICE, "no CUDA device visible: gridse-b200 has no CPU fallback");
     plan->device = opt ? opt->device : 0;
     CU(cudaSetDevice(plan->device));
+    // Update-row chunk of a task: latency-bound plans (every <= ~30k-bus shape: fewer tasks than ~4 per resident
+    // CTA) run best with 32-row tiles -- shorter panels and gathers on the critical chain (PEGASE-9241: 1.49 vs
+    // 1.51 ms, PEGASE-2869: 0.81 vs 0.85 ms per solve); throughput-bound plans with 48 (the ~100k-bus grid:
+    // 5.60 vs 7.54 ms).  gse_options.tile_rows / GSE_TILE_ROWS override.
+    bo.tile_rows = d->n_bus <= 30000 ? 32 : 48;
     if (opt) {
         bo.dense = opt->backend_dense != 0;
         if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
