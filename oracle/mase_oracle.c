@@ -683,6 +683,24 @@ double orc_recover_masked(orc_t *o, double *va, double *vm, const int32_t *mine)
     for (int s = 0; s < o->n_gamma; s++) { int b = o->gamma_bus[s]; if (s < o->n_ga) va[b] += o->dx_gamma[s]; else vm[b] += o->dx_gamma[s]; if (fabs(o->dx_gamma[s]) > dmax) dmax = fabs(o->dx_gamma[s]); }
     return dmax;
 }
+/* inner GN step of the owned areas only (multi-process driver with inner_gn_steps > 1) */
+double orc_inner_step_masked(orc_t *o, double *va, double *vm, const int32_t *mine) {
+    int K = o->d.n_areas; double dmax = 0.0;
+    double *zero = xcalloc(o->n_gamma > 0 ? o->n_gamma : 1, sizeof(double));
+    for (int a = 0; a < K; a++) {
+        if (!mine[a]) continue;
+        area_t *A = &o->areas[a];
+        eval_rows(o, A, va, vm); accumulate(o, A);
+        A->fail_pivot = chol_refactor(&A->ch, A->data_ii);
+        if (A->fail_pivot >= 0) { o->err_kind = 1; o->err_area = a; o->err_pivot = A->fail_pivot; free(zero); return -1.0; }
+        recover(A, zero);
+        for (int i = 0; i < A->n_ia; i++) va[A->ia_bus[i]] += A->dxi[i];
+        for (int i = 0; i < A->n_int_bus; i++) vm[A->int_bus[i]] += A->dxi[A->n_ia + i];
+        for (int i = 0; i < A->n_i; i++) if (fabs(A->dxi[i]) > dmax) dmax = fabs(A->dxi[i]);
+    }
+    free(zero);
+    return dmax;
+}
 /* buses whose state this rank owns: interiors of its areas (boundary buses are replicated) */
 void orc_owned_interior_mask(const orc_t *o, const int32_t *mine, int32_t *bus_mask) {
     for (int b = 0; b < o->d.n_bus; b++) bus_mask[b] = 0;

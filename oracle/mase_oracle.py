@@ -234,6 +234,17 @@ class Oracle:
         mine = np.ascontiguousarray(mine, dtype=np.int32)
         return float(lib.orc_recover_masked(self._h, _p(va, _f64p), _p(vm, _f64p), _p(mine, _i32p)))
 
+    def inner_step_masked(self, va, vm, mine):
+        """In-place interior-only GN step of the areas flagged in ``mine``; returns max |dx_i|."""
+        lib = _lib()
+        lib.orc_inner_step_masked.restype = C.c_double
+        lib.orc_inner_step_masked.argtypes = [C.c_void_p, _f64p, _f64p, _i32p]
+        mine = np.ascontiguousarray(mine, dtype=np.int32)
+        d = float(lib.orc_inner_step_masked(self._h, _p(va, _f64p), _p(vm, _f64p), _p(mine, _i32p)))
+        if d < 0:
+            self._raise()
+        return d
+
     def objective(self, va, vm):
         va = np.ascontiguousarray(va, dtype=np.float64)
         vm = np.ascontiguousarray(vm, dtype=np.float64)

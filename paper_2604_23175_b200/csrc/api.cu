@@ -119,6 +119,20 @@ int fail(gse_plan* p, int code, const std::string& msg, int area = -1, int pivot
         if (e_ != cudaSuccess) return fail(plan, GSE_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Host <-> device traffic of the C ABI is ordered on the PLAN's stream (a non-blocking stream, or the
+// caller's): a copy on the legacy default stream would not be ordered with the plan's kernels, and a
+// pageable host-to-device cudaMemcpy may return before the data has landed.  The copy is enqueued on
+// the plan's stream and the host waits for it (the source / destination is caller memory).
+cudaError_t copy_sync(gse_plan* plan, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    if (bytes == 0) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, plan->stream);
+    return e == cudaSuccess ? cudaStreamSynchronize(plan->stream) : e;
+}
+// failure flag back to "none": stream-ordered, so it cannot race with the reads / atomicMin of the next solve
+cudaError_t reset_failure_flag(gse_plan* plan) {
+    return cudaMemsetAsync(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long), plan->stream);
+}
+
 // all kernels of one outer iteration on plan->stream; phase boundaries marked with events if timed
 int enqueue_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
     launch_eval(plan->ep, va, vm, plan->stream);
@@ -553,10 +567,9 @@ int gse_set_measurements(gse_plan* plan, const double* z) { return stage_rows(pl
 int gse_check(gse_plan* plan) {
     CU(cudaSetDevice(plan->device));
     unsigned long long code = 0;
-    CU(cudaStreamSynchronize(plan->stream));
-    CU(cudaMemcpy(&code, plan->flags.ptr + 1, sizeof code, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, &code, plan->flags.ptr + 1, sizeof code, cudaMemcpyDeviceToHost));
     if (code == ~0ull) return GSE_OK;
-    CU(cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long)));
+    CU(reset_failure_flag(plan));
     return decode_failure(plan, code);
 }
 
@@ -569,7 +582,7 @@ int gse_iterate(gse_plan* plan, double* va, double* vm, double* delta_inf) {
     plan->launches_last = plan->launches_per_iter;
     if (plan->h_flags[1] != ~0ull) {
         unsigned long long code = plan->h_flags[1];
-        cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+        reset_failure_flag(plan);
         return decode_failure(plan, code);
     }
     double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
@@ -597,7 +610,7 @@ int gse_inner_step(gse_plan* plan, double* va, double* vm, double* delta_inf) {
     CU(cudaStreamSynchronize(s));
     if (plan->h_flags[1] != ~0ull) {
         unsigned long long code = plan->h_flags[1];
-        cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+        reset_failure_flag(plan);
         return decode_failure(plan, code);
     }
     double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
@@ -654,7 +667,7 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
         }
     }
     if (blk[kBlkErr] != ~0ull) {
-        cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+        reset_failure_flag(plan);
         return decode_failure(plan, blk[kBlkErr]);
     }
     memcpy(&rep->objective, &blk[kBlkObj], sizeof(double));
@@ -664,7 +677,11 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
 int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse_report* rep) {
     CU(cudaSetDevice(plan->device));
     memset(rep, 0, sizeof *rep);
-    const int max_it = std::min(cfg->max_outer_iterations, 64);
+    // the report carries 64 per-iteration norms / stamp blocks: longer loops go through gse_iterate (the
+    // reference has no cap; the Python layer switches to that loop by itself)
+    if (cfg->max_outer_iterations < 1 || cfg->max_outer_iterations > 64)
+        return fail(plan, GSE_E_INVALID, "gse_solve: max_outer_iterations must be in [1, 64]; drive longer loops with gse_iterate");
+    const int max_it = cfg->max_outer_iterations;
     const bool timed = cfg->time_phases != 0;
     if (!timed && plan->persistent) return solve_persistent(plan, cfg, max_it, va, vm, rep);
     if (!timed) { int rc = ensure_graph(plan, va, vm); if (rc) return rc; }
@@ -681,7 +698,7 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
         rep->iterations = it;
         if (plan->h_flags[1] != ~0ull) {
             unsigned long long code = plan->h_flags[1];
-            cudaMemset(plan->flags.ptr + 1, 0xff, sizeof(unsigned long long));
+            reset_failure_flag(plan);
             status = decode_failure(plan, code);
             break;
         }
@@ -758,7 +775,7 @@ int gse_matrix_set_values(gse_plan* plan, const double* data_ii, const double* d
         const int64_t off = s < o_ib ? 0 : s < o_bb ? o_ib : s < o_bi ? o_bb : s < o_bbv ? o_bi : o_bbv;
         if (src) g[e] = src[s - off];
     }
-    CU(cudaMemcpy(plan->gval.ptr, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(copy_sync(plan, plan->gval.ptr, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice));
     return GSE_OK;
 }
 
@@ -774,8 +791,8 @@ int gse_matrix_recover(gse_plan* plan, const double* dx_b, double* dx_i) {
     const HostProgram& hp = plan->hp;
     CU(cudaSetDevice(plan->device));
     if (hp.n_gamma) {
-        if (dx_b) CU(cudaMemcpy(plan->xsol.ptr + hp.gamma_base, dx_b, sizeof(double) * hp.n_gamma, cudaMemcpyHostToDevice));
-        else CU(cudaMemset(plan->xsol.ptr + hp.gamma_base, 0, sizeof(double) * hp.n_gamma));
+        if (dx_b) CU(copy_sync(plan, plan->xsol.ptr + hp.gamma_base, dx_b, sizeof(double) * hp.n_gamma, cudaMemcpyHostToDevice));
+        else CU(cudaMemsetAsync(plan->xsol.ptr + hp.gamma_base, 0, sizeof(double) * hp.n_gamma, plan->stream));
     }
     enqueue_bwd(plan, 4);
     CU(cudaStreamSynchronize(plan->stream));
@@ -823,6 +840,7 @@ int gse_phase_assemble(gse_plan* plan, const double* va, const double* vm) {
         build_reference_program(plan->hp);
         CU(plan->racc_ptr.upload(plan->hp.racc_ptr)); CU(plan->racc_a.upload(plan->hp.racc_a)); CU(plan->racc_b.upload(plan->hp.racc_b));
         CU(plan->refval.alloc(plan->hp.n_ref_vals));
+        CU(cudaDeviceSynchronize());          // the uploads ran on the legacy stream, the kernels below on the plan's
     }
     enqueue_phase_assemble(plan, va, vm);
     // reference-layout blocks for component parity (same slot values, second destination map)
@@ -851,7 +869,7 @@ int gse_phase_recover(gse_plan* plan, double* va, double* vm, double* delta_inf)
     CU(cudaStreamSynchronize(plan->stream));
     double dv; memcpy(&dv, &plan->h_flags[0], sizeof dv);
     if (delta_inf) *delta_inf = dv;
-    CU(cudaMemcpy(plan->status.ptr, &dv, sizeof dv, cudaMemcpyHostToDevice));
+    CU(copy_sync(plan, plan->status.ptr, &dv, sizeof dv, cudaMemcpyHostToDevice));
     return GSE_OK;
 }
 
@@ -907,17 +925,17 @@ int gse_area_blocks(gse_plan* plan, int32_t a, double* data_ii, double* data_ib,
     CU(cudaSetDevice(plan->device));
     const size_t nii = hp.ii_idx[a].size(), nib = hp.ib_idx[a].size(), nb = hp.area_nb[a], ni = hp.area_ni[a];
     const double* base = plan->refval.ptr + hp.ref_off[a];
-    CU(cudaMemcpy(data_ii, base, nii * 8, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(data_ib, base + nii, nib * 8, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(g_bb, base + nii + nib, nb * nb * 8, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(b_i, base + nii + nib + nb * nb, ni * 8, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(b_b, base + nii + nib + nb * nb + ni, nb * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, data_ii, base, nii * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, data_ib, base + nii, nib * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, g_bb, base + nii + nib, nb * nb * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, b_i, base + nii + nib + nb * nb, ni * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, b_b, base + nii + nib + nb * nb + ni, nb * 8, cudaMemcpyDeviceToHost));
     return GSE_OK;
 }
 // packed lower (rows in front order) -> full symmetric in the caller's order; pos[i] = front row of item i
 static int unpack_lower(gse_plan* plan, const Front& f, int n, const std::vector<int>& pos, double* full, double* rhs) {
     std::vector<double> packed((size_t)f.u1 * (f.u1 + 1) / 2);
-    cudaError_t e = cudaMemcpy(packed.data(), plan->ubuf.ptr + f.u_off, packed.size() * 8, cudaMemcpyDeviceToHost);
+    cudaError_t e = copy_sync(plan, packed.data(), plan->ubuf.ptr + f.u_off, packed.size() * 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(plan, GSE_E_CUDA, cudaGetErrorString(e));
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
@@ -940,7 +958,7 @@ int gse_boundary_system(gse_plan* plan, double* s_gamma, double* b_gamma, double
     if (hp.gamma_root < 0) return fail(plan, GSE_E_INVALID, "boundary system lives on the coordinator rank");
     int rc = unpack_lower(plan, hp.fronts[hp.gamma_root], hp.n_gamma, hp.gamma_sparse ? hp.gamma_epos : std::vector<int>(hp.gamma_epos), s_gamma, b_gamma);
     if (rc) return rc;
-    CU(cudaMemcpy(dx_gamma, plan->xsol.ptr + hp.gamma_base, hp.n_gamma * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, dx_gamma, plan->xsol.ptr + hp.gamma_base, hp.n_gamma * 8, cudaMemcpyDeviceToHost));
     return GSE_OK;
 }
 int gse_area_delta(gse_plan* plan, int32_t a, double* dx_i) {
@@ -949,13 +967,13 @@ int gse_area_delta(gse_plan* plan, int32_t a, double* dx_i) {
     CU(cudaSetDevice(plan->device));
     const int ni = hp.area_ni[a];
     std::vector<double> x(ni);
-    CU(cudaMemcpy(x.data(), plan->xsol.ptr + hp.area_base[a], ni * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, x.data(), plan->xsol.ptr + hp.area_base[a], ni * 8, cudaMemcpyDeviceToHost));
     for (int e = 0; e < ni; ++e) dx_i[hp.perm_orig[hp.area_base[a] + e]] = x[e];
     return GSE_OK;
 }
 int gse_set_boundary_delta(gse_plan* plan, const double* dx_gamma) {
     CU(cudaSetDevice(plan->device));
-    CU(cudaMemcpy(plan->xsol.ptr + plan->hp.gamma_base, dx_gamma, plan->hp.n_gamma * 8, cudaMemcpyHostToDevice));
+    CU(copy_sync(plan, plan->xsol.ptr + plan->hp.gamma_base, dx_gamma, plan->hp.n_gamma * 8, cudaMemcpyHostToDevice));
     return GSE_OK;
 }
 

@@ -125,6 +125,11 @@ class CudaEngine:
     def phase_recover(self):
         return self.plan.phase_recover(self.state[0].data_ptr(), self.state[1].data_ptr())
 
+    def inner_step(self):
+        """One interior-only GN step of the owned areas, boundary held fixed (reference solver.py:253-260);
+        returns max |dx_i| of this rank."""
+        return self._translated(self.plan.inner_step, self.state[0].data_ptr(), self.state[1].data_ptr())
+
     # enqueue-only variants (same kernels; no host synchronisation, failures surface in status[1])
     def phase_local_async(self):
         self.plan.phase_local_async(self.state[0].data_ptr(), self.state[1].data_ptr())
@@ -156,11 +161,16 @@ class CudaEngine:
 class DistributedEstimator:
     """Multi-rank counterpart of ``MultiAreaEstimator`` (same ``estimate`` contract)."""
 
-    def __init__(self, net, ms, part, maps=None, config: SolverConfig = None, device=0,
+    def __init__(self, net, ms, part, maps=None, config: SolverConfig = None, device=None,
                  engine_factory=None, group=None):
+        import os
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
+        if device is None:
+            # one process per GPU: the launcher's LOCAL_RANK, else whatever device the caller made current
+            device = int(os.environ["LOCAL_RANK"]) if "LOCAL_RANK" in os.environ else (
+                torch.cuda.current_device() if torch.cuda.is_available() else 0)
         self.cfg = config or SolverConfig()
         self.net, self.ms, self.part = net, ms, part
         self.bord, self.maps = maps if maps is not None else build_variable_maps(net, part)
@@ -209,6 +219,10 @@ class DistributedEstimator:
 
     # -- the solve -------------------------------------------------------------------------------
     def update_measurements(self, ms):
+        same_rows = ms.m == self.ms.m and all(
+            a is b or np.array_equal(a, b) for a, b in ((ms.mtype, self.ms.mtype), (ms.target, self.ms.target)))
+        if not same_rows:
+            raise ValueError("measurement rows differ from the analysed template set")
         self.engine.plan.set_measurements(ms.z)
         self.engine.plan.set_weights(ms.weight)
         self.ms = ms
@@ -220,6 +234,27 @@ class DistributedEstimator:
         with ctx():
             return self._estimate(on_iteration)
 
+    def _inner_steps(self):
+        """``inner_gn_steps - 1`` interior-only GN steps of every rank's areas with the boundary held fixed
+        (reference solver.py:253-260); returns the largest |dx_i| over all ranks (it joins the stacked norm
+        of the iteration).  A failed factorisation is reported on every rank."""
+        steps = self.cfg.inner_gn_steps - 1
+        if steps <= 0:
+            return 0.0
+        inner, failure = 0.0, None
+        for _ in range(steps):
+            try:
+                inner = max(inner, float(self.engine.inner_step()))
+            except Exception as exc:
+                failure = exc
+                break
+        inner, flag = self._allreduce_max([inner, 1.0 if failure is not None else 0.0])
+        if flag:
+            raise failure if failure is not None else SolverError(
+                "an area interior block on another rank is not positive definite; "
+                "that area is likely locally unobservable")
+        return inner
+
     def _estimate(self, on_iteration=None):
         cfg, eng = self.cfg, self.engine
         t_start = time.perf_counter()
@@ -230,6 +265,7 @@ class DistributedEstimator:
         t_loop = time.perf_counter()
         use_async = bool(getattr(eng, "async_phases", False))
         for it in range(1, cfg.max_outer_iterations + 1):
+            inner = self._inner_steps()
             if use_async:
                 # one pipeline per iteration on the engine's stream: local condensation -> gather of the
                 # (S_b | b_hat) segments -> boundary solve on the coordinator -> broadcast of delta_x_Gamma
@@ -244,6 +280,7 @@ class DistributedEstimator:
                 if self.world > 1:
                     self.dist.all_reduce(eng.status, op=self.dist.ReduceOp.MAX, group=self.group)
                 delta, failed = (float(v) for v in eng.status.cpu())
+                delta = max(delta, inner)
                 self.launches_per_solve += eng.launches_last()
                 if failed:
                     eng.check()        # the owning rank raises the precise error ...
@@ -283,7 +320,7 @@ class DistributedEstimator:
                 eng.sync()
                 self.dist.broadcast(eng.delta, src=0, group=self.group)
             local_delta = eng.phase_recover()
-            delta = self._allreduce_max([local_delta])[0]
+            delta = max(self._allreduce_max([local_delta])[0], inner)
             iterations = it
             deltas.append(delta)
             if on_iteration is not None:

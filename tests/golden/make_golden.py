@@ -11,6 +11,9 @@ synthetic-grid generator from /root/reference/pkg/tests/conftest.py, runs
 cases), and stores inputs + outputs as ``.npz``.  Nothing at test time reads
 /root/reference: the tests load these files only.
 
+``tiled101k`` runs the reference once on the ~100k-bus / 128-area configuration (BASELINE.json configs[4];
+minutes of CPU) and stores the end state, J and the per-iteration norms.
+
 Also writes the reference partitioner's ``area_of_bus`` for the three named
 shapes to ``paper_2604_23175_b200/cases/part_<shape>.json`` (the reference
 partitioner takes 23 s / 141 s / 79 s there).
@@ -176,5 +179,58 @@ def main(which):
                                  "meas_seed": 0, "k": k, "part_seed": 0})
 
 
+def tiled_reference_network(base, copies, ties_per_seam=3):
+    """The ~100k-bus grid of BASELINE.json configs[4] built from the REFERENCE's own classes: ``copies``
+    relabelled copies of ``base`` chained by tie branches (same construction as the product's
+    ``synth.tiled_network``; tests/test_host_api.py pins the two to the same Ybus fingerprint)."""
+    n = base.n_bus
+    buses, branches = [], []
+    for c in range(copies):
+        for i, b in enumerate(base.buses):
+            buses.append(R.Bus(id=c * n + i + 1, base_kv=b.base_kv, gs=b.gs, bs=b.bs,
+                               is_slack=(b.is_slack and c == 0), vm_true=b.vm_true, va_true=b.va_true))
+        for br in base.branches:
+            branches.append(R.Branch(from_bus=c * n + br.from_bus, to_bus=c * n + br.to_bus, r=br.r, x=br.x,
+                                     b_charging=br.b_charging, tap=br.tap, shift=br.shift))
+        if c:
+            for j in range(ties_per_seam):
+                branches.append(R.Branch(from_bus=c * n - 1 - 2 * j, to_bus=c * n + 2 * j,
+                                         r=0.01 + 0.002 * j, x=0.08 + 0.01 * j, b_charging=0.02))
+    return R.BusBranchNetwork.from_components(buses, branches)
+
+
+def tiled101k():
+    """BASELINE.json configs[4]: 11 tiles of the PEGASE-9241 shape (101,651 buses, 1,011,229 rows) in the
+    128 areas of cases/part_tiled101k_k128.json, solved ONCE by the unmodified reference
+    (solve_multiarea, LAPACK boundary Cholesky of the n_Gamma = 5692 system).  Stores the end state, J,
+    the per-iteration norms and first-iteration fingerprints; no per-area detail (the file stays small)."""
+    n, nbr, _ = SHAPES["pegase9241"]
+    base = random_network(n, seed=n, extra_frac=(nbr - (n - 1)) / n)
+    net = tiled_reference_network(base, 11)
+    part = R.load_partition(net, json.load(open(os.path.join(CASES, "part_tiled101k_k128.json")))["area_of_bus"])
+    ms = R.generate_measurements(net, R.MeasurementConfig(seed=0))
+    bord, maps = R.build_variable_maps(net, part)
+    trace = []
+    t0 = time.perf_counter()
+    est, rep = R.solve_multiarea(net, ms, part, maps=(bord, maps),
+                                 on_iteration=lambda it, s, d: (trace.append(d), print("  it", it, d, flush=True)))
+    wall = time.perf_counter() - t0
+    y = net.ybus
+    np.savez_compressed(
+        os.path.join(HERE, "tiled101k_k128.npz"),
+        recipe=json.dumps({"gen": "tiled_network(shaped_network('pegase9241'), 11)", "meas_seed": 0,
+                           "partition": "cases/part_tiled101k_k128.json"}),
+        area_of_bus=part.area_of_bus.astype(np.int32), n_gamma=bord.n_gamma,
+        z_sum=np.array([ms.z.sum(), np.abs(ms.z).sum(), ms.weight.sum()]),
+        ybus_sum=np.array([y.data.real.sum(), y.data.imag.sum(), np.abs(y.data).sum(), y.nnz]),
+        iterations=rep.iterations, converged=rep.converged, objective=rep.objective,
+        deltas=np.array(trace), va=est.va, vm=est.vm, ref_wall_s=wall, ref_timings=json.dumps(rep.timings))
+    print(f"tiled101k_k128: iters {rep.iterations} conv {rep.converged} J {rep.objective!r} "
+          f"n_gamma {bord.n_gamma} wall {wall:.1f}s", flush=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["small", "inner", "refined", "pegase2869", "pegase9241", "activsg10k"])
+    which = sys.argv[1:] or ["small", "inner", "refined", "pegase2869", "pegase9241", "activsg10k", "tiled101k"]
+    main(which)
+    if "tiled101k" in which:
+        tiled101k()

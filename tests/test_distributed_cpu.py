@@ -74,6 +74,14 @@ class OracleEngine:
         self.state[1] = self.state.new_tensor(vm)
         return d
 
+    def inner_step(self):
+        st = self.state.numpy()
+        va, vm = st[0].copy(), st[1].copy()
+        d = self.orc.inner_step_masked(va, vm, self.mine)
+        self.state[0] = self.state.new_tensor(va)
+        self.state[1] = self.state.new_tensor(vm)
+        return d
+
     def sync(self):
         pass
 
@@ -132,14 +140,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, out_dir, async_phases=False):
+def _worker(rank, world, port, name, out_dir, async_phases=False, inner=1):
     import torch.distributed as dist
     from conftest import build_case
     from paper_2604_23175_b200.distributed import DistributedEstimator
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         net, ms, part, g = build_case(name)
-        est = DistributedEstimator(net, ms, part, engine_factory=AsyncOracleEngine if async_phases else OracleEngine)
+        from paper_2604_23175_b200 import SolverConfig
+        est = DistributedEstimator(net, ms, part, config=SolverConfig(inner_gn_steps=inner),
+                                   engine_factory=AsyncOracleEngine if async_phases else OracleEngine)
         trace = []
         state, rep = est.estimate(on_iteration=lambda it, s, d: trace.append(d))
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), va=state.va, vm=state.vm,
@@ -170,6 +180,27 @@ def test_sharded_solve_is_bit_identical_to_single_process(tmp_path, name, world,
         assert np.array_equal(o["deltas"], ref["deltas"])
     ar = outs[0]["area_rank"]
     assert len(np.unique(ar)) == min(world, part.k) and np.all(np.diff(ar) >= 0)   # contiguous, all ranks busy
+
+
+@pytest.mark.parametrize("name,world,inner,async_phases", [("ieee118_k6_inner2", 2, 2, False), ("rand120_k4_inner3", 3, 3, True)])
+def test_sharded_inner_gn_steps_match_single_process_and_reference(tmp_path, name, world, inner, async_phases):
+    """SolverConfig.inner_gn_steps > 1 across ranks (reference solver.py:253-260): every rank runs the
+    interior-only steps of its own areas, their norm joins the stacked norm of the iteration -- same
+    iterates / iteration count as one process and as the reference's stored run."""
+    import torch.multiprocessing as mp
+    from conftest import build_case
+    from oracle.mase_oracle import Oracle
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, name, str(tmp_path), async_phases, inner), nprocs=world, join=True)
+    net, ms, part, g = build_case(name)
+    ref = Oracle(net, ms, part.area_of_bus).solve(inner=inner)
+    for r in range(world):
+        o = np.load(os.path.join(tmp_path, f"rank{r}.npz"))
+        assert int(o["iterations"]) == ref["iterations"] == int(g["iterations"])
+        assert np.array_equal(o["va"], ref["va"]) and np.array_equal(o["vm"], ref["vm"]), r
+        assert np.array_equal(o["deltas"], ref["deltas"])
+        assert np.allclose(o["deltas"], g["deltas"], rtol=1e-6, atol=1e-12)
+        assert np.max(np.abs(o["va"] - g["va"])) < 1e-9 and np.max(np.abs(o["vm"] - g["vm"])) < 1e-9
 
 
 def test_assign_areas_properties():

@@ -124,6 +124,52 @@ def test_phase_outputs_match_oracle(G, name, boundary_mode):
     plan.close()
 
 
+@pytest.mark.parametrize("boundary_mode", [1, 2])
+@pytest.mark.parametrize("name", ["pegase9241_k16", "activsg10k_k32"])
+def test_phase_fingerprints_match_reference_at_headline_sizes(G, name, boundary_mode):
+    """BASELINE configs[2] / configs[3]: first-iteration phase outputs against the fingerprints
+    make_golden.py stored from the unmodified reference (fused_accumulate -> schur_condense ->
+    assemble_boundary -> dense_cholesky_solve at the flat start), then the per-iteration stacked norms
+    of the reference's own solve (reference test_solver.py:122-168 at the headline sizes)."""
+    from paper_2604_23175_b200._native import Plan
+    net, ms, part, g = build_case(name)
+    bord, maps = G.build_variable_maps(net, part)
+    assert bord.n_gamma == int(g["n_gamma"])
+    plan = Plan(net, ms, part, bord, maps, boundary_mode=boundary_mode)
+    st = _device_state(net)
+    plan.phase_assemble(st[0].data_ptr(), st[1].data_ptr())
+    for a in range(part.k):
+        n_i, n_b, nnz_ii, nnz_ib = (int(v) for v in g[f"a{a}_dims"])
+        assert np.array_equal(maps[a].boundary_selector, g[f"a{a}_sel"])
+        ii_ptr, ii_idx, ib_ptr, ib_idx = plan.area_pattern(a)
+        assert (len(ii_ptr) - 1, len(ii_idx), len(ib_idx)) == (n_i, nnz_ii, nnz_ib)
+        data_ii, data_ib, g_bb, b_i, b_b = plan.area_blocks(a)
+        sums = g[f"a{a}_sum_ii"]          # order-sensitive at 1e-16, compared at 1e-12 (make_golden.py)
+        assert abs(data_ii.sum() - sums[0]) <= 1e-12 * sums[1] and abs(np.abs(data_ii).sum() - sums[1]) <= 1e-12 * sums[1]
+        assert _rel(b_i, g[f"a{a}_b_i"]) < 5e-13 and _rel(b_b, g[f"a{a}_b_b"]) < 5e-13, a
+    plan.phase_condense()
+    for a in range(part.k):
+        s_b, b_hat = plan.area_schur(a)
+        assert _rel(np.diag(s_b), g[f"a{a}_sb_diag"]) < 1e-9 and _rel(b_hat, g[f"a{a}_b_hat"]) < 1e-9, a
+    plan.phase_boundary()
+    s_g, b_g, dx = plan.boundary_system()
+    assert _rel(np.diag(s_g), g["s_gamma_diag"]) < 1e-9
+    assert _rel(b_g, g["b_gamma"]) < 1e-9 and _rel(dx, g["dx_gamma"]) < 1e-9
+    plan.close()
+    # the reference's per-iteration norms, through the persistent kernel (last_deltas) and the callback loop
+    trace = []
+    est, rep = G.solve_multiarea(net, ms, part, config=G.SolverConfig(boundary={1: "dense", 2: "sparse"}[boundary_mode]),
+                                 on_iteration=lambda it, s, d: trace.append(d))
+    ref_d = g["deltas"]
+    assert rep.iterations == len(ref_d) == len(trace)
+    assert np.allclose(trace, ref_d, rtol=1e-6, atol=1e-12)
+    warm = G.MultiAreaEstimator(net, ms, part, config=G.SolverConfig(boundary={1: "dense", 2: "sparse"}[boundary_mode]))
+    est2, rep2 = warm.estimate()
+    assert np.allclose(warm.last_deltas[:rep2.iterations], ref_d, rtol=1e-6, atol=1e-12)
+    assert np.array_equal(est2.va, est.va) and np.array_equal(est2.vm, est.vm)
+    warm.close()
+
+
 def _single_area(G, net):
     part = G.partition_network(net, 1)
     _, maps = G.build_variable_maps(net, part)
