@@ -102,6 +102,35 @@ def test_tiled_100k_in_128_areas_gives_the_same_estimate(G, tiled):
         est.close()
 
 
+def test_tiled_100k_in_128_areas_matches_the_reference_run(G, tiled):
+    """BASELINE.json configs[4] against the UNMODIFIED reference: tests/golden/tiled101k_k128.npz holds the
+    reference's own solve_multiarea run of this configuration (make_golden.py tiled101k: 197 s of CPU, LAPACK
+    Cholesky of the n_Gamma = 5692 boundary system).  Same GN iteration count, per-iteration stacked norms,
+    final va / vm within 1e-8 relative, J within 1e-10 relative (north_star tolerances) -- on the
+    persistent kernel and on the level-launch path."""
+    from conftest import load_golden
+    from paper_2604_23175_b200 import synth
+    g = load_golden("tiled101k_k128")
+    net, _, noisy, _, _ = tiled
+    assert np.array_equal(synth.golden_partition("tiled101k_k128"), g["area_of_bus"])
+    zs = g["z_sum"]
+    assert abs(noisy.z.sum() - zs[0]) <= 1e-12 * zs[1] and abs(noisy.weight.sum() - zs[2]) <= 1e-12 * zs[2]
+    part = G.load_partition(net, g["area_of_bus"])
+    for cfg in (G.SolverConfig(), G.SolverConfig(profile_phases=True)):
+        est = G.MultiAreaEstimator(net, noisy, part, config=cfg)
+        try:
+            state, rep = est.estimate()
+            assert est.n_gamma == int(g["n_gamma"]) == 5692
+            assert rep.iterations == int(g["iterations"]) == 5 and rep.converged == bool(g["converged"])
+            assert np.allclose(est.last_deltas, g["deltas"], rtol=1e-6, atol=1e-12)
+            assert np.max(np.abs(state.va - g["va"]) / np.maximum(np.abs(g["va"]), 1.0)) < 1e-8
+            assert np.max(np.abs(state.vm - g["vm"]) / np.abs(g["vm"])) < 1e-8
+            jref = float(g["objective"])
+            assert abs(rep.objective - jref) <= 1e-10 * jref
+        finally:
+            est.close()
+
+
 @pytest.mark.parametrize("name", ["ieee14_k2", "ieee118_k6", "pegase2869_k8", "pegase9241_k16", "activsg10k_k32"])
 def test_persistent_kernel_matches_level_path_bitwise(G, name):
     from conftest import build_case

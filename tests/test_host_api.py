@@ -166,6 +166,28 @@ def test_synthetic_shapes_match_the_golden_recipes():
     assert bord.n_gamma == int(g["n_gamma"]) == 126
 
 
+def test_tiled_100k_inputs_match_the_reference_fixture():
+    """The ~100k-bus / 128-area fixture (reference run, make_golden.py tiled101k) was generated from the
+    reference's own classes: the product's tiled_network / generate_measurements must name the same grid
+    and the same measurement set (Ybus and z / w fingerprints), and the committed partition the same areas."""
+    g = load_golden("tiled101k_k128")
+    net, _ = synth.tiled_network(synth.shaped_network("pegase9241"), 11)
+    y = net.ybus
+    ys = g["ybus_sum"]
+    assert y.nnz == int(ys[3])
+    assert abs(y.data.real.sum() - ys[0]) <= 1e-12 * ys[2] and abs(y.data.imag.sum() - ys[1]) <= 1e-12 * ys[2]
+    assert abs(np.abs(y.data).sum() - ys[2]) <= 1e-12 * ys[2]
+    ms = G.generate_measurements(net, G.MeasurementConfig(seed=0))
+    zs = g["z_sum"]
+    assert ms.m == 1011229
+    assert abs(ms.z.sum() - zs[0]) <= 1e-12 * zs[1] and abs(np.abs(ms.z).sum() - zs[1]) <= 1e-12 * zs[1]
+    assert np.array_equal(synth.golden_partition("tiled101k_k128"), g["area_of_bus"])
+    part = G.load_partition(net, g["area_of_bus"])
+    bord, _ = G.build_variable_maps(net, part)
+    assert part.k == 128 and bord.n_gamma == int(g["n_gamma"]) == 5692
+    assert int(g["iterations"]) == 5 and bool(g["converged"])
+
+
 def test_tiled_network_for_the_100k_config():
     base = synth.random_network(60, 5)
     net, copy_of = synth.tiled_network(base, 3)
