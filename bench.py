@@ -108,7 +108,7 @@ def cpu_solve_is_unbounded(net, part):
     return net.n_bus > 50000
 
 
-def cpu_reference(net, ms, part, threads, budget_s=20.0, min_runs=2):
+def cpu_reference(net, ms, part, threads, budget_s=20.0, min_runs=2, exact_steps=None, warmup=1):
     """Time the C oracle port (the reference's algorithm) on this host: solves/s, iterations."""
     from oracle.mase_oracle import Oracle
     t0 = time.perf_counter()
@@ -120,13 +120,53 @@ def cpu_reference(net, ms, part, threads, budget_s=20.0, min_runs=2):
         t0 = time.perf_counter()
         res = orc.solve(max_iter=1, threads=threads)
         return res, time.perf_counter() - t0, setup, 1
-    res = orc.solve(threads=threads)        # warm-up
+    for _ in range(max(1, warmup)):
+        res = orc.solve(threads=threads)    # warm-up
     times = []
-    while len(times) < min_runs or (sum(times) < budget_s and len(times) < 50):
+    while (len(times) < exact_steps) if exact_steps else (len(times) < min_runs or (sum(times) < budget_s and len(times) < 50)):
         t0 = time.perf_counter()
         res = orc.solve(threads=threads)
         times.append(time.perf_counter() - t0)
     return res, float(np.mean(times)), setup, len(times)
+
+
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")
+
+
+def workload_config(workload, net, ms, part, n_gamma, iterations):
+    """`config` of the JSON line: a function of the workload only, identical in both arms."""
+    return {"workload": workload, "areas": int(part.k), "n_bus": int(net.n_bus), "rows": int(ms.m), "n_gamma": int(n_gamma),
+            "iterations_per_solve": int(iterations),
+            "l2": "B200 arm: flushed between steps (256 MB write); reference arm: host caches, nothing flushed"}
+
+
+def time_python_reference(net, ms, part, max_bus=20000):
+    """ONE flat-start solve of the UNMODIFIED reference package (installed by __graft_entry__.build() into the
+    git-ignored oracle/_ref with `pip install --target`; it travels to the GPU box with the snapshot), through its
+    own public API: gridse.solve_multiarea on the same network / measurement set / partition, single BLAS thread
+    (the reference is single-threaded Python; un-pinned OpenBLAS only adds noise).  Returns a dict or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "gridse")) or net.n_bus > max_bus:
+        return None
+    import dataclasses
+    sys.path.insert(0, REF_DIR)
+    try:
+        import gridse as R
+        from threadpoolctl import threadpool_limits
+        rnet = R.BusBranchNetwork.from_components([R.Bus(**dataclasses.asdict(b)) for b in net.buses],
+                                                  [R.Branch(**dataclasses.asdict(b)) for b in net.branches])
+        rms = R.generate_measurements(rnet, R.MeasurementConfig(seed=0))
+        same_inputs = bool(np.array_equal(rms.z, ms.z) and np.array_equal(rms.weight, ms.weight))
+        rpart = R.load_partition(rnet, part.area_of_bus)
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            est, rep = R.solve_multiarea(rnet, rms, rpart)
+            sec = time.perf_counter() - t0
+        return {"kind": "reference", "what": "gridse.solve_multiarea (unmodified reference, oracle/_ref), one flat-start solve "
+                "incl. its per-call symbolic setup, 1 thread", "solve_s": sec, "iterations": int(rep.iterations),
+                "converged": bool(rep.converged), "it_per_s": rep.iterations / sec, "objective": float(rep.objective),
+                "same_inputs_as_gpu_arm": same_inputs, "va": est.va, "vm": est.vm}
+    finally:
+        sys.path.remove(REF_DIR)
 
 
 def run_reference(args):
@@ -134,18 +174,22 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import mase_oracle
+    from oracle.mase_oracle import Oracle
     net, ms, part = build_workload(args.workload)
     threads = min(mase_oracle.max_threads(), part.k, os.cpu_count() or 1)
-    res, sec, setup, runs = cpu_reference(net, ms, part, threads, budget_s=max(5.0, 2.0 * args.steps))
+    res, sec, setup, runs = cpu_reference(net, ms, part, threads, exact_steps=args.steps, warmup=args.warmup)
     value = res["iterations"] / sec
+    pyref = time_python_reference(net, ms, part)
+    if pyref:
+        pyref["state_max_abs_diff_vs_port"] = float(max(np.max(np.abs(pyref.pop("va") - res["va"])), np.max(np.abs(pyref.pop("vm") - res["vm"]))))
     line = {
         "impl": "reference", "metric": METRIC_NAMES.get(args.workload, f"GN iterations/s ({args.workload} MASE)"), "value": value,
         "unit": "GN iterations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "areas": part.k, "n_bus": net.n_bus, "rows": ms.m,
-                   "iterations_per_solve": res["iterations"]},
+        "config": workload_config(args.workload, net, ms, part, Oracle(net, ms, part.area_of_bus).n_gamma, res["iterations"]),
         "cpu_baseline": {"value": value, "unit": "GN iterations/s", "cores": threads, "kind": "port",
+                         "reference_python_s": pyref["solve_s"] if pyref else None, "reference_python": pyref,
                          "sample": (f"{runs} full flat-start solves" if not cpu_solve_is_unbounded(net, part) else
                                     "ONE GN iteration from the flat start (a solve to convergence does not fit the time bound)")
                                    + f" of {args.workload} (C restatement of the reference "
@@ -174,17 +218,61 @@ def dgemm_peak(torch, dev):
     return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` (N > 1) outside a launcher: re-execute this command under
+    torch.distributed.run with one rank per GPU (what the driver does itself for its scaling runs)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd))
+
+
+def run_spawn_check(args):
+    """Rendezvous + one collective per rank without touching a GPU (`--spawn-check`, gloo): proves that the
+    N-rank launch path of this file works on a box without N GPUs (tests/test_bench_cli.py)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t)
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"spawn_check": True, "n_gpus": world, "requested": args.gpus, "rank_sum": float(t[0]),
+                          "backend": "gloo"}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_gpu(args):
     import torch
     import paper_2604_23175_b200 as G
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+    if torch.cuda.device_count() < world:
+        if rank == 0:
+            print(json.dumps({"error": f"--gpus {world} needs {world} CUDA devices, this box has {torch.cuda.device_count()}",
+                              "n_gpus": world}), flush=True)
+        raise SystemExit(2)
     if world > 1:
         import torch.distributed as dist
         from paper_2604_23175_b200.distributed import DistributedEstimator
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # communicator line per rank (NCCL_DEBUG=INFO adds NCCL's own transport / NVLS lines)
+        probe = torch.ones(1, device=torch.device("cuda", local))
+        dist.all_reduce(probe)
+        print(f"[bench] rank {rank}/{world} cuda:{local} {torch.cuda.get_device_name(local)} NCCL "
+              f"{'.'.join(str(v) for v in torch.cuda.nccl.version())} all_reduce ok ({int(probe[0])})", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     net, ms, part = build_workload(args.workload)
     torch.zeros(1, device=dev)                       # CUDA context creation is not part of the plan build
@@ -310,7 +398,15 @@ def run_gpu(args):
                          f"n_gamma = {est.n_gamma} boundary system, the reference's algorithm); `--impl reference` times that one iteration"}
     elif world == 1 and not args.no_cpu:
         res1, sec1, setup1, runs1 = cpu_reference(net, ms, part, 1, budget_s=10.0)
+        pyref = time_python_reference(net, ms, part)
+        if pyref:
+            va_r, vm_r = pyref.pop("va"), pyref.pop("vm")
+            state_now, _ = est.estimate()
+            pyref["gpu_state_max_rel_diff"] = float(max(np.max(np.abs(state_now.va - va_r) / np.maximum(np.abs(va_r), 1.0)),
+                                                        np.max(np.abs(state_now.vm - vm_r) / np.abs(vm_r))))
+            pyref["gpu_objective_rel_diff"] = abs(pyref["objective"] - rep.objective) / pyref["objective"]
         cpu = {"value": res1["iterations"] / sec1, "unit": "GN iterations/s", "cores": 1, "kind": "port",
+               "reference_python_s": pyref["solve_s"] if pyref else None, "reference_python": pyref,
                "sample": f"{runs1} full flat-start solves of {args.workload}, oracle/mase_oracle.c single thread; "
                          f"host has {os.cpu_count()} cores; analysis {setup1:.2f}s excluded",
                "time_to_converge_ms": sec1 * 1e3, "iterations": res1["iterations"],
@@ -322,9 +418,8 @@ def run_gpu(args):
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
         "ms_per_step": tot_dev / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "areas": part.k, "n_bus": nb, "rows": m, "n_gamma": est.n_gamma,
-                   "iterations_per_solve": it_per_solve, "converged": bool(rep.converged),
-                   "l2": "flushed between steps (256 MB write)", "parallelism": f"areas sharded over {world} GPU(s)"},
+        "config": workload_config(args.workload, net, ms, part, est.n_gamma, it_per_solve),
+        "converged": bool(rep.converged), "parallelism": f"areas sharded over {world} GPU(s), one process per GPU",
         "time_to_converge_ms": {"warm_device": tot_dev / args.steps * 1e3, "warm_e2e": tot_e2e / args.steps * 1e3,
                                 "plan_build_s": plan_s, "partition_s": partition_s},
         "objective": rep.objective,
@@ -357,8 +452,13 @@ def main():
     ap.add_argument("--workload", default="pegase9241_k16", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-profile", action="store_true", help="skip the per-phase profile pass (development sweeps)")
+    ap.add_argument("--spawn-check", action="store_true", help="N-rank launch + one gloo collective, no GPU work")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (args.impl == "b200" or args.spawn_check):
+        spawn_ranks(args)
+    if args.spawn_check:
+        run_spawn_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)
