@@ -122,7 +122,9 @@ def test_tiled_100k_in_128_areas_matches_the_reference_run(G, tiled):
             state, rep = est.estimate()
             assert est.n_gamma == int(g["n_gamma"]) == 5692
             assert rep.iterations == int(g["iterations"]) == 5 and rep.converged == bool(g["converged"])
-            assert np.allclose(est.last_deltas, g["deltas"], rtol=1e-6, atol=1e-12)
+            # (late norms are differences of nearly equal iterates: 1e-6 relative while they are above the state
+            # tolerance, 1e-10 absolute below -- the solvers differ in elimination order, not in the iterate)
+            assert np.allclose(est.last_deltas, g["deltas"], rtol=1e-6, atol=1e-10)
             assert np.max(np.abs(state.va - g["va"]) / np.maximum(np.abs(g["va"]), 1.0)) < 1e-8
             assert np.max(np.abs(state.vm - g["vm"]) / np.abs(g["vm"])) < 1e-8
             jref = float(g["objective"])
