@@ -74,6 +74,8 @@ typedef struct {
     int32_t tile_rows;       /* update-row chunk per task, multiple of 8, <= 96 (0 = default: 32 up to 30k buses, else 48) */
     int32_t boundary_mode;   /* boundary factorisation: 0 auto, 1 dense chain (dense_cholesky_solve), 2 block-sparse tree */
     void *stream;            /* cudaStream_t every kernel / copy of the plan is enqueued on; NULL = a stream of its own */
+    int32_t max_ctas;        /* cap on the CTAs of the persistent kernel (0 = every resident slot of the device);
+                              * rank plans that share one GPU must fit side by side                          */
 } gse_options;
 
 typedef struct {
@@ -207,6 +209,34 @@ int gse_exchange_offsets(const gse_plan *plan, int64_t *off);
 double *gse_boundary_delta_dev(gse_plan *plan);
 /* Device pointer to [delta_inf, failure code] as two doubles for a MAX all-reduce. */
 double *gse_status_dev(gse_plan *plan);
+
+/* ---- peer-linked multi-rank solve: the exchanges INSIDE the persistent kernel, over peer memory -------
+ * One process (or plan) per GPU; every rank runs the whole GN loop in one launch of its own.  The two
+ * exchange points of the reference loop (solver.py:277-298 gather of the areas' Schur blocks, 318-326
+ * broadcast of delta_x_Gamma) and the convergence scalar (solver.py:328-338) happen inside the kernels:
+ * area roots of rank r store (S_b | b_hat) straight into the coordinator's update storage and bump its
+ * completion counters; the coordinator's boundary back-substitution tasks store their pivots' share of
+ * delta_x_Gamma into every rank's solution vector; every rank max-merges its norm / failure code into
+ * every rank's copy.  No collective, no host round trip inside the loop; results are bit-identical to
+ * the single-rank solve.  Setup: every rank fills a gse_peer_info, the records are exchanged by the host
+ * layer (torch.distributed all_gather of the raw bytes), every rank links.  Ranks in other processes are
+ * mapped with CUDA IPC, rank plans of the same process (tests; one process driving several GPUs) with
+ * their device addresses + cudaDeviceEnablePeerAccess.  At most 8 ranks. */
+typedef struct {
+    int32_t rank, world, n_gamma_fronts, device;
+    int64_t pid;                 /* exporting process                                                  */
+    uint64_t ubuf, xsol, sync;   /* device addresses (exporting process) of the update storage, the
+                                  * solution vector and the sync block                                  */
+    uint8_t ipc[3][64];          /* cudaIpcMemHandle_t of the allocations that hold them                */
+    int64_t ipc_off[3];          /* their byte offsets inside those allocations                         */
+} gse_peer_info;
+int gse_peer_info_get(gse_plan *plan, gse_peer_info *out);
+/* all: world records ordered by rank (this rank's own included).  After a successful link gse_solve runs
+ * the peer-linked persistent kernel; gse_report.objective is NaN (J needs the merged state: gse_objective). */
+int gse_peer_link(gse_plan *plan, const gse_peer_info *all);
+/* Before EVERY gse_solve of a linked plan: clears this rank's sync block and waits for it; then the host
+ * layer barriers the ranks (no rank may launch before every block is clear), then gse_solve. */
+int gse_peer_solve_prepare(gse_plan *plan);
 
 /* ---- partitioner passes on the host (no device involved) ---------------------------------
  * One attempt of partition_network (reference partition.py:373-403; passes partition.py:198-365:

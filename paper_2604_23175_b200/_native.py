@@ -49,6 +49,18 @@ class Options(C.Structure):
         ("area_rank", i32p), ("persistent", C.c_int32), ("tile_rows", C.c_int32),
         ("boundary_mode", C.c_int32),
         ("stream", C.c_void_p),
+        ("max_ctas", C.c_int32),
+    ]
+
+
+class PeerInfo(C.Structure):
+    """gse_peer_info: what a rank publishes for the peer-linked solve (plain bytes, exchanged by the host layer)."""
+    _fields_ = [
+        ("rank", C.c_int32), ("world", C.c_int32), ("n_gamma_fronts", C.c_int32), ("device", C.c_int32),
+        ("pid", C.c_int64),
+        ("ubuf", C.c_uint64), ("xsol", C.c_uint64), ("sync", C.c_uint64),
+        ("ipc", (C.c_uint8 * 64) * 3),
+        ("ipc_off", C.c_int64 * 3),
     ]
 
 
@@ -137,6 +149,9 @@ def lib():
     L.gse_plan_stats.argtypes = [vp, f64p, C.c_int32]
     L.gse_stream.argtypes = [vp]
     L.gse_stream.restype = vp
+    L.gse_peer_info_get.argtypes = [vp, C.POINTER(PeerInfo)]
+    L.gse_peer_link.argtypes = [vp, C.POINTER(PeerInfo)]
+    L.gse_peer_solve_prepare.argtypes = [vp]
     _LIB = L
     return L
 
@@ -151,6 +166,7 @@ EXPORTED = [
     "gse_version", "gse_stream", "gse_matrix_plan_create", "gse_matrix_set_values", "gse_matrix_condense",
     "gse_matrix_recover", "gse_assemble_boundary", "gse_phase_local_async", "gse_phase_boundary_async",
     "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout", "gse_partition_attempt", "gse_partition_thin_cuts",
+    "gse_peer_info_get", "gse_peer_link", "gse_peer_solve_prepare",
 ]
 
 
@@ -231,7 +247,8 @@ class Plan:
     """Owner of one ``gse_plan`` (analysis + device program of one problem)."""
 
     def __init__(self, net, ms, part, bord, maps, *, device=0, dense=False, leaf_buses=0,
-                 max_pivots=0, rank=0, world=1, area_rank=None, tile_rows=0, boundary_mode=0, stream=None):
+                 max_pivots=0, rank=0, world=1, area_rank=None, tile_rows=0, boundary_mode=0, stream=None,
+                 max_ctas=0):
         L = lib()
         self._desc, self._keep = make_desc(net, ms, part, bord, maps)
         opt = Options()
@@ -240,6 +257,7 @@ class Plan:
         opt.rank, opt.world = int(rank), int(world)
         opt.tile_rows = int(tile_rows)
         opt.boundary_mode = int(boundary_mode)
+        opt.max_ctas = int(max_ctas)
         opt.stream = int(stream) if stream else None      # cudaStream_t of the caller (e.g. torch's current stream)
         if area_rank is not None:
             self._keep["area_rank"] = np.ascontiguousarray(area_rank, dtype=np.int32)
@@ -295,6 +313,23 @@ class Plan:
         rep = Report()
         self._call(lib().gse_solve(self._h, C.byref(cfg), va_ptr, vm_ptr, C.byref(rep)))
         return rep
+
+    # -- peer-linked multi-rank solve (exchanges inside the persistent kernel) ---------
+    def peer_info(self):
+        """This rank's ``gse_peer_info`` as bytes (for an all-gather through the host layer)."""
+        info = PeerInfo()
+        self._call(lib().gse_peer_info_get(self._h, C.byref(info)))
+        return bytes(info)
+
+    def peer_link(self, infos):
+        """``infos``: the records of all ranks, ordered by rank (bytes as returned by ``peer_info``)."""
+        arr = (PeerInfo * len(infos))()
+        for k, raw in enumerate(infos):
+            C.memmove(C.byref(arr[k]), raw, C.sizeof(PeerInfo))
+        self._call(lib().gse_peer_link(self._h, arr))
+
+    def peer_solve_prepare(self):
+        self._call(lib().gse_peer_solve_prepare(self._h))
 
     def iterate(self, va_ptr, vm_ptr):
         d = C.c_double()

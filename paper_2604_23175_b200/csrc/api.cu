@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "kernels.cuh"
 #include "plan.hpp"
 
@@ -38,7 +40,10 @@ struct DevBuf {
 };
 
 struct LevelLaunch { int pclass; int first, count; size_t smem; int phase; };
-constexpr int kBlkDelta = 0, kBlkResult = 64, kBlkErr = 65, kBlkObj = 66, kBlkStamps = 68, kBlkWords = 68 + 1 + 64 * 8;
+// (kBlkGDelta / kBlkGErr: this rank's copy of the GLOBAL per-iteration norms and of the inverted global failure
+// code of a peer-linked solve -- every rank max-merges its own values into every copy)
+constexpr int kBlkDelta = 0, kBlkResult = 64, kBlkErr = 65, kBlkObj = 66, kBlkStamps = 68, kBlkGDelta = 68 + 1 + 64 * 8,
+              kBlkGErr = kBlkGDelta + 64, kBlkWords = kBlkGErr + 2;
 struct BwdLaunch { int first, count, phase; };
 
 }  // namespace
@@ -92,9 +97,13 @@ struct gse_plan {
     DevBuf<unsigned long long> syncblk;       // [delta 64 | result | err copy | J | pad | stamps 1+512 | counters...]
     unsigned long long* h_blk = nullptr;      // pinned mirror of the first kBlkWords words
     DevBuf<unsigned long long> trace;         // per-item stamps of the persistent kernel (debug)
-    int solve_grid = 0;
+    int solve_grid = 0, max_ctas = 0;
     size_t solve_smem = 0, sync_bytes = 0;
     bool persistent = false, stamps = true;
+    // peer-linked multi-rank solve (gse_peer_link): exchanges inside the persistent kernel over peer memory
+    bool linked = false, prepared = false, shares_device = false;
+    int n_gamma_fronts = 0;
+    std::vector<void*> ipc_opened;            // allocations of other processes mapped with cudaIpcOpenMemHandle
 
     cudaGraphExec_t graph = nullptr;
     const double* graph_va = nullptr;
@@ -188,6 +197,8 @@ int enqueue_iteration(gse_plan* plan, double* va, double* vm, bool events) {
 
 int decode_failure(gse_plan* plan, unsigned long long code) {
     const int f = (int)(code >> 32), k = (int)(code & 0xffffffffull);
+    if (f < 0 || f >= (int)plan->hp.fronts.size())      // peer-linked solve: a boundary front, which only the coordinator's plan holds
+        return fail(plan, GSE_E_NOT_SPD_BOUNDARY, "boundary system not positive definite (reported by the coordinator rank)", -1, -1);
     const Front& fr = plan->hp.fronts[f];
     const int pos = fr.rows[k];
     const int orig = plan->hp.perm_orig[pos];
@@ -223,6 +234,7 @@ gse_plan::~gse_plan() {
     if (h_flags) cudaFreeHost(h_flags);
     if (h_obj) cudaFreeHost(h_obj);
     if (h_blk) cudaFreeHost(h_blk);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (int i = 0; i < 2; ++i) { if (h_stage[i]) cudaFreeHost(h_stage[i]); if (stage_done[i]) cudaEventDestroy(stage_done[i]); }
     syncblk.release(); trace.release();
     DevBuf<int32_t>* ib[] = {&y_ptr, &y_idx, &br_from, &br_to, &m_type, &m_target, &vm_bus, &vm_row, &vm_slot, &fl_branch,
@@ -271,6 +283,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         if (opt->tile_rows >= 8 && opt->tile_rows <= kMaxTile) bo.tile_rows = opt->tile_rows / 8 * 8;
         if (opt->boundary_mode >= 0 && opt->boundary_mode <= 2) bo.boundary_mode = opt->boundary_mode;
         bo.rank = opt->rank; bo.world = std::max(1, opt->world);
+        plan->max_ctas = std::max(0, opt->max_ctas);
         if (opt->area_rank) bo.area_rank.assign(opt->area_rank, opt->area_rank + d->n_areas);
     }
     if (const char* e = getenv("GSE_TILE_ROWS")) { int v = atoi(e); if (v >= 8 && v <= kMaxTile) bo.tile_rows = v / 8 * 8; }
@@ -399,8 +412,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
                 L.smem = std::max(L.smem, sizeof(double) * task_smem_doubles(f.p, ni, nj, diag, direct, kind));
                 TaskRec r{};
                 r.front = t.front; r.ci = t.ci; r.cj = t.cj; r.p = f.p; r.u1 = f.u1; r.T = T;
-                r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = (direct ? 1 : 0) | (f.n_orig > 0 ? 2 : 0);
-                r.phase = phase; r.kind = kind; r.nch = f.nch;
+                r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = (direct ? 1 : 0) | (f.n_orig > 0 ? 2 : 0) | ((f.kind == 1 && bo.world > 1 && bo.rank != 0) ? 4 : 0);
+                r.phase = phase; r.kind = kind; r.nch = f.nch; r.area = f.area;
                 r.dinv_off = dinv_off[t.front];
                 const int32_t* rp = &hp.reg_ptr[hp.front_reg_off[t.front]];
                 const int ridI = (t.ci + 1) * (t.ci + 2) / 2, ridJ = (t.cj + 1) * (t.cj + 2) / 2;
@@ -420,7 +433,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
                     cr.eP = f.p ? lb(f.p) : 0;
                     cr.bI = lb(f.p + t.ci * T); cr.eI = lb(f.p + t.ci * T + ni);
                     cr.bJ = lb(f.p + t.cj * T); cr.eJ = lb(f.p + t.cj * T + nj);
-                    cr.front = ch; cr.need = ntasks_of(ch);
+                    cr.front = (c.kind == 1 && c.area >= 0 && !hp.owned[c.area]) ? -(c.area + 1) : ch; cr.need = ntasks_of(ch);
                     const bool hits_panel = f.p && kind != 2 && cr.eP > 0;
                     const bool hits_tile = !direct && kind != 1 && cr.eI > cr.bI && cr.eJ > cr.bJ;
                     if (!hits_panel && !hits_tile && !direct) continue;   // pruned (order of the rest is kept)
@@ -501,7 +514,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         sp.m_type = plan->m_type.ptr; sp.m_target = plan->m_target.ptr; sp.br_from = plan->br_from.ptr; sp.br_to = plan->br_to.ptr;
         sp.gval = plan->gval.ptr; sp.lbuf = plan->lbuf.ptr; sp.ubuf = plan->ubuf.ptr; sp.xsol = plan->xsol.ptr;
         sp.bpart = plan->bpart.ptr; sp.obj_partial = plan->obj_partial.ptr; sp.bcnt = plan->bcnt.ptr;
-        const size_t nctr = CTR_FRONT0 + 3 * nf;
+        sp.front0 = ctr_front0(hp.n_areas);
+        const size_t nctr = sp.front0 + 3 * nf;
         plan->sync_bytes = sizeof(unsigned long long) * kBlkWords + sizeof(unsigned) * nctr;
         CU(plan->syncblk.alloc(kBlkWords + (nctr + 1) / 2));
         CU(cudaMallocHost(&plan->h_blk, sizeof(unsigned long long) * kBlkWords));
@@ -523,8 +537,10 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
             if (const char* e = getenv("GSE_FUSED_UPDATE")) fuse = atoi(e) != 0;
             if (fuse) { sp.items_per_it -= sp.n_upd_items; sp.n_upd_items = 0; }
             plan->solve_grid = std::min(cap, sp.items_per_it);
+            if (plan->max_ctas > 0) plan->solve_grid = std::min(plan->solve_grid, plan->max_ctas);
             plan->persistent = true;
         }
+        for (auto& f : hp.fronts) if (f.kind == 3 && f.p > 0) ++plan->n_gamma_fronts;
     }
     CU(cudaDeviceSynchronize());
     plan->err.code = GSE_OK; plan->err.area = -1; plan->err.pivot = -1; plan->err.message[0] = 0;
@@ -637,8 +653,15 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 32 * (size_t)sp.items_per_it * 16, s));
     auto t0 = std::chrono::steady_clock::now();
     cudaEventRecord(plan->ev[6], s);
-    CU(cudaMemsetAsync(plan->syncblk.ptr, 0, plan->sync_bytes, s));
-    CU(launch_solve(sp, plan->ep, plan->ft, va, vm, plan->solve_grid, plan->solve_smem, s));
+    if (plan->linked) {
+        // the sync block was cleared by gse_peer_solve_prepare BEFORE the ranks' barrier: a peer that starts
+        // first may already be counting its area roots into it
+        if (!plan->prepared) return fail(plan, GSE_E_INVALID, "peer-linked plan: call gse_peer_solve_prepare (then barrier the ranks) before gse_solve");
+        plan->prepared = false;
+    } else {
+        CU(cudaMemsetAsync(plan->syncblk.ptr, 0, plan->sync_bytes, s));
+    }
+    CU(launch_solve(sp, plan->ep, plan->ft, va, vm, plan->solve_grid, plan->solve_smem, s, !plan->shares_device));
     CU(cudaMemcpyAsync(plan->h_blk, plan->syncblk.ptr, sizeof(unsigned long long) * kBlkWords, cudaMemcpyDeviceToHost, s));
     cudaEventRecord(plan->ev[7], s);
     CU(cudaStreamSynchronize(s));
@@ -648,7 +671,8 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     const int32_t* res = reinterpret_cast<const int32_t*>(blk + kBlkResult);
     rep->iterations = res[0]; rep->converged = res[1];
     plan->launches_last = 1;
-    for (int it = 0; it < rep->iterations && it < 64; ++it) memcpy(&rep->delta_inf[it], &blk[kBlkDelta + it], sizeof(double));
+    for (int it = 0; it < rep->iterations && it < 64; ++it)
+        memcpy(&rep->delta_inf[it], &blk[(plan->linked ? kBlkGDelta : kBlkDelta) + it], sizeof(double));
     if (plan->stamps) {
         // phase end stamps (globaltimer ns) per iteration: 0 eval, 1 accumulate, 2 local condense,
         // 3 boundary assemble, 4 boundary factor, 5 boundary back-substitution, 6 recovery, 7 update.
@@ -671,6 +695,7 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
         return decode_failure(plan, blk[kBlkErr]);
     }
     memcpy(&rep->objective, &blk[kBlkObj], sizeof(double));
+    if (plan->linked) rep->objective = std::nan("");      // J needs the merged state of all ranks: gse_objective afterwards
     return GSE_OK;
 }
 
@@ -977,6 +1002,108 @@ int gse_set_boundary_delta(gse_plan* plan, const double* dx_gamma) {
     return GSE_OK;
 }
 
+// ---- peer-linked multi-rank solve: the exchanges inside the persistent kernel, over peer memory --------------
+// (reference solver.py:277-298 gather of the Schur blocks, 318-326 broadcast of delta_x_Gamma, 328-338 the
+// convergence scalar)
+static cudaError_t allocation_base(const void* p, unsigned long long* base) {
+    typedef int (*range_fn)(unsigned long long*, size_t*, unsigned long long);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &qr);
+    if (e != cudaSuccess) return e;
+    if (!fn || qr != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
+    size_t size = 0;
+    return reinterpret_cast<range_fn>(fn)(base, &size, (unsigned long long)(uintptr_t)p) == 0 ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int gse_peer_info_get(gse_plan* plan, gse_peer_info* out) {
+    CU(cudaSetDevice(plan->device));
+    memset(out, 0, sizeof *out);
+    const HostProgram& hp = plan->hp;
+    out->rank = hp.rank; out->world = hp.world; out->device = plan->device;
+    out->n_gamma_fronts = plan->n_gamma_fronts;
+    out->pid = (int64_t)getpid();
+    unsigned long long* blk = plan->syncblk.ptr;
+    const void* ptrs[3] = {plan->ubuf.ptr, plan->xsol.ptr, blk};
+    out->ubuf = (uint64_t)(uintptr_t)plan->ubuf.ptr; out->xsol = (uint64_t)(uintptr_t)plan->xsol.ptr;
+    out->sync = (uint64_t)(uintptr_t)blk;
+    for (int k = 0; k < 3; ++k) {
+        unsigned long long base = 0;
+        CU(allocation_base(ptrs[k], &base));
+        out->ipc_off[k] = (int64_t)((unsigned long long)(uintptr_t)ptrs[k] - base);
+        cudaIpcMemHandle_t h;
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        CU(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+        memcpy(out->ipc[k], &h, 64);
+    }
+    return GSE_OK;
+}
+
+int gse_peer_link(gse_plan* plan, const gse_peer_info* all) {
+    CU(cudaSetDevice(plan->device));
+    const HostProgram& hp = plan->hp;
+    const int world = hp.world, rank = hp.rank;
+    if (world < 2) return fail(plan, GSE_E_INVALID, "gse_peer_link: the plan is not rank-sharded (world < 2)");
+    if (world > kMaxPeers) return fail(plan, GSE_E_INVALID, "gse_peer_link: at most 8 ranks (one node); larger worlds use the collective driver");
+    SolveProg& sp = plan->sp;
+    if (sp.items_per_it <= 0 || sp.n_upd_items <= 0) return fail(plan, GSE_E_INVALID, "gse_peer_link: this rank has no work items");
+    PeerLink lk{};
+    lk.rank = rank; lk.world = world;
+    const int64_t pid = (int64_t)getpid();
+    for (int q = 0; q < world; ++q) {
+        const gse_peer_info& pi = all[q];
+        if (pi.rank != q || pi.world != world) return fail(plan, GSE_E_INVALID, "gse_peer_link: peer records must be ordered by rank and share the world size");
+        unsigned char* base[3];
+        if (q == rank || pi.pid == pid) {
+            // same address space (this rank, or rank plans that share a process): the device addresses as they are
+            base[0] = (unsigned char*)(uintptr_t)pi.ubuf; base[1] = (unsigned char*)(uintptr_t)pi.xsol; base[2] = (unsigned char*)(uintptr_t)pi.sync;
+            if (q != rank && pi.device == plan->device) plan->shares_device = true;
+            if (pi.device != plan->device) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(pi.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) return fail(plan, GSE_E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+            }
+        } else {
+            for (int k = 0; k < 3; ++k) {
+                cudaIpcMemHandle_t h;
+                memcpy(&h, pi.ipc[k], 64);
+                void* mapped = nullptr;
+                CU(cudaIpcOpenMemHandle(&mapped, h, cudaIpcMemLazyEnablePeerAccess));
+                plan->ipc_opened.push_back(mapped);
+                base[k] = (unsigned char*)mapped + pi.ipc_off[k];
+            }
+        }
+        unsigned long long* blk = reinterpret_cast<unsigned long long*>(base[2]);
+        lk.xsol[q] = reinterpret_cast<double*>(base[1]);
+        lk.ctr[q] = reinterpret_cast<unsigned*>(blk + kBlkWords);
+        lk.gdelta[q] = blk + kBlkGDelta;
+        lk.gerr[q] = blk + kBlkGErr;
+        if (q == 0) {
+            lk.root_ctr = lk.ctr[0];
+            lk.n_gamma_fronts = pi.n_gamma_fronts;
+            plan->ft.ubuf_root = rank == 0 ? nullptr : reinterpret_cast<double*>(base[0]);
+        }
+    }
+    sp.lk = lk;
+    // all ranks run the persistent kernel; the state update stays in its own items (they also refresh this
+    // rank's replica of the boundary state, and the last one publishes the rank's norm)
+    const int cap = solve_kernel_max_ctas(plan->solve_smem, plan->device);
+    if (cap <= 0) return fail(plan, GSE_E_CUDA, "persistent solve kernel does not fit this device");
+    plan->solve_grid = std::min(cap, sp.items_per_it);
+    if (plan->max_ctas > 0) plan->solve_grid = std::min(plan->solve_grid, plan->max_ctas);
+    plan->persistent = true; plan->linked = true; plan->prepared = false;
+    return GSE_OK;
+}
+
+int gse_peer_solve_prepare(gse_plan* plan) {
+    CU(cudaSetDevice(plan->device));
+    if (!plan->linked) return fail(plan, GSE_E_INVALID, "gse_peer_solve_prepare: the plan is not peer-linked");
+    CU(cudaMemsetAsync(plan->syncblk.ptr, 0, plan->sync_bytes, plan->stream));
+    CU(cudaStreamSynchronize(plan->stream));
+    plan->prepared = true;
+    return GSE_OK;
+}
+
 double* gse_exchange_buffer_dev(gse_plan* plan, int64_t* n) { if (n) *n = plan->hp.xchg_len; return plan->ubuf.ptr + plan->hp.xchg_off; }
 int gse_exchange_offsets(const gse_plan* plan, int64_t* off) {
     for (size_t i = 0; i < plan->hp.xchg_area_off.size(); ++i) off[i] = plan->hp.xchg_area_off[i];
@@ -1053,6 +1180,20 @@ int gse_debug_trace(gse_plan* plan, int enable, unsigned long long* out, int64_t
     if (out && plan->trace.ptr) CU(cudaMemcpy(out, plan->trace.ptr, sizeof(unsigned long long) * std::min<size_t>(max_words, words), cudaMemcpyDeviceToHost));
     plan->sp.trace = nullptr;
     return plan->sp.items_per_it;
+}
+// Debug: arm the watchdog record of the persistent kernel.  buf = host memory from cudaHostAlloc(mapped) with
+// 4 words per CTA ({counter address, target, value seen, 1} of a wait that timed out), ms = watchdog period.
+// out[0..2] = device addresses of this plan's counter block, update storage, solution vector (to decode records).
+int gse_debug_watchdog(gse_plan* plan, unsigned long long** buf, int32_t ms, uint64_t* out) {
+    CU(cudaSetDevice(plan->device));
+    static unsigned long long* host = nullptr;
+    if (!host) { CU(cudaHostAlloc(&host, sizeof(unsigned long long) * 4 * 1024, cudaHostAllocMapped)); memset(host, 0, sizeof(unsigned long long) * 4 * 1024); }
+    unsigned long long* dev = nullptr;
+    CU(cudaHostGetDevicePointer(&dev, host, 0));
+    CU(solve_kernel_debug_watchdog(dev, (unsigned long long)ms * 1000000ull));
+    if (buf) *buf = host;
+    if (out) { out[0] = (uint64_t)(uintptr_t)plan->sp.ctr; out[1] = (uint64_t)(uintptr_t)plan->ubuf.ptr; out[2] = (uint64_t)(uintptr_t)plan->xsol.ptr; }
+    return GSE_OK;
 }
 // Item layout of one iteration of the persistent kernel: eval, accumulate, front, backward, update counts.
 int gse_solve_layout(const gse_plan* plan, int32_t* out) {

@@ -545,7 +545,8 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
         const int nbi = round8(ni) >> 3, nbj = round8(nj) >> 3;
         const int ngj = (nbj + 3) >> 2;                 // groups of four 8-wide column blocks
         const int kend = (p + 3) & ~3;
-        double* U = ubuf + hdr.u_off;
+        // (an area root of a non-coordinator rank stores S_b | b_hat straight into the coordinator's buffer)
+        double* U = (((hdr.flags & 4) && ft.ubuf_root) ? ft.ubuf_root : ubuf) + hdr.u_off;
         const double* Uc = direct ? ubuf + crec[0].u_off : nullptr;   // chain: F_IJ lives in the child's U
         for (int w = warp; w < nbi * ngj; w += nwarps) {
             const int bi = w / ngj, gj = w % ngj;

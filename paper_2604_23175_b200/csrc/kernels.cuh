@@ -28,11 +28,16 @@ struct TaskRec {                                      // 128 bytes
     int64_t gval_off, l_off, u_off;
     int32_t flags, dinv_off;                          // flags bit 0: tile read directly from the single child's U;
                                                       //       bit 1: the front has original entries (waits for the accumulation)
-    int32_t phase, kind, nch, pad[5];                 // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
+                                                      //       bit 2: area root of a non-coordinator rank -- its update matrix (S_b | b_hat)
+                                                      //              goes straight into the coordinator's exchange buffer (peer memory)
+    int32_t phase, kind, nch, area, pad[4];           // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
                                                       // kind: 0 fused, 1 panel, 2 update (front_body.cuh); nch: row chunks of the front
+                                                      // area: owning area of the front (-1: boundary front)
 };
 // One child of a task (children that do not reach the task's regions are pruned on the host).
 // front / need: dataflow dependency -- the child is complete when its counter reaches need per iteration.
+// front < 0: the root of area -(front + 1), owned by another rank -- its tiles arrive over peer memory and are
+// counted per area (CTR_AREA0).
 struct ChildRec { int64_t u_off; int32_t rel_off, eP, bI, eI, bJ, eJ; int32_t front, need, pad[2]; };   // 48 bytes
 // dep: nearest ancestor front with pivots (-1: none); need: forward tasks of the own front
 struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, dinv_off; int64_t l_off; int32_t dep, need, phase, pad[3]; };   // 64 bytes
@@ -50,6 +55,8 @@ struct FrontTab {
     const int32_t *rows_off, *rows;        // global positions of [pivots | update rows]
     const ChildRec* crecs;          // per-task child records
     double* dinv;                          // reciprocal pivots per front (written forward, read backward)
+    double* ubuf_root;                     // peer-linked multi-rank solve: the coordinator's update storage (tasks with flag bit 2
+                                           // write there); nullptr = this rank's own
     long long* tbuf;                       // optional per-task phase clocks (debug), 8 per task
     const void* task0;                     // base of the task array (indexes tbuf)
 };
@@ -106,12 +113,36 @@ cudaError_t configure_unit_kernels();
 // CTAs pull item indices from a global counter and spin on per-front completion counters.
 constexpr int kSolveThreads = 256;
 constexpr int kEvalPerItem = 256, kUpdPerItem = 1024;
-enum { CTR_NEXT = 0, CTR_EVAL = 32, CTR_ACC = 64, CTR_FWD = 96, CTR_BWD = 128, CTR_UPD = 160, CTR_OBJ = 192, CTR_FRONT0 = 224 };
-// per-front counters after CTR_FRONT0: fdone[n_fronts] (tasks that wrote U), pdone[n_fronts] (tasks that
-// stored a factor panel), bdone[n_fronts] (backward solves)
+enum { CTR_NEXT = 0, CTR_EVAL = 32, CTR_ACC = 64, CTR_FWD = 96, CTR_BWD = 128, CTR_UPD = 160, CTR_OBJ = 192,
+       CTR_GAMMA = 224,      // peer-linked solve: boundary fronts whose share of delta_x_Gamma has arrived from the coordinator
+       CTR_ITER = 256,       // peer-linked solve: ranks that have finished (and published the norm of) an iteration
+       CTR_AREA0 = 288 };    // peer-linked solve: per AREA, tasks of its root that have stored their tile of (S_b | b_hat) in the
+                             // coordinator's buffer (fronts are numbered per rank, areas are not)
+// per-front counters from SolveProg::front0 = CTR_AREA0 + n_areas rounded up to 32: fdone[n_fronts] (tasks that
+// wrote U), pdone[n_fronts] (tasks that stored a factor panel), bdone[n_fronts] (backward solves)
+inline __host__ __device__ int ctr_front0(int n_areas) { return CTR_AREA0 + ((n_areas + 31) / 32) * 32; }
+
+// Peer-linked multi-rank solve (one process per GPU, areas sharded over the ranks; reference solver.py:277-298,
+// 318-326 are the two exchange points).  Every rank runs gn_solve_kernel over its own items; the exchanges happen
+// INSIDE the kernels over peer-mapped memory (NVLink): the area roots of a rank write (S_b | b_hat) straight into
+// the coordinator's update storage and bump the coordinator's completion counters, the coordinator's boundary
+// back-substitution tasks store their pivots' share of delta_x_Gamma into every rank's solution vector, and the
+// per-iteration norm / failure code are max-merged into every rank's copy, so all ranks take the same decision.
+constexpr int kMaxPeers = 8;
+struct PeerLink {
+    int32_t rank, world;               // world == 1: not linked (single-rank plan)
+    int32_t n_gamma_fronts;            // boundary fronts with pivots (pieces delta_x_Gamma arrives in)
+    int32_t pad;
+    unsigned* root_ctr;                // the coordinator's counter block (fdone of the area roots lives there)
+    double* xsol[kMaxPeers];           // every rank's solution vector
+    unsigned* ctr[kMaxPeers];          // every rank's counter block (CTR_GAMMA, CTR_ITER)
+    unsigned long long* gdelta[kMaxPeers];   // every rank's copy of the global per-iteration norm [64]
+    unsigned long long* gerr[kMaxPeers];     // every rank's copy of the global failure code, stored inverted (0 = none)
+};
 struct SolveProg {
     int32_t n_eval_items, n_acc_items, n_tasks, n_btasks, n_upd_items, items_per_it;
     int32_t n_units, n_upd, n_bwd_fronts, n_fronts, n_rows, max_it;
+    int32_t front0, pad0;         // offset of the per-front counters inside ctr (ctr_front0(n_areas))
     int64_t n_gval;
     double tol;
     const TaskRec* tasks;
@@ -132,11 +163,13 @@ struct SolveProg {
     unsigned long long* err_out;  // copy of *err for the single readback
     double* obj_out;              // J(x) at the final state
     unsigned long long* trace;    // optional per-item stamps [item][8]: pull, originals ready, children ready, end, smid (debug)
+    PeerLink lk;                  // multi-rank exchange over peer memory (world == 1: unused)
 };
 size_t solve_kernel_static_smem();
+cudaError_t solve_kernel_debug_watchdog(unsigned long long* host_mapped, unsigned long long ns);
 // returns the number of co-resident CTAs (0 on failure)
 int solve_kernel_max_ctas(size_t dyn_smem, int device);
 cudaError_t launch_solve(const SolveProg& sp, const EvalProg& ep, const FrontTab& ft, double* va, double* vm,
-                         int grid, size_t dyn_smem, cudaStream_t s);
+                         int grid, size_t dyn_smem, cudaStream_t s, bool cooperative = true);
 
 }  // namespace gse

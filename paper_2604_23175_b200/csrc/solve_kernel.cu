@@ -33,21 +33,45 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire64_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 // Spin until *p >= target.  Called by ONE thread per dependency (the rest of the CTA parks on a
 // barrier, which costs no issue slots); the back-off keeps a waiting CTA from stealing load/store
 // bandwidth from the CTA it shares the SM with -- often the very producer it is waiting for.
-__device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target) {
+// Debug record of a wait that ran into the watchdog: [cta][4] = {counter address, target, value seen, 1} in
+// host-mapped memory (it outlives the aborted context); armed by gse_debug_watchdog, nullptr otherwise.
+__device__ unsigned long long* g_stuck = nullptr;
+__device__ unsigned long long g_watchdog_ns = 10000000000ull;
+// sys: the counter is bumped by another GPU over peer memory (peer-linked multi-rank solve).
+__device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target, bool sys = false) {
     unsigned polls = 0;
     unsigned long long t0 = 0;
-    while (ld_acquire(p) < target) {
+    unsigned v;
+    while ((v = (sys ? ld_acquire_sys(p) : ld_acquire(p))) < target) {
         __nanosleep(40);
         // watchdog: a dependency that never completes would hang the device; after ~10 s of waiting
         // the kernel aborts instead (the launch then fails with an error the host reports)
-        if ((++polls & 0xffffu) == 0) {
+        if ((++polls & 0xfffu) == 0) {
             unsigned long long now;
             asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
             if (t0 == 0) t0 = now;
-            else if (now - t0 > 10000000000ull) __trap();
+            else if (now - t0 > g_watchdog_ns) {
+                if (g_stuck) {
+                    unsigned long long* d = g_stuck + 4 * (size_t)((blockIdx.x + 97u * gridDim.x) & 1023u);   // (rank plans sharing a device differ in grid size)
+                    d[0] = (unsigned long long)(size_t)p; d[1] = target; d[2] = v; d[3] = 1ull;
+                    __threadfence_system();
+                    if (now - t0 < 2 * g_watchdog_ns) continue;      // let the other waiters leave their records too
+                }
+                __trap();
+            }
         }
     }
 }
@@ -67,15 +91,27 @@ struct SpinWait {
     unsigned epoch;          // iteration + 1
     unsigned acc_target;
     unsigned long long* tr;  // trace slots of this item (debug) or nullptr
-    int n_fronts;
+    int n_fronts, front0;
+    bool sys;                // peer-linked solve: child counters may be bumped by other GPUs
+    unsigned gamma_need;     // non-coordinator ranks: pieces of delta_x_Gamma to wait for (0: none)
+    // completion counter of a child: its front's, or -- root of an area another rank owns -- the area's
+    __device__ __forceinline__ const unsigned* child_ctr(int cf) const { return cf >= 0 ? ctr + front0 + cf : ctr + CTR_AREA0 + (-cf - 1); }
     // backward tasks: own factor complete (all its panel-storing tasks), then the nearest ancestor solved
     __device__ __forceinline__ void factor(const BwdTask& tk) const {
-        if (threadIdx.x == 0) wait_ge(ctr + CTR_FRONT0 + n_fronts + tk.front, (unsigned)tk.need * epoch);
+        if (threadIdx.x == 0) wait_ge(ctr + front0 + n_fronts + tk.front, (unsigned)tk.need * epoch);
         __syncthreads();
     }
     __device__ __forceinline__ void parent(const BwdTask& tk) const {
-        if (tk.dep < 0) return;
-        if (threadIdx.x == 0) { wait_ge(ctr + CTR_FRONT0 + 2 * n_fronts + tk.dep, epoch); if (tr) tr[2] = globaltimer(); }
+        if (tk.dep < 0) {
+            // no ancestor with pivots on this rank: on a non-coordinator rank the boundary values come from the
+            // coordinator's back-substitution tasks, piece by piece, over peer memory
+            if (gamma_need) {
+                if (threadIdx.x == 0) { wait_ge(ctr + CTR_GAMMA, gamma_need * epoch, true); if (tr) tr[2] = globaltimer(); }
+                __syncthreads();
+            }
+            return;
+        }
+        if (threadIdx.x == 0) { wait_ge(ctr + front0 + 2 * n_fronts + tk.dep, epoch); if (tr) tr[2] = globaltimer(); }
         __syncthreads();
     }
     __device__ __forceinline__ void originals(const TaskRec& hdr) const {
@@ -85,14 +121,14 @@ struct SpinWait {
     }
     __device__ __forceinline__ void panels(const TaskRec& hdr) const {
         if (threadIdx.x == 0) {
-            wait_ge(ctr + CTR_FRONT0 + n_fronts + hdr.front, (unsigned)hdr.nch * epoch);
+            wait_ge(ctr + front0 + n_fronts + hdr.front, (unsigned)hdr.nch * epoch);
             if (tr) tr[5] = globaltimer();
         }
         __syncthreads();
     }
     __device__ __forceinline__ void children(const TaskRec& hdr, const ChildRec* cr) const {
         for (int c = threadIdx.x; c < hdr.nchild; c += blockDim.x) {
-            wait_ge(ctr + CTR_FRONT0 + cr[c].front, (unsigned)cr[c].need * epoch);
+            wait_ge(child_ctr(cr[c].front), (unsigned)cr[c].need * epoch, sys);
             if (tr) atomicMax(tr + 2, globaltimer());
         }
         __syncthreads();
@@ -101,9 +137,10 @@ struct SpinWait {
     // of the batch are complete as well (without waiting for them).  cr = records of the batch.
     __device__ __forceinline__ int ready_children(const TaskRec&, const ChildRec* cr, int c, int nb, int* s_n) const {
         if (threadIdx.x == 0) {
-            wait_ge(ctr + CTR_FRONT0 + cr[c].front, (unsigned)cr[c].need * epoch);
+            wait_ge(child_ctr(cr[c].front), (unsigned)cr[c].need * epoch, sys);
             int n = 1;
-            while (c + n < nb && ld_acquire(ctr + CTR_FRONT0 + cr[c + n].front) >= (unsigned)cr[c + n].need * epoch) ++n;
+            while (c + n < nb && (sys ? ld_acquire_sys(child_ctr(cr[c + n].front)) : ld_acquire(child_ctr(cr[c + n].front)))
+                                     >= (unsigned)cr[c + n].need * epoch) ++n;
             *s_n = n;
             if (tr) tr[2] = globaltimer();
         }
@@ -128,12 +165,15 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
     if (tid == 0) mbar_init(&s_bar, 1);
     __syncthreads();
     unsigned* ctr = sp.ctr;
-    unsigned* fdone = ctr + CTR_FRONT0;
+    unsigned* fdone = ctr + sp.front0;
     unsigned* pdone = fdone + sp.n_fronts;
     unsigned* bdone = pdone + sp.n_fronts;
     const int o_acc = sp.n_eval_items, o_front = o_acc + sp.n_acc_items, o_bwd = o_front + sp.n_tasks,
               o_upd = o_bwd + sp.n_btasks;
     const bool fused_update = sp.n_upd_items == 0;      // latency-bound plans: the update rides on the backward tasks
+    const PeerLink& lk = sp.lk;
+    const bool linked = lk.world > 1;                   // areas sharded over several GPUs, exchanges over peer memory
+    const unsigned gamma_need = (linked && lk.rank != 0) ? (unsigned)lk.n_gamma_fronts : 0u;
     if (sp.stamps && blockIdx.x == 0 && tid == 0) sp.stamps[0] = globaltimer();
 #define GSE_STAMP(it, k) do { if (sp.stamps) atomicMax(sp.stamps + 1 + 8 * (it) + (k), globaltimer()); } while (0)
 
@@ -151,6 +191,17 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             if (tid == 0) {
                 int stop = 0;
                 for (int j = known + 1; j <= it && !stop; ++j) {
+                    if (linked) {
+                        // every rank has finished iteration j and max-merged its norm / failure code into this
+                        // rank's copy: all ranks read the same values and take the same decision
+                        wait_ge(ctr + CTR_ITER, (unsigned)lk.world * (unsigned)j, true);
+                        const unsigned long long ge = ld_acquire64_sys(lk.gerr[lk.rank]);
+                        const double gd = __longlong_as_double((long long)ld_acquire64_sys(lk.gdelta[lk.rank] + (j - 1)));
+                        if (ge != 0ull) stop = 2 * 65536 + j;
+                        else if (gd < sp.tol) stop = 1 * 65536 + j;
+                        else if (j == sp.max_it) stop = 3 * 65536 + j;
+                        continue;
+                    }
                     if (fused_update) {
                         wait_ge(ctr + CTR_BWD, (unsigned)sp.n_bwd_fronts * (unsigned)j);     // every front solved, state updated
                         wait_ge(ctr + CTR_FWD, (unsigned)sp.n_tasks * (unsigned)j);
@@ -199,11 +250,18 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
                 tr[6] = (unsigned long long)S.hdr.kind | ((unsigned long long)S.hdr.front << 8) | ((unsigned long long)S.hdr.ci << 32) | ((unsigned long long)S.hdr.cj << 48);
                 tr[7] = (unsigned long long)S.hdr.p | ((unsigned long long)S.hdr.u1 << 16) | ((unsigned long long)S.hdr.nchild << 32) | ((unsigned long long)S.hdr.phase << 48);
             }
-            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr, sp.n_fronts};
+            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr, sp.n_fronts, sp.front0, linked, 0u};
             if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
             else front_task_body<0>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
             __syncthreads();
-            if (tid == 0) {
+            if (tid == 0 && linked && (S.hdr.flags & 4)) {
+                // area root of a non-coordinator rank: its tile of (S_b | b_hat) sits in the coordinator's
+                // memory; the coordinator's boundary fronts wait on THEIR counter of this front
+                __threadfence_system();
+                atomicAdd_system(lk.root_ctr + CTR_AREA0 + S.hdr.area, 1u);
+                atomicAdd(ctr + CTR_FWD, 1u);
+                GSE_STAMP(it, 1 + S.hdr.phase);
+            } else if (tid == 0) {
                 __threadfence();
                 const int kind = S.hdr.p ? S.hdr.kind : 0;
                 if (kind != 2 && S.hdr.p && S.hdr.ci == S.hdr.cj) atomicAdd(pdone + S.hdr.front, 1u);
@@ -214,8 +272,23 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
         } else if (loc < o_upd) {
             // ---- backward substitution task ---------------------------------------------------------
             const BwdTask tk = sp.btasks[loc - o_bwd];
-            const SpinWait w{ctr, epoch, 0u, tr, sp.n_fronts};
+            const SpinWait w{ctr, epoch, 0u, tr, sp.n_fronts, sp.front0, linked, gamma_need};
             const bool solved = backward_body(*reinterpret_cast<BwdScratch*>(sm), tk, ft, sp.lbuf, sp.xsol, sp.bpart, sp.bcnt, w);
+            if (solved && linked && lk.rank == 0 && tk.phase == 3) {
+                // coordinator, boundary front: this front's pivots are a piece of delta_x_Gamma -- store it into every
+                // rank's solution vector (peer memory) and count the piece there (reference solver.py:318-326: the
+                // broadcast of delta_x_Gamma, here tile by tile as the back-substitution produces it)
+                if (tid < tk.p) {
+                    const int pos = ft.rows[tk.rows_off + tid];
+                    const double x = ldc(sp.xsol + pos);
+                    for (int q = 1; q < lk.world; ++q) lk.xsol[q][pos] = x;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence_system();
+                    for (int q = 1; q < lk.world; ++q) atomicAdd_system(lk.ctr[q] + CTR_GAMMA, 1u);
+                }
+            }
             if (solved && !fused_update) {
                 if (tid == 0) {
                     __threadfence();
@@ -257,6 +330,7 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             if (tid == 0) {
                 wait_ge(ctr + CTR_BWD, (unsigned)sp.n_bwd_fronts * epoch);
                 wait_ge(ctr + CTR_FWD, (unsigned)sp.n_tasks * epoch);
+                if (gamma_need) wait_ge(ctr + CTR_GAMMA, gamma_need * epoch, true);     // this rank's replica of x_Gamma is updated here too
                 if (tr) tr[2] = globaltimer();
             }
             __syncthreads();
@@ -275,7 +349,21 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
             if (tid == 0) {
                 for (int k = 1; k < kSolveThreads / 32; ++k) bits = s_red[k] > bits ? s_red[k] : bits;
                 if (bits) atomicMax(sp.delta + it, bits);
-                signal(ctr + CTR_UPD);
+                __threadfence();
+                const unsigned before = atomicAdd(ctr + CTR_UPD, 1u);
+                if (linked && before + 1u == (unsigned)sp.n_upd_items * epoch) {
+                    // last update item of this rank's iteration: max-merge the rank's norm and failure code into every
+                    // rank's copy, then count this rank as done there (the convergence scalar of solver.py:328-338;
+                    // one 8-byte atomic per peer instead of a collective)
+                    __threadfence();
+                    const unsigned long long d = ld_acquire64(sp.delta + it), e = ld_acquire64(sp.err);
+                    for (int q = 0; q < lk.world; ++q) {
+                        if (d) atomicMax_system(lk.gdelta[q] + it, d);
+                        if (e != ~0ull) atomicMax_system(lk.gerr[q], ~e);
+                    }
+                    __threadfence_system();
+                    for (int q = 0; q < lk.world; ++q) atomicAdd_system(lk.ctr[q] + CTR_ITER, 1u);
+                }
                 GSE_STAMP(it, 7);
             }
         }
@@ -284,8 +372,12 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
     }
 #undef GSE_STAMP
 
-    if (blockIdx.x == 0 && tid == 0) { sp.result[0] = final_it; sp.result[1] = converged; *sp.err_out = ld_acquire64(sp.err); }
-    if (failed) return;
+    if (blockIdx.x == 0 && tid == 0) {
+        sp.result[0] = final_it; sp.result[1] = converged;
+        *sp.err_out = linked ? ~ld_acquire64_sys(lk.gerr[lk.rank]) : ld_acquire64(sp.err);
+    }
+    // (peer-linked ranks hold only their own interiors: J is evaluated by the host layer on the merged state)
+    if (failed || linked) return;
 
     // ---- objective J(x) at the final state: per-block partials, last CTA adds them in block order ----
     double* red = sm;
@@ -316,6 +408,11 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
     if (tid == 0) *sp.obj_out = red[0];
 }
 
+cudaError_t solve_kernel_debug_watchdog(unsigned long long* host_mapped, unsigned long long ns) {
+    cudaError_t e = cudaMemcpyToSymbol(g_stuck, &host_mapped, sizeof host_mapped);
+    return e == cudaSuccess ? cudaMemcpyToSymbol(g_watchdog_ns, &ns, sizeof ns) : e;
+}
+
 size_t solve_kernel_static_smem() {
     cudaFuncAttributes a{};
     if (cudaFuncGetAttributes(&a, gn_solve_kernel) != cudaSuccess) return 0;
@@ -330,10 +427,16 @@ int solve_kernel_max_ctas(size_t dyn_smem, int device) {
     return per_sm * sms;
 }
 
+// cooperative: the launch itself guarantees that the whole grid is resident.  Rank plans that SHARE one device
+// (peer-linked plans of one process on one GPU: tests, emulation) are launched plainly instead -- cooperative
+// launches do not overlap with each other, and those kernels wait for one another; their grids are capped by the
+// caller (gse_options.max_ctas) so that all of them fit side by side.
 cudaError_t launch_solve(const SolveProg& sp, const EvalProg& ep, const FrontTab& ft, double* va, double* vm,
-                         int grid, size_t dyn_smem, cudaStream_t s) {
+                         int grid, size_t dyn_smem, cudaStream_t s, bool cooperative) {
     void* args[] = {(void*)&sp, (void*)&ep, (void*)&ft, (void*)&va, (void*)&vm};
-    return cudaLaunchCooperativeKernel((const void*)gn_solve_kernel, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
+    if (cooperative)
+        return cudaLaunchCooperativeKernel((const void*)gn_solve_kernel, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
+    return cudaLaunchKernel((const void*)gn_solve_kernel, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
 }
 
 }  // namespace gse

@@ -12,6 +12,13 @@ SURVEY.md section 8(e): areas are independent between the two coordinator exchan
      replica of the boundary state,
   4. one MAX all-reduce carries the convergence scalar (and the failure flag).
 
+On one node (up to 8 ranks) the same four steps run INSIDE each rank's persistent kernel over peer memory
+(``exchange="peer"``, the default when the ranks can be linked): the area roots store ``(S_b | b_hat)``
+straight into the coordinator's buffer, the coordinator's back-substitution tasks store their share of
+``delta_x_Gamma`` into every rank's solution vector, and the norm is max-merged with one atomic per peer --
+one kernel launch per rank and solve, no collective inside the loop (``gse_peer_link``).  The collective
+driver below remains for ``on_iteration`` callbacks, inner GN steps, phase timing and larger worlds.
+
 The driver is engine-agnostic: the product engine (``CudaEngine``) wraps the C-ABI plan;
 the CPU tests inject an oracle-backed engine and run the same code under ``gloo``.
 """
@@ -63,7 +70,7 @@ class CudaEngine:
     # stream need no host synchronisation between the phases (one per iteration: the status read)
     async_phases = True
 
-    def __init__(self, net, ms, part, bord, maps, cfg, rank, world, area_rank, device, stream=None):
+    def __init__(self, net, ms, part, bord, maps, cfg, rank, world, area_rank, device, stream=None, max_ctas=0):
         import torch
         from . import _native
         self.torch = torch
@@ -73,7 +80,7 @@ class CudaEngine:
         self.stream = stream if stream is not None else torch.cuda.Stream(self.dev)
         self.plan = _native.Plan(net, ms, part, bord, maps, device=device,
                                  dense=cfg.backend == "dense", rank=rank, world=world,
-                                 area_rank=area_rank, stream=self.stream.cuda_stream,
+                                 area_rank=area_rank, stream=self.stream.cuda_stream, max_ctas=max_ctas,
                                  boundary_mode={"auto": 0, "dense": 1, "sparse": 2}[cfg.boundary])
         self.net, self.bord = net, bord
         self.n_bus, self.n_gamma = net.n_bus, bord.n_gamma
@@ -144,6 +151,21 @@ class CudaEngine:
         """Raise the precise error of a failed factorisation owned by this rank (synchronises)."""
         self._translated(self.plan.check)
 
+    # peer-linked solve: the exchanges inside the persistent kernel (gse_peer_link)
+    def peer_info(self):
+        return self.plan.peer_info()
+
+    def peer_link(self, infos):
+        self.plan.peer_link(infos)
+
+    def solve_prepare(self):
+        self.plan.peer_solve_prepare()
+
+    def solve_linked(self, cfg):
+        """The whole GN loop of this rank in one launch; returns the native report (objective unset)."""
+        return self._translated(self.plan.solve, self.state[0].data_ptr(), self.state[1].data_ptr(),
+                                cfg.max_outer_iterations, cfg.convergence_tol, False)
+
     def launches_last(self):
         """Kernels this rank's plan enqueued in the iteration just finished."""
         return int(self.plan.stats()["launches_last"])
@@ -162,7 +184,7 @@ class DistributedEstimator:
     """Multi-rank counterpart of ``MultiAreaEstimator`` (same ``estimate`` contract)."""
 
     def __init__(self, net, ms, part, maps=None, config: SolverConfig = None, device=None,
-                 engine_factory=None, group=None):
+                 engine_factory=None, group=None, exchange="auto"):
         import os
         import torch
         import torch.distributed as dist
@@ -191,6 +213,37 @@ class DistributedEstimator:
             self.segments.append((int(off[mine[0]]), int(off[mine[-1] + 1])) if mine.size else (0, 0))
         self.launches_per_solve = 0
         self.last_gpu_s = 0.0
+        self.linked = False
+        if exchange not in ("auto", "peer", "collective"):
+            raise ValueError("exchange must be 'auto', 'peer' or 'collective'")
+        if exchange != "collective" and self.world > 1:
+            self._link_peers(required=exchange == "peer")
+
+    def _link_peers(self, required):
+        """Exchange the ranks' ``gse_peer_info`` records and link the plans (CUDA IPC between processes).  Every
+        rank must succeed, otherwise all of them stay on the collective driver."""
+        eng, dist = self.engine, self.dist
+        ok, err = 1.0, None
+        if not hasattr(eng, "peer_info") or self.world > 8:
+            ok = 0.0
+        infos = [None] * self.world
+        try:
+            mine = eng.peer_info() if ok else b""
+        except Exception as exc:        # e.g. no IPC support on this platform
+            ok, err, mine = 0.0, exc, b""
+        dist.all_gather_object(infos, mine, group=self.group)
+        if ok and all(infos):
+            try:
+                eng.peer_link(infos)
+            except Exception as exc:
+                ok, err = 0.0, exc
+        else:
+            ok = 0.0
+        t = self.torch.tensor([ok], dtype=self.torch.float64, device=getattr(eng, "dev", "cpu"))
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        self.linked = bool(float(t.cpu()[0]))
+        if required and not self.linked:
+            raise RuntimeError(f"peer exchange requested but the ranks could not be linked: {err}")
 
     # -- collectives ---------------------------------------------------------------------------
     def _gather_blocks(self):
@@ -255,8 +308,32 @@ class DistributedEstimator:
                 "that area is likely locally unobservable")
         return inner
 
+    def _estimate_linked(self):
+        """One launch per rank: the loop, both exchanges and the convergence decision live in the kernels."""
+        cfg, eng = self.cfg, self.engine
+        t_start = time.perf_counter()
+        flat = StateVector.flat_start(self.net)
+        eng.load_state(flat.va, flat.vm)
+        eng.solve_prepare()                      # this rank's counters are clear ...
+        self.dist.barrier(group=self.group)      # ... and so are everybody else's: peers may signal from now on
+        t_loop = time.perf_counter()
+        rep = eng.solve_linked(cfg)              # raises the same SolverError on every rank (the failure code is global)
+        self.last_gpu_s = time.perf_counter() - t_loop
+        self.launches_per_solve = 1
+        state = self._full_state(load_back=True)
+        j = eng.objective()
+        self.last_deltas = [float(rep.delta_inf[k]) for k in range(rep.iterations)]
+        timings = {p: 0.0 for p in PHASES}
+        timings["total"] = time.perf_counter() - t_start
+        return state, SolveReport(method="multiarea", iterations=int(rep.iterations), converged=bool(rep.converged),
+                                  objective=float(j), weighted_residual_norm=float(np.sqrt(j)),
+                                  n_gamma=self.n_gamma, timings=timings)
+
     def _estimate(self, on_iteration=None):
         cfg, eng = self.cfg, self.engine
+        if (self.linked and on_iteration is None and cfg.inner_gn_steps == 1 and cfg.max_outer_iterations <= 64
+                and not cfg.profile_phases):
+            return self._estimate_linked()
         t_start = time.perf_counter()
         flat = StateVector.flat_start(self.net)
         eng.load_state(flat.va, flat.vm)

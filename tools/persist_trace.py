@@ -100,3 +100,23 @@ for it in range(rep.iterations):
         print("   backward wavefront:")
         for i in range(0, len(b), step):
             print(f"     {i:5d}: {(b[i,0]-s0)/1e3:7.1f} {(max(b[i,2],b[i,0])-s0)/1e3:7.1f} {(b[i,3]-s0)/1e3:7.1f}")
+        if os.environ.get("GSE_TRACE_HIST"):
+            # where the CTA time of the front tasks goes: by (pivots, update rows) class -- tasks, CTA-time from ready to
+            # end, and its phases (gather, panel, update, signal)
+            bf = blk[bounds[2]:bounds[3]]
+            cls = {}
+            for i in range(len(bf)):
+                pv = int(bf[i, 7] & 0xffff); u1 = int((bf[i, 7] >> 16) & 0xffff); nchild = int((bf[i, 7] >> 32) & 0xffff)
+                st = bf[i, 8:16]
+                rdy = max(bf[i, 1], bf[i, 2], bf[i, 0])
+                cw = max(bf[i, 2], st[7]) if bf[i, 2] else st[7]
+                key = (min(pv // 16 * 16, 64), 0 if u1 <= 32 else 1 if u1 <= 96 else 2 if u1 <= 256 else 3)
+                d = cls.setdefault(key, np.zeros(8))
+                d += [1, (bf[i, 3] - rdy) / 1e3, (bf[i, 3] - bf[i, 0]) / 1e3, (st[3] - cw) / 1e3, (st[4] - st[3]) / 1e3,
+                      (st[5] - st[4]) / 1e3, (bf[i, 3] - st[5]) / 1e3, (st[7] - st[0]) / 1e3]
+            print("   front tasks by class (p>=, u class 0:<=32 1:<=96 2:<=256 3:more | tasks  exec-us total  held-us total | mean gather panel update signal prep):")
+            for key in sorted(cls):
+                d = cls[key]; n = d[0]
+                print(f"     p>={key[0]:2d} u{key[1]} | {int(n):6d} {d[1]:10.0f} {d[2]:10.0f} | {d[3]/n:5.1f} {d[4]/n:5.1f} {d[5]/n:5.1f} {d[6]/n:5.1f} {d[7]/n:5.1f}")
+            bb = blk[bounds[3]:bounds[4]]
+            print(f"   backward tasks: n={len(bb)} exec total {np.sum(bb[:,3]-np.maximum(bb[:,2],bb[:,0]))/1e3:.0f} us  held total {np.sum(bb[:,3]-bb[:,0])/1e3:.0f} us")
