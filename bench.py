@@ -420,6 +420,9 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.workload, net, ms, part, est.n_gamma, it_per_solve),
         "converged": bool(rep.converged), "parallelism": f"areas sharded over {world} GPU(s), one process per GPU",
+        "exchange": ("none (single rank)" if world == 1 else
+                     "in-kernel over peer memory (CUDA IPC / NVLink): one persistent launch per rank and solve" if getattr(est, "linked", False)
+                     else "torch.distributed collectives between level launches"),
         "time_to_converge_ms": {"warm_device": tot_dev / args.steps * 1e3, "warm_e2e": tot_e2e / args.steps * 1e3,
                                 "plan_build_s": plan_s, "partition_s": partition_s},
         "objective": rep.objective,
