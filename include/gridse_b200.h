@@ -194,6 +194,13 @@ int gse_matrix_condense(gse_plan *plan);
 /* interior_recover (linalg.py:427-434): dx_i = G_ii^-1 (b_i - G_ib dx_b) with the factor and b_i of the
  * last gse_matrix_condense; dx_b NULL = zeros (a plain cache.solve(b_i)). */
 int gse_matrix_recover(gse_plan *plan, const double *dx_b, double *dx_i);
+/* SparseCholeskyCache.forward / .backward (linalg.py:340-383), in this factor's coordinates.  perm[e] =
+ * original index of elimination position e (cache.perm).  gse_matrix_forward_get: y = L^-1 P b of the b_i given to
+ * the last gse_matrix_set_values + gse_matrix_condense (the right-hand side rides through the factorisation as
+ * one extra row of every front).  gse_matrix_backward: x = P^T L^-T y, x in original order.  Host arrays [n_i]. */
+int gse_matrix_perm(const gse_plan *plan, int32_t *perm);
+int gse_matrix_forward_get(gse_plan *plan, double *y);
+int gse_matrix_backward(gse_plan *plan, const double *y, double *x);
 /* assemble_boundary (solver.py:106-119) for caller-supplied Schur blocks: s_b = the areas' n_b x n_b
  * blocks concatenated, b_hat likewise, sel_ptr / sel the boundary selectors.  Host in, host out. */
 int gse_assemble_boundary(int32_t n_gamma, int32_t n_areas, const int32_t *sel_ptr, const int32_t *sel,

@@ -125,6 +125,9 @@ def lib():
     L.gse_matrix_set_values.argtypes = [vp, f64p, f64p, f64p, f64p, f64p]
     L.gse_matrix_condense.argtypes = [vp]
     L.gse_matrix_recover.argtypes = [vp, f64p, f64p]
+    L.gse_matrix_perm.argtypes = [vp, i32p]
+    L.gse_matrix_forward_get.argtypes = [vp, f64p]
+    L.gse_matrix_backward.argtypes = [vp, f64p, f64p]
     L.gse_assemble_boundary.argtypes = [C.c_int32, C.c_int32, i32p, i32p, f64p, f64p, f64p, f64p]
     L.gse_phase_assemble.argtypes = [vp, vp, vp]
     L.gse_phase_condense.argtypes = [vp]
@@ -167,6 +170,7 @@ EXPORTED = [
     "gse_matrix_recover", "gse_assemble_boundary", "gse_phase_local_async", "gse_phase_boundary_async",
     "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout", "gse_partition_attempt", "gse_partition_thin_cuts",
     "gse_peer_info_get", "gse_peer_link", "gse_peer_solve_prepare",
+    "gse_matrix_perm", "gse_matrix_forward_get", "gse_matrix_backward",
 ]
 
 
@@ -503,6 +507,24 @@ class MatrixPlan:
         if self.n_b:
             self._call(lib().gse_area_schur(self._h, 0, _fp(s_b), _fp(b_hat)))
         return s_b, b_hat
+
+    def perm(self):
+        """perm[e] = original index of elimination position e (the reference's ``cache.perm``)."""
+        out = np.zeros(max(self.n_i, 1), dtype=np.int32)
+        self._call(lib().gse_matrix_perm(self._h, _ip(out)))
+        return out[:self.n_i]
+
+    def forward_get(self):
+        """y = L^-1 P b of the right-hand side given to the last set_values + condense."""
+        y = np.zeros(max(self.n_i, 1))
+        self._call(lib().gse_matrix_forward_get(self._h, _fp(y)))
+        return y[:self.n_i]
+
+    def backward(self, y):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        x = np.zeros(max(self.n_i, 1))
+        self._call(lib().gse_matrix_backward(self._h, _fp(y) if y.size else None, _fp(x)))
+        return x[:self.n_i]
 
     def recover(self, dx_b=None):
         dx_i = np.zeros(max(self.n_i, 1))

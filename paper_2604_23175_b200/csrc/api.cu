@@ -824,6 +824,42 @@ int gse_matrix_recover(gse_plan* plan, const double* dx_b, double* dx_i) {
     return gse_area_delta(plan, 0, dx_i);
 }
 
+// SparseCholeskyCache.forward / .backward (linalg.py:340-383) in THIS factor's coordinates: perm[e] = original
+// index of elimination position e (the reference's cache.perm).  forward: y = L^-1 P b is the right-hand-side row
+// every front carries through the factorisation (read after gse_matrix_set_values(b_i = b) + gse_matrix_condense).
+int gse_matrix_perm(const gse_plan* plan, int32_t* perm) {
+    const HostProgram& hp = plan->hp;
+    if (hp.gval_src.size() != (size_t)hp.n_gval) return GSE_E_INVALID;
+    for (int e = 0; e < hp.area_ni[0]; ++e) perm[e] = hp.perm_orig[hp.area_base[0] + e];
+    return GSE_OK;
+}
+int gse_matrix_forward_get(gse_plan* plan, double* y) {
+    const HostProgram& hp = plan->hp;
+    if (hp.gval_src.size() != (size_t)hp.n_gval) return fail(plan, GSE_E_INVALID, "not a matrix plan");
+    CU(cudaSetDevice(plan->device));
+    for (const Front& f : hp.fronts) {
+        if (f.kind != 0 || f.p == 0) continue;
+        // pivots of a front are consecutive elimination positions; its solved right-hand side is row p + u of the panel
+        CU(cudaMemcpyAsync(y + (f.rows[0] - hp.area_base[0]), plan->lbuf.ptr + f.l_off + (size_t)(f.p + f.u1 - 1) * f.p,
+                           sizeof(double) * f.p, cudaMemcpyDeviceToHost, plan->stream));
+    }
+    CU(cudaStreamSynchronize(plan->stream));
+    return GSE_OK;
+}
+// backward: x = P^T L^-T y with the factor of the last gse_matrix_condense (the boundary increment held at zero)
+int gse_matrix_backward(gse_plan* plan, const double* y, double* x) {
+    const HostProgram& hp = plan->hp;
+    if (hp.gval_src.size() != (size_t)hp.n_gval) return fail(plan, GSE_E_INVALID, "not a matrix plan");
+    CU(cudaSetDevice(plan->device));
+    for (const Front& f : hp.fronts) {
+        if (f.kind != 0 || f.p == 0) continue;
+        CU(cudaMemcpyAsync(plan->lbuf.ptr + f.l_off + (size_t)(f.p + f.u1 - 1) * f.p, y + (f.rows[0] - hp.area_base[0]),
+                           sizeof(double) * f.p, cudaMemcpyHostToDevice, plan->stream));
+    }
+    CU(cudaStreamSynchronize(plan->stream));      // (y is pageable caller memory)
+    return gse_matrix_recover(plan, nullptr, x);
+}
+
 // assemble_boundary (solver.py:106-119): S_Gamma[sel, sel] += S_b, b_Gamma[sel] += b_hat, areas in
 // ascending order.  Host in / host out; the sums run on the device in area order per entry.
 int gse_assemble_boundary(int32_t n_gamma, int32_t n_areas, const int32_t* sel_ptr, const int32_t* sel, const double* s_b,

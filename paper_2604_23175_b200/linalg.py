@@ -10,9 +10,10 @@ here run the same multifrontal kernels on caller-supplied matrices through *matr
 boundary rows are the columns of ``g_ib``.
 
 Differences a caller can observe: the ordering is nested dissection instead of the reference's
-greedy minimum degree (the reference allows any ordering, ``SPEC.md:362``), so ``forward`` /
-``backward`` -- whose intermediate vector lives in the permuted factor's coordinates -- are not
-offered separately; ``solve`` is.  There is no CPU fallback: every call needs a CUDA device.
+greedy minimum degree (the reference allows any ordering, ``SPEC.md:362``), so the intermediate
+vector of ``forward`` / ``backward`` lives in THIS factor's coordinates (``cache.perm``, as in the
+reference: ``y = L^-1 P b``); ``backward(forward(b))`` equals ``solve(b)`` bit for bit and
+``y @ y == b @ G^-1 b`` whatever the ordering.  There is no CPU fallback: every call needs a CUDA device.
 """
 
 from __future__ import annotations
@@ -150,6 +151,45 @@ class SparseCholeskyCache:
         except _native.NativeError as exc:
             self._raise(exc)
         return x
+
+    @property
+    def perm(self):
+        """Elimination order of this factor: ``perm[e]`` = original index eliminated at position ``e``
+        (reference ``SparseCholeskyCache.perm``; a nested-dissection order here)."""
+        return self._plan().perm() if self.n else np.zeros(0, dtype=np.int32)
+
+    def forward(self, b):
+        """``y = L^-1 P b`` (reference linalg.py:340-364); ``b`` is a vector or a matrix of columns.  On the device
+        the right-hand side rides through the factorisation as one extra row of every front, so this is a
+        refactorisation with ``b`` attached."""
+        if not self._factorized:
+            raise RuntimeError("numeric factorization has not been run")
+        b = np.asarray(b, dtype=float)
+        if b.ndim == 2:
+            return np.stack([self.forward(b[:, j]) for j in range(b.shape[1])], axis=1) if b.shape[1] else b.copy()
+        if self.n == 0:
+            return b.copy()
+        plan = self._plan()
+        try:
+            plan.set_values(data_ii=self._values, b_i=b)
+            plan.condense()
+            return plan.forward_get()
+        except _native.NativeError as exc:
+            self._raise(exc)
+
+    def backward(self, y):
+        """``x = P^T L^-T y`` (reference linalg.py:366-383) with the current factor."""
+        if not self._factorized:
+            raise RuntimeError("numeric factorization has not been run")
+        y = np.asarray(y, dtype=float)
+        if y.ndim == 2:
+            return np.stack([self.backward(y[:, j]) for j in range(y.shape[1])], axis=1) if y.shape[1] else y.copy()
+        if self.n == 0:
+            return y.copy()
+        try:
+            return self._plan().backward(y)
+        except _native.NativeError as exc:
+            self._raise(exc)
 
     def stats(self):
         """Pattern statistics (the factor is a tree of dense fronts on the device)."""

@@ -153,3 +153,34 @@ def test_component_pipeline_reproduces_solver_boundary_system(G):
     assert np.max(np.abs(bs.b_gamma - g["b_gamma"]) / (1 + np.abs(g["b_gamma"]))) < 1e-9
     dx = G.dense_cholesky_solve(bs.s_gamma, bs.b_gamma)
     assert np.max(np.abs(dx - g["dx_gamma"])) < 1e-9
+
+
+@pytest.mark.parametrize("n,seed", [(12, 0), (64, 1), (300, 2)])
+def test_forward_backward_in_factor_coordinates(G, n, seed):
+    """SparseCholeskyCache.forward / .backward (reference linalg.py:340-383): y = L^-1 P b lives in this factor's
+    coordinates (cache.perm), so the checks are the ordering-independent ones -- backward(forward(b)) is the solve
+    (bit for bit: the same device sequence), y.y = b.G^-1.b, y equals the triangular solve of the permuted matrix's
+    Cholesky factor, and matrix right-hand sides go column by column (reference test_linalg.py:137-160)."""
+    import scipy.linalg as sla
+    a, rng = _spd_sparse(n, seed)
+    cache = G.symbolic_analyze(a)
+    G.numeric_refactor(cache, a.data)
+    b = rng.standard_normal(n)
+    perm = np.asarray(cache.perm)
+    assert sorted(perm.tolist()) == list(range(n))
+    y = cache.forward(b)
+    x = cache.backward(y)
+    assert np.array_equal(x, cache.solve(b))
+    dense = a.toarray()
+    assert abs(y @ y - b @ np.linalg.solve(dense, b)) <= 1e-11 * abs(y @ y)
+    lfac = np.linalg.cholesky(dense[np.ix_(perm, perm)])
+    assert np.max(np.abs(y - sla.solve_triangular(lfac, b[perm], lower=True))) < 1e-10 * (1 + np.max(np.abs(y)))
+    assert np.max(np.abs(x - np.linalg.solve(dense, b))) < 1e-9 * (1 + np.max(np.abs(x)))
+    bm = rng.standard_normal((n, 3))
+    ym = cache.forward(bm)
+    assert ym.shape == (n, 3) and np.array_equal(ym[:, 0], cache.forward(bm[:, 0]))
+    assert np.array_equal(cache.backward(ym)[:, 2], cache.solve(bm[:, 2]))
+    fresh = G.symbolic_analyze(a)
+    with pytest.raises(RuntimeError, match="numeric factorization has not been run"):
+        fresh.forward(b)
+    cache.close(); fresh.close()
