@@ -259,7 +259,10 @@ static void eval_rows(const orc_t *o, area_t *A, const double *va, const double 
             else { h = vi * (vi * gd + sum_p); if (dth >= 0) g[dth] = -vi * sum_q; g[dvm] = 2.0 * vi * gd + sum_p; }
         } else {
             int f = d->br_from[tg], tt = d->br_to[tg]; const double *y = d->br_y + 8 * (size_t)tg;
-            int from_end = (t == 3 || t == 5), reactive = (t >= 5);
+            /* types 7 / 8: current magnitude |i_o| at the from / to end -- NOT in the reference (measurement.py:27-34
+               stops at QT); a north_star template, restated here from the same two-port current i_o, parity unpinned
+               (tests check it against finite differences and the device template against this) */
+            int from_end = (t == 3 || t == 5 || t == 7), reactive = (t == 5 || t == 6), current = (t >= 7);
             int ob = from_end ? f : tt, ub = from_end ? tt : f;
             double yor = from_end ? y[0] : y[6], yoi = from_end ? y[1] : y[7];
             double yur = from_end ? y[2] : y[4], yui = from_end ? y[3] : y[5];
@@ -286,6 +289,16 @@ static void eval_rows(const orc_t *o, area_t *A, const double *va, const double 
             h = reactive ? si : sr;
             double g_tho = reactive ? dthoi : dthor, g_thu = reactive ? dthui : dthur;
             double g_vo = reactive ? dvoi : dvor, g_vu = reactive ? dvui : dvur;
+            if (current) {
+                /* h = |i_o|; dh/dx = Re(conj(i_o) di_o/dx) / h with di/dth_o = j y_own v_o, di/dth_u = j y_oth v_u,
+                   di/dvm_o = y_own v_o / vm_o, di/dvm_u = y_oth v_u / vm_u; a vanishing current (flat start on a
+                   branch without charging) has no gradient: the row then contributes nothing to this iteration */
+                double m2 = ir * ir + ii * ii;
+                h = sqrt(m2);
+                double ih = m2 > 1e-24 ? 1.0 / h : 0.0;
+                g_tho = (ir * (-t1i) + ii * t1r) * ih; g_thu = (ir * (-t2i) + ii * t2r) * ih;
+                g_vo = (ir * t1r + ii * t1i) / vmo * ih; g_vu = (ir * t2r + ii * t2i) / vmu * ih;
+            }
             int c = 0;
             if (f != d->slack) g[c++] = (f == ob) ? g_tho : g_thu;
             if (tt != d->slack) g[c++] = (tt == ob) ? g_tho : g_thu;
@@ -587,11 +600,11 @@ double orc_objective(const orc_t *o, const double *va, const double *vm) {
             for (int p = d->y_ptr[tg]; p < d->y_ptr[tg + 1]; p++) { int j = d->y_idx[p]; double th = va[tg] - va[j];
                 acc += (t == 1) ? vm[j] * (d->y_g[p] * cos(th) + d->y_b[p] * sin(th)) : vm[j] * (d->y_g[p] * sin(th) - d->y_b[p] * cos(th)); }
             h = vm[tg] * acc; }
-        else { int f = d->br_from[tg], tt = d->br_to[tg]; const double *y = d->br_y + 8 * (size_t)tg; int fe = (t == 3 || t == 5);
+        else { int f = d->br_from[tg], tt = d->br_to[tg]; const double *y = d->br_y + 8 * (size_t)tg; int fe = (t == 3 || t == 5 || t == 7);
             int ob = fe ? f : tt, ub = fe ? tt : f; double yor = fe ? y[0] : y[6], yoi = fe ? y[1] : y[7], yur = fe ? y[2] : y[4], yui = fe ? y[3] : y[5];
             double vor = vm[ob] * cos(va[ob]), voi = vm[ob] * sin(va[ob]), vur = vm[ub] * cos(va[ub]), vui = vm[ub] * sin(va[ub]);
             double ir = (yor * vor - yoi * voi) + (yur * vur - yui * vui), ii = (yor * voi + yoi * vor) + (yur * vui + yui * vur);
-            h = (t >= 5) ? (vor * (-ii) + voi * ir) : (vor * ir - voi * (-ii)); }
+            h = (t >= 7) ? sqrt(ir * ir + ii * ii) : (t >= 5) ? (vor * (-ii) + voi * ir) : (vor * ir - voi * (-ii)); }
         double res = d->m_z[r] - h, term = d->m_w[r] * res * res;
         double tsum = sum + term; comp += (fabs(sum) >= fabs(term)) ? (sum - tsum) + term : (term - tsum) + sum; sum = tsum;
     }

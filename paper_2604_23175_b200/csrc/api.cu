@@ -338,6 +338,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     ep.y_ptr = plan->y_ptr.ptr; ep.y_idx = plan->y_idx.ptr; ep.y_g = plan->y_g.ptr; ep.y_b = plan->y_b.ptr;
     ep.br_y = plan->br_y.ptr; ep.z = plan->z.ptr; ep.w = plan->w.ptr; ep.slack = d->slack;
     ep.n_vm = (int)hp.vm_bus.size(); ep.n_fl = (int)hp.fl_branch.size(); ep.n_inj = (int)hp.inj_bus.size();
+    ep.has_current = 0;
+    for (int r = 0; r < d->n_rows; ++r) if (d->m_type[r] >= 7) { ep.has_current = 1; break; }
     ep.vm_bus = plan->vm_bus.ptr; ep.vm_row = plan->vm_row.ptr; ep.vm_slot = plan->vm_slot.ptr;
     ep.fl_branch = plan->fl_branch.ptr; ep.fl_from = plan->fl_from.ptr; ep.fl_to = plan->fl_to.ptr;
     ep.fl_row = plan->fl_row.ptr; ep.fl_slot = plan->fl_slot.ptr;

@@ -13,6 +13,7 @@ struct EvalProg {
     const double *z, *w;
     int32_t slack;
     int32_t n_vm, n_fl, n_inj;
+    int32_t has_current;          // any current-magnitude row (types 7 / 8) in the plan
     const int32_t *vm_bus, *vm_row, *vm_slot;
     const int32_t *fl_branch, *fl_from, *fl_to, *fl_row, *fl_slot;
     const int32_t *inj_bus, *inj_rowp, *inj_rowq, *inj_slotp, *inj_slotq, *inj_nth;

@@ -54,7 +54,7 @@ struct HostProgram {
 
     // template evaluation units
     std::vector<int32_t> vm_bus, vm_row, vm_slot;
-    std::vector<int32_t> fl_branch, fl_from, fl_to, fl_row /*4 per unit*/, fl_slot /*4 per unit*/;
+    std::vector<int32_t> fl_branch, fl_from, fl_to, fl_row /*8 per unit: PF PT QF QT IF IT - -*/, fl_slot /*8 per unit*/;
     std::vector<int32_t> inj_bus, inj_rowp, inj_rowq, inj_slotp, inj_slotq, inj_nth /*angle slots of the row*/;
 
     // accumulation: destination-sorted contribution lists (solver layout -> gval)

@@ -59,7 +59,7 @@ __device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target, bool
         __nanosleep(40);
         // watchdog: a dependency that never completes would hang the device; after ~10 s of waiting
         // the kernel aborts instead (the launch then fails with an error the host reports)
-        if ((++polls & 0xfffu) == 0) {
+        if ((++polls & 0xffffu) == 0) {
             unsigned long long now;
             asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
             if (t0 == 0) t0 = now;
@@ -153,8 +153,10 @@ struct SpinWait {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kSolveThreads, 2)
-gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) {
+// LINKED: the peer-linked multi-rank variant (exchanges over peer memory, sp.lk).  A separate instantiation: the
+// single-rank kernel runs at the 128-register cap of two CTAs per SM and must not carry the other's live values.
+template <bool LINKED>
+__device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalProg& ep, const FrontTab& ft, double* va, double* vm) {
     extern __shared__ __align__(16) double sm[];
     __shared__ FrontScratch S;
     __shared__ int s_item, s_stop;
@@ -172,7 +174,7 @@ gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) 
               o_upd = o_bwd + sp.n_btasks;
     const bool fused_update = sp.n_upd_items == 0;      // latency-bound plans: the update rides on the backward tasks
     const PeerLink& lk = sp.lk;
-    const bool linked = lk.world > 1;                   // areas sharded over several GPUs, exchanges over peer memory
+    constexpr bool linked = LINKED;                     // areas sharded over several GPUs, exchanges over peer memory
     const unsigned gamma_need = (linked && lk.rank != 0) ? (unsigned)lk.n_gamma_fronts : 0u;
     if (sp.stamps && blockIdx.x == 0 && tid == 0) sp.stamps[0] = globaltimer();
 #define GSE_STAMP(it, k) do { if (sp.stamps) atomicMax(sp.stamps + 1 + 8 * (it) + (k), globaltimer()); } while (0)
@@ -413,6 +415,11 @@ cudaError_t solve_kernel_debug_watchdog(unsigned long long* host_mapped, unsigne
     return e == cudaSuccess ? cudaMemcpyToSymbol(g_watchdog_ns, &ns, sizeof ns) : e;
 }
 
+__global__ void __launch_bounds__(kSolveThreads, 2)
+gn_solve_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) { gn_solve_body<false>(sp, ep, ft, va, vm); }
+__global__ void __launch_bounds__(kSolveThreads, 2)
+gn_solve_linked_kernel(SolveProg sp, EvalProg ep, FrontTab ft, double* va, double* vm) { gn_solve_body<true>(sp, ep, ft, va, vm); }
+
 size_t solve_kernel_static_smem() {
     cudaFuncAttributes a{};
     if (cudaFuncGetAttributes(&a, gn_solve_kernel) != cudaSuccess) return 0;
@@ -421,8 +428,11 @@ size_t solve_kernel_static_smem() {
 
 int solve_kernel_max_ctas(size_t dyn_smem, int device) {
     if (cudaFuncSetAttribute(gn_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem) != cudaSuccess) return 0;
-    int per_sm = 0, sms = 0;
+    if (cudaFuncSetAttribute(gn_solve_linked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem) != cudaSuccess) return 0;
+    int per_sm = 0, sms = 0, per_sm_l = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_solve_kernel, kSolveThreads, dyn_smem) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, gn_solve_linked_kernel, kSolveThreads, dyn_smem) != cudaSuccess) return 0;
+    per_sm = per_sm < per_sm_l ? per_sm : per_sm_l;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
     return per_sm * sms;
 }
@@ -434,9 +444,9 @@ int solve_kernel_max_ctas(size_t dyn_smem, int device) {
 cudaError_t launch_solve(const SolveProg& sp, const EvalProg& ep, const FrontTab& ft, double* va, double* vm,
                          int grid, size_t dyn_smem, cudaStream_t s, bool cooperative) {
     void* args[] = {(void*)&sp, (void*)&ep, (void*)&ft, (void*)&va, (void*)&vm};
-    if (cooperative)
-        return cudaLaunchCooperativeKernel((const void*)gn_solve_kernel, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
-    return cudaLaunchKernel((const void*)gn_solve_kernel, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
+    const void* fn = sp.lk.world > 1 ? (const void*)gn_solve_linked_kernel : (const void*)gn_solve_kernel;
+    if (cooperative) return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(kSolveThreads), args, dyn_smem, s);
 }
 
 }  // namespace gse

@@ -421,7 +421,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
     // ---- rows per area -----------------------------------------------------------
     for (int r = 0; r < m; ++r) {
         int t = d.m_type[r], tg = d.m_target[r];
-        if (t < 0 || t > 6) return "unknown measurement type";
+        if (t < 0 || t > 8) return "unknown measurement type";      // 0 VM, 1-2 P/Q injection, 3-6 P/Q flow, 7-8 current magnitude
         if (tg < 0 || tg >= (t >= 3 ? d.n_branch : nbus)) return "measurement target out of range";
         int owner = t >= 3 ? d.br_from[tg] : tg;
         as[d.area_of_bus[owner]].rows.push_back(r);
@@ -496,10 +496,10 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                     if (u < 0) {
                         u = unit_of_branch[tg] = (int)hp.fl_branch.size();
                         hp.fl_branch.push_back(tg); hp.fl_from.push_back(f); hp.fl_to.push_back(tt);
-                        for (int q = 0; q < 4; ++q) { hp.fl_row.push_back(-1); hp.fl_slot.push_back(-1); }
+                        for (int q = 0; q < 8; ++q) { hp.fl_row.push_back(-1); hp.fl_slot.push_back(-1); }   // PF PT QF QT IF IT - -
                     }
-                    if (hp.fl_row[4 * u + (t - 3)] >= 0) return "duplicate flow row";
-                    hp.fl_row[4 * u + (t - 3)] = r; hp.fl_slot[4 * u + (t - 3)] = gslot;
+                    if (hp.fl_row[8 * u + (t - 3)] >= 0) return "duplicate flow row";
+                    hp.fl_row[8 * u + (t - 3)] = r; hp.fl_slot[8 * u + (t - 3)] = gslot;
                 }
             }
             A.slot_ptr[k + 1] = (int)A.slot_var.size();

@@ -33,10 +33,14 @@ __device__ __forceinline__ void flow_row(const EvalProg& ep, int row, int slot, 
 // Writes, per template slot, the partial g and w*g, and per row the weighted residual w*r.
 __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const double* va, const double* vm) {
     if (u < ep.n_fl) {
-        // one unit per measured branch: PF, PT, QF, QT share one sincos of the angle difference
+        // one unit per measured branch: PF, PT, QF, QT (and the current magnitudes IF, IT) share one sincos of the
+        // angle difference
         const int e = ep.fl_branch[u], f = ep.fl_from[u], t = ep.fl_to[u];
-        const int4 rows = reinterpret_cast<const int4*>(ep.fl_row)[u];
-        const int4 slots = reinterpret_cast<const int4*>(ep.fl_slot)[u];
+        const int4 rows = reinterpret_cast<const int4*>(ep.fl_row)[2 * u];
+        const int4 slots = reinterpret_cast<const int4*>(ep.fl_slot)[2 * u];
+        // (plans without ammeter rows -- every reference-generated set -- skip the two loads)
+        const int2 irows = ep.has_current ? reinterpret_cast<const int2*>(ep.fl_row)[4 * u + 2] : make_int2(-1, -1);
+        const int2 islots = ep.has_current ? reinterpret_cast<const int2*>(ep.fl_slot)[4 * u + 2] : make_int2(-1, -1);
         const double4* yy = reinterpret_cast<const double4*>(ep.br_y + 8 * (size_t)e);
         const double4 y0 = yy[0], y1 = yy[1];   // (ff.re ff.im ft.re ft.im) (tf.re tf.im tt.re tt.im)
         const double vf = ldc(vm + f), vt = ldc(vm + t);
@@ -63,6 +67,28 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
                      vt * ec, 2.0 * vt * a + vf * ec);
             flow_row(ep, rows.w, slots.w, fs, ts, vt * (-vt * b + vf * es), -vv * ec, vv * ec,
                      vt * es, -2.0 * vt * b + vf * es);
+        }
+        // current magnitudes (north_star template; the reference has none, measurement.py:27-34): with i = y_own V_o +
+        // y_oth V_u,  |i|^2 = |y_own|^2 Vo^2 + |y_oth|^2 Vu^2 + 2 Vo Vu (al cos d - be sin d),  al + j be = y_own conj(y_oth),
+        // d = th_o - th_u;  h = |i| and dh/dx = d|i|^2/dx / (2 h).  A vanishing current (flat start on a branch without
+        // charging) has no gradient: the row then contributes nothing to this iteration.
+        if (irows.x >= 0) {
+            const double a = y0.x, b = y0.y, c = y0.z, d = y0.w;
+            const double al = a * c + b * d, be = b * c - a * d, A = a * a + b * b, C = c * c + d * d;
+            const double E = al * cs - be * sn, vv = vf * vt;
+            const double m2 = A * vf * vf + C * vt * vt + 2.0 * vv * E;
+            const double h = sqrt(fmax(m2, 0.0)), ih = m2 > 1e-24 ? 1.0 / h : 0.0;
+            const double dth = vv * (-al * sn - be * cs) * ih;
+            flow_row(ep, irows.x, islots.x, fs, ts, h, dth, -dth, (A * vf + vt * E) * ih, (C * vt + vf * E) * ih);
+        }
+        if (irows.y >= 0) {
+            const double a = y1.z, b = y1.w, c = y1.x, d = y1.y;       // own = t: y_tt, y_tf; d = th_t - th_f (sin negated)
+            const double al = a * c + b * d, be = b * c - a * d, A = a * a + b * b, C = c * c + d * d;
+            const double E = al * cs + be * sn, vv = vf * vt;
+            const double m2 = A * vt * vt + C * vf * vf + 2.0 * vv * E;
+            const double h = sqrt(fmax(m2, 0.0)), ih = m2 > 1e-24 ? 1.0 / h : 0.0;
+            const double dtt = vv * (al * sn - be * cs) * ih;
+            flow_row(ep, irows.y, islots.y, fs, ts, h, -dtt, dtt, (C * vf + vt * E) * ih, (A * vt + vf * E) * ih);
         }
         return;
     }
@@ -288,12 +314,17 @@ __device__ __forceinline__ double objective_row(const EvalProg& ep, const int32_
     } else {
         const int f = br_from[tg], tt = br_to[tg];
         const double* y = ep.br_y + 8 * (size_t)tg;
-        const bool fe = (t == 3 || t == 5);
+        const bool fe = (t == 3 || t == 5 || t == 7);
         const int ob = fe ? f : tt, ub = fe ? tt : f;
         const double a = fe ? y[0] : y[6], b = fe ? y[1] : y[7], c = fe ? y[2] : y[4], d = fe ? y[3] : y[5];
         double sn, cs;
         sincos(ldc(va + ob) - ldc(va + ub), &sn, &cs);
         const double vo = ldc(vm + ob), vu = ldc(vm + ub);
+        if (t >= 7) {
+            const double m2 = (a * a + b * b) * vo * vo + (c * c + d * d) * vu * vu
+                              + 2.0 * vo * vu * ((a * c + b * d) * cs - (b * c - a * d) * sn);
+            h = sqrt(fmax(m2, 0.0));
+        } else
         h = (t >= 5) ? vo * (-vo * b + vu * (c * sn - d * cs)) : vo * (vo * a + vu * (c * cs + d * sn));
     }
         const double res = ep.z[r] - h;

@@ -47,13 +47,22 @@ void eval(Sim& s, const double* va, const double* vm) {
         const double* y = d.br_y + 8 * (size_t)e;
         double vf = vm[f], vt = vm[t], sn = std::sin(va[f] - va[t]), cs = std::cos(va[f] - va[t]);
         bool fs = f == d.slack, ts = t == d.slack;
-        const int32_t* rows = &hp.fl_row[4 * u]; const int32_t* sl = &hp.fl_slot[4 * u];
+        const int32_t* rows = &hp.fl_row[8 * u]; const int32_t* sl = &hp.fl_slot[8 * u];
         { double a = y[0], b = y[1], c = y[2], dd = y[3], ec = c * cs + dd * sn, es = c * sn - dd * cs, vv = vf * vt;
           flow_row(s, rows[0], sl[0], fs, ts, vf * (vf * a + vt * ec), -vv * es, vv * es, 2.0 * vf * a + vt * ec, vf * ec);
           flow_row(s, rows[2], sl[2], fs, ts, vf * (-vf * b + vt * es), vv * ec, -vv * ec, -2.0 * vf * b + vt * es, vf * es); }
         { double a = y[6], b = y[7], c = y[4], dd = y[5], ec = c * cs - dd * sn, es = -c * sn - dd * cs, vv = vf * vt;
           flow_row(s, rows[1], sl[1], fs, ts, vt * (vt * a + vf * ec), vv * es, -vv * es, vt * ec, 2.0 * vt * a + vf * ec);
           flow_row(s, rows[3], sl[3], fs, ts, vt * (-vt * b + vf * es), -vv * ec, vv * ec, vt * es, -2.0 * vt * b + vf * es); }
+        // current magnitudes at the from / to end (unit_bodies.cuh)
+        if (rows[4] >= 0) { double a = y[0], b = y[1], c = y[2], dd = y[3], al = a * c + b * dd, be = b * c - a * dd, A = a * a + b * b, C = c * c + dd * dd;
+          double E = al * cs - be * sn, vv = vf * vt, m2 = A * vf * vf + C * vt * vt + 2.0 * vv * E, h = std::sqrt(std::max(m2, 0.0)), ih = m2 > 1e-24 ? 1.0 / h : 0.0;
+          double dth = vv * (-al * sn - be * cs) * ih;
+          flow_row(s, rows[4], sl[4], fs, ts, h, dth, -dth, (A * vf + vt * E) * ih, (C * vt + vf * E) * ih); }
+        if (rows[5] >= 0) { double a = y[6], b = y[7], c = y[4], dd = y[5], al = a * c + b * dd, be = b * c - a * dd, A = a * a + b * b, C = c * c + dd * dd;
+          double E = al * cs + be * sn, vv = vf * vt, m2 = A * vt * vt + C * vf * vf + 2.0 * vv * E, h = std::sqrt(std::max(m2, 0.0)), ih = m2 > 1e-24 ? 1.0 / h : 0.0;
+          double dtt = vv * (al * sn - be * cs) * ih;
+          flow_row(s, rows[5], sl[5], fs, ts, h, -dtt, dtt, (C * vf + vt * E) * ih, (A * vt + vf * E) * ih); }
     }
     for (size_t u = 0; u < hp.inj_bus.size(); ++u) {
         int i = hp.inj_bus[u], rp = hp.inj_rowp[u], rq = hp.inj_rowq[u], sp = hp.inj_slotp[u], sq = hp.inj_slotq[u];
