@@ -3,6 +3,8 @@
 // dataflow kernel (solve_kernel.cu).  Loads of data produced by other CTAs go through ldc()
 // (ld.global.cg, L2-coherent): see unit_bodies.cuh.
 #pragma once
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "unit_bodies.cuh"
 
@@ -10,6 +12,9 @@ namespace gse {
 
 #ifndef GSE_PANEL_QUIET
 #define GSE_PANEL_QUIET 1
+#endif
+#ifndef GSE_UPDATE_NARROW
+#define GSE_UPDATE_NARROW 1
 #endif
 
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
@@ -543,56 +548,65 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     if (!no_tile) {
         const double* Pj = diag ? Pi : pan + (size_t)(rp + ri) * ld;
         const int nbi = round8(ni) >> 3, nbj = round8(nj) >> 3;
-        const int ngj = (nbj + 3) >> 2;                 // groups of four 8-wide column blocks
         const int kend = (p + 3) & ~3;
-        // (an area root of a non-coordinator rank stores S_b | b_hat straight into the coordinator's buffer)
-        double* U = (((hdr.flags & 4) && ft.ubuf_root) ? ft.ubuf_root : ubuf) + hdr.u_off;
+        double* U = (((hdr.flags & 4) && ft.ubuf_root) ? ft.ubuf_root : ubuf) + hdr.u_off;     // (area root of a non-coordinator rank: the coordinator's buffer)
         const double* Uc = direct ? ubuf + crec[0].u_off : nullptr;   // chain: F_IJ lives in the child's U
-        for (int w = warp; w < nbi * ngj; w += nwarps) {
-            const int bi = w / ngj, gj = w % ngj;
-            if (diag && gj * 4 > bi) continue;
-            const int row = bi * 8 + (lane >> 2);
-            const int I = i0 + row;
-            double fv[8];
+        // one warp per (8-row block, group of GW 8-wide column blocks); GW = 4 reuses every A fragment four times,
+        // GW = 2 is taken when four-wide groups would leave warps idle (a 32 x 32 tile is four groups of four but
+        // eight groups of two: half the MMA chain per warp on the critical path of a latency-bound front)
+        auto update_groups = [&](auto gw_tag) {
+            constexpr int GW = decltype(gw_tag)::value;
+            const int ngj = (nbj + GW - 1) / GW;
+            for (int w = warp; w < nbi * ngj; w += nwarps) {
+                const int bi = w / ngj, gj = w % ngj;
+                if (diag && gj * GW > bi) continue;
+                const int row = bi * 8 + (lane >> 2);
+                const int I = i0 + row;
+                double fv[2 * GW];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) fv[q] = 0.0;
-            if (direct && row < ni) {
-                const double* crow = Uc + (size_t)(p + I) * (p + I + 1) / 2 + p;
+                for (int q = 0; q < 2 * GW; ++q) fv[q] = 0.0;
+                if (direct && row < ni) {
+                    const double* crow = Uc + (size_t)(p + I) * (p + I + 1) / 2 + p;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int col = (gj * 4 + q) * 8 + 2 * (lane & 3), J = j0 + col;
-                    if (col < nj && J <= I) fv[2 * q] = ldc(crow + J);
-                    if (col + 1 < nj && J + 1 <= I) fv[2 * q + 1] = ldc(crow + J + 1);
+                    for (int q = 0; q < GW; ++q) {
+                        const int col = (gj * GW + q) * 8 + 2 * (lane & 3), J = j0 + col;
+                        if (col < nj && J <= I) fv[2 * q] = ldc(crow + J);
+                        if (col + 1 < nj && J + 1 <= I) fv[2 * q + 1] = ldc(crow + J + 1);
+                    }
                 }
-            }
-            double c[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            if (p) {
-                const double* ap = Pi + (size_t)(bi * 8 + (lane >> 2)) * ld + (lane & 3);
-                const double* bp[4];
+                double c[2 * GW];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int bj = min(gj * 4 + q, nbj - 1);
-                    bp[q] = Pj + (size_t)(bj * 8 + (lane >> 2)) * ld + (lane & 3);
-                }
+                for (int q = 0; q < 2 * GW; ++q) c[q] = 0.0;
+                if (p) {
+                    const double* ap = Pi + (size_t)(bi * 8 + (lane >> 2)) * ld + (lane & 3);
+                    const double* bp[GW];
+#pragma unroll
+                    for (int q = 0; q < GW; ++q) {
+                        const int bj = min(gj * GW + q, nbj - 1);
+                        bp[q] = Pj + (size_t)(bj * 8 + (lane >> 2)) * ld + (lane & 3);
+                    }
 #pragma unroll 2
-                for (int kk = 0; kk < kend; kk += 4) {
-                    const double a = ap[kk];
+                    for (int kk = 0; kk < kend; kk += 4) {
+                        const double a = ap[kk];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) dmma_m8n8k4(c[2 * q], c[2 * q + 1], a, bp[q][kk]);
+                        for (int q = 0; q < GW; ++q) dmma_m8n8k4(c[2 * q], c[2 * q + 1], a, bp[q][kk]);
+                    }
+                }
+                if (row < ni) {
+                    double* urow = U + (size_t)I * (I + 1) / 2;
+#pragma unroll
+                    for (int q = 0; q < GW; ++q) {
+                        const int bj = gj * GW + q;
+                        if (bj >= nbj) break;
+                        const int col = bj * 8 + 2 * (lane & 3), J = j0 + col;
+                        if (col < nj && J <= I) urow[J] = (direct ? fv[2 * q] : tile[row * ldt + col]) - c[2 * q];
+                        if (col + 1 < nj && J + 1 <= I) urow[J + 1] = (direct ? fv[2 * q + 1] : tile[row * ldt + col + 1]) - c[2 * q + 1];
+                    }
                 }
             }
-            if (row < ni) {
-                double* urow = U + (size_t)I * (I + 1) / 2;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int bj = gj * 4 + q;
-                    if (bj >= nbj) break;
-                    const int col = bj * 8 + 2 * (lane & 3), J = j0 + col;
-                    if (col < nj && J <= I) urow[J] = (direct ? fv[2 * q] : tile[row * ldt + col]) - c[2 * q];
-                    if (col + 1 < nj && J + 1 <= I) urow[J + 1] = (direct ? fv[2 * q + 1] : tile[row * ldt + col + 1]) - c[2 * q + 1];
-                }
-            }
-        }
+        };
+        if (GSE_UPDATE_NARROW && nbi * ((nbj + 3) >> 2) < nwarps) update_groups(std::integral_constant<int, 2>{});
+        else update_groups(std::integral_constant<int, 4>{});
     }
     GSE_TICK(5);
     {
