@@ -678,6 +678,11 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
         if ((p & 1) && tid == 0) l11[p * p - 1] = ldc(L + p * p - 1);
     }
     const double yk = (tid < p) ? ldc(L + (size_t)(p + u) * p + tid) : 0.0;
+    // what the triangular solve of the last CTA needs besides L11 -- reciprocal pivots, the pivots' positions in
+    // the solution vector -- is fetched here as well: nothing but the parent's x is loaded after the hand-off
+    const double* di = ft.dinv + tk.dinv_off;
+    const double r0 = (tid < 32 && tid < p) ? ldc(di + tid) : 0.0, r1 = (tid < 32 && tid + 32 < p) ? ldc(di + tid + 32) : 0.0;
+    const int prow0 = (tid < 32 && tid < p) ? rows[tid] : -1, prow1 = (tid < 32 && tid + 32 < p) ? rows[tid + 32] : -1;
     const int xrow = (tid < kBwdRows && tid < n) ? rows[p + lo + tid] : -1;
     const int a = (h & 1) * (kBwdRows / 2), b = min(n, a + kBwdRows / 2);
     double v[kBwdRows / 2];
@@ -703,8 +708,8 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
         if (tid < 128) half[h][k] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
-    if (tid < 64) bpart[(size_t)(tk.pbase + tk.split) * 64 + tid] = half[0][tid] + half[1][tid];
     if (tk.nsplit > 1) {
+        if (tid < 64) bpart[(size_t)(tk.pbase + tk.split) * 64 + tid] = half[0][tid] + half[1][tid];
         __threadfence();
         __syncthreads();
         if (tid == 0) s_last = atomicAdd(&bcnt[f], 1) == tk.nsplit - 1;
@@ -715,7 +720,11 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
     // ---- last CTA of the front: combine (split order), then solve L11^T x = t in warp 0 ------
     if (tid < 64) {
         double acc = 0.0;
-        if (tid < p) {
+        if (tk.nsplit == 1) {
+            // a single split (at most 64 update rows, most fronts): the partial sum never leaves the CTA
+            // (0.0 + s, the same sum the general path forms after its round trip through global memory)
+            acc = tid < p ? yk - (0.0 + (half[0][tid] + half[1][tid])) : 0.0;
+        } else if (tid < p) {
             const volatile double* bp = bpart + (size_t)tk.pbase * 64 + tid;
             int s = 0;
             for (; s + 3 < tk.nsplit; s += 4) {
@@ -732,8 +741,6 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
     __syncthreads();
     if (tid < 32) {
         double t0 = tv[tid], t1 = tv[tid + 32];
-        const double* di = ft.dinv + tk.dinv_off;
-        const double r0 = tid < p ? ldc(di + tid) : 0.0, r1 = tid + 32 < p ? ldc(di + tid + 32) : 0.0;
         // the lanes carry s_i = t_i / L_ii, so the serial chain per pivot is one shuffle and one FMA:
         // x_c = s_c, then s_i -= (L_ci / L_ii) x_c with the scaled factor entry formed off the chain
         t0 *= r0; t1 *= r1;
@@ -745,8 +752,8 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
             t0 = fma(-lc0, xc, t0);
             t1 = fma(-lc1, xc, t1);
         }
-        if (tid < p) xsol[rows[tid]] = t0;
-        if (tid + 32 < p) xsol[rows[tid + 32]] = t1;
+        if (prow0 >= 0) xsol[prow0] = t0;
+        if (prow1 >= 0) xsol[prow1] = t1;
     }
     __syncthreads();
     return true;
