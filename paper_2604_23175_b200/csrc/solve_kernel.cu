@@ -23,6 +23,9 @@ namespace gse {
 
 namespace {
 
+// Release fence of a hand-off (writes -> fence -> counter bump, observed with ld.acquire): acq_rel is all the
+// pattern needs; __threadfence() is the sequentially consistent fence (MEMBAR.SC.GPU), which costs more.
+__device__ __forceinline__ void fence_release() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -77,7 +80,7 @@ __device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target, bool
 }
 // called by one thread after a CTA barrier that follows the item's last global write
 __device__ __forceinline__ void signal(unsigned* p) {
-    __threadfence();
+    fence_release();
     atomicAdd(p, 1u);
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -264,7 +267,7 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
                 atomicAdd(ctr + CTR_FWD, 1u);
                 GSE_STAMP(it, 1 + S.hdr.phase);
             } else if (tid == 0) {
-                __threadfence();
+                fence_release();
                 const int kind = S.hdr.p ? S.hdr.kind : 0;
                 if (kind != 2 && S.hdr.p && S.hdr.ci == S.hdr.cj) atomicAdd(pdone + S.hdr.front, 1u);
                 if (kind != 1) atomicAdd(fdone + S.hdr.front, 1u);
@@ -293,7 +296,7 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
             }
             if (solved && !fused_update) {
                 if (tid == 0) {
-                    __threadfence();
+                    fence_release();
                     atomicAdd(bdone + tk.front, 1u);
                     atomicAdd(ctr + CTR_BWD, 1u);
                     GSE_STAMP(it, tk.phase == 3 ? 5 : 6);
@@ -301,7 +304,7 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
             } else if (solved) {
                 // the children only need x: release them first, then fold the state update and the stacked
                 // infinity norm of this front's pivots in (reference partition.py:59-62,113-116, solver.py:328-333)
-                if (tid == 0) { __threadfence(); atomicAdd(bdone + tk.front, 1u); }
+                if (tid == 0) { fence_release(); atomicAdd(bdone + tk.front, 1u); }
                 unsigned long long bits = 0ull;
                 if (tid < tk.p) {
                     const int pos = ft.rows[tk.rows_off + tid];
@@ -321,7 +324,7 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
                 if (tid == 0) {
                     bits = s_red[1] > bits ? s_red[1] : bits;
                     if (bits) atomicMax(sp.delta + it, bits);
-                    __threadfence();
+                    fence_release();
                     atomicAdd(ctr + CTR_BWD, 1u);
                     GSE_STAMP(it, tk.phase == 3 ? 5 : 6);
                     GSE_STAMP(it, 7);
@@ -351,13 +354,13 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
             if (tid == 0) {
                 for (int k = 1; k < kSolveThreads / 32; ++k) bits = s_red[k] > bits ? s_red[k] : bits;
                 if (bits) atomicMax(sp.delta + it, bits);
-                __threadfence();
+                fence_release();
                 const unsigned before = atomicAdd(ctr + CTR_UPD, 1u);
                 if (linked && before + 1u == (unsigned)sp.n_upd_items * epoch) {
                     // last update item of this rank's iteration: max-merge the rank's norm and failure code into every
                     // rank's copy, then count this rank as done there (the convergence scalar of solver.py:328-338;
                     // one 8-byte atomic per peer instead of a collective)
-                    __threadfence();
+                    fence_release();
                     const unsigned long long d = ld_acquire64(sp.delta + it), e = ld_acquire64(sp.err);
                     for (int q = 0; q < lk.world; ++q) {
                         if (d) atomicMax_system(lk.gdelta[q] + it, d);
