@@ -165,6 +165,12 @@ int gse_area_pattern(const gse_plan *plan, int32_t area, int32_t *ii_ptr, int32_
  * g_bb[n_b*n_b] row-major full, b_i[n_i], b_b[n_b] (assembly.py:32-53).  Host outputs. */
 int gse_area_blocks(gse_plan *plan, int32_t area, double *data_ii, double *data_ib,
                     double *g_bb, double *b_i, double *b_b);
+/* The materialised template layer of an area after gse_phase_assemble -- what the reference's explicit oracle path
+ * builds its JacobianTriplets from (explicit_assemble, assembly.py:531-560): rows[n_rows] global row ids,
+ * slot_ptr[n_rows + 1], slot_var[n_slots] local variable per slot (x_i slots, then n_i + local boundary slot),
+ * g[n_slots] = dh/dx per slot, wr[n_rows] = w (z - h).  Sizes: gse_area_dims out[4], out[5].  Host outputs. */
+int gse_area_templates(gse_plan *plan, int32_t area, int32_t *rows, int32_t *slot_ptr, int32_t *slot_var,
+                       double *g, double *wr);
 /* SchurResult after gse_phase_condense: s_b[n_b*n_b] full symmetric, b_hat[n_b] (linalg.py:38-43). */
 int gse_area_schur(gse_plan *plan, int32_t area, double *s_b, double *b_hat);
 /* Interior update of the last gse_phase_recover, in x_i slot order (solver.py:269). */

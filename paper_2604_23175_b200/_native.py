@@ -139,6 +139,7 @@ def lib():
     L.gse_area_pattern.argtypes = [vp, C.c_int32, i32p, i32p, i32p, i32p]
     L.gse_area_blocks.argtypes = [vp, C.c_int32, f64p, f64p, f64p, f64p, f64p]
     L.gse_area_schur.argtypes = [vp, C.c_int32, f64p, f64p]
+    L.gse_area_templates.argtypes = [vp, C.c_int32, i32p, i32p, i32p, f64p, f64p]
     L.gse_area_delta.argtypes = [vp, C.c_int32, f64p]
     L.gse_boundary_system.argtypes = [vp, f64p, f64p, f64p]
     L.gse_set_boundary_delta.argtypes = [vp, f64p]
@@ -170,7 +171,7 @@ EXPORTED = [
     "gse_matrix_recover", "gse_assemble_boundary", "gse_phase_local_async", "gse_phase_boundary_async",
     "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout", "gse_partition_attempt", "gse_partition_thin_cuts",
     "gse_peer_info_get", "gse_peer_link", "gse_peer_solve_prepare",
-    "gse_matrix_perm", "gse_matrix_forward_get", "gse_matrix_backward",
+    "gse_matrix_perm", "gse_matrix_forward_get", "gse_matrix_backward", "gse_area_templates",
 ]
 
 
@@ -383,7 +384,18 @@ class Plan:
         out = np.zeros(8, dtype=np.int32)
         self._call(lib().gse_area_dims(self._h, a, _ip(out)))
         return {"n_i": int(out[0]), "n_b": int(out[1]), "nnz_ii": int(out[2]),
-                "nnz_ib": int(out[3]), "fronts": int(out[6]), "factor_nnz": int(out[7])}
+                "nnz_ib": int(out[3]), "rows": int(out[4]), "slots": int(out[5]), "fronts": int(out[6]),
+                "factor_nnz": int(out[7])}
+
+    def area_templates(self, a):
+        """Template layer of area ``a`` after ``phase_assemble``: (rows, slot_ptr, slot_var, g, w*r)."""
+        d = self.area_dims(a)
+        rows = np.zeros(max(d["rows"], 1), dtype=np.int32)
+        slot_ptr = np.zeros(d["rows"] + 1, dtype=np.int32)
+        slot_var = np.zeros(max(d["slots"], 1), dtype=np.int32)
+        g, wr = np.zeros(max(d["slots"], 1)), np.zeros(max(d["rows"], 1))
+        self._call(lib().gse_area_templates(self._h, a, _ip(rows), _ip(slot_ptr), _ip(slot_var), _fp(g), _fp(wr)))
+        return rows[:d["rows"]], slot_ptr, slot_var[:d["slots"]], g[:d["slots"]], wr[:d["rows"]]
 
     def area_pattern(self, a):
         d = self.area_dims(a)

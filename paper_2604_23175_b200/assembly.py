@@ -7,8 +7,11 @@ single-area device plan) and ``fused_accumulate(vmap, ms, x_i, x_b, pattern)``
 returns the area's ``AreaNormalBlocks`` in the reference's layout -- CSR
 ``g_ii`` / ``g_ib`` with the same sorted patterns, dense full ``g_bb``, ``b_i``,
 ``b_b`` -- computed by the template + accumulation kernels without
-materialising the Jacobian.  The explicit-Jacobian route of the reference
-(``explicit_assemble``) is its test oracle and has no device version.
+materialising the Jacobian.  ``explicit_assemble`` (the reference's test oracle, reference
+``assembly.py:531-572``) is offered in the same spirit: the template layer comes from the device
+(``gse_area_templates``: the partials exactly as the template kernel wrote them), the Jacobian is
+materialised and the blocks are formed by sparse triple products on the host -- so a disagreement with
+``fused_accumulate`` isolates the device accumulation program.
 """
 
 from __future__ import annotations
@@ -38,6 +41,22 @@ class AreaNormalBlocks:
     @property
     def n_boundary(self):
         return self.g_bb.shape[0]
+
+
+@dataclass
+class JacobianTriplets:
+    """Materialized area Jacobian (oracle path only; reference assembly.py:57-72)."""
+
+    rows: np.ndarray
+    cols: np.ndarray
+    vals: np.ndarray
+    weights: np.ndarray
+    residuals: np.ndarray
+    n_rows: int
+    n_cols: int
+
+    def to_csr(self):
+        return sp.csr_matrix((self.vals, (self.rows, self.cols)), shape=(self.n_rows, self.n_cols))
 
 
 def area_row_ids(vmap: AreaVariableMap, ms: MeasurementSet) -> np.ndarray:
@@ -132,3 +151,37 @@ def fused_accumulate(vmap: AreaVariableMap, ms: MeasurementSet, x_i, x_b,
     g_ii = sp.csr_matrix((data_ii, pat.gii_indices, pat.gii_indptr), shape=(n_i, n_i))
     g_ib = sp.csr_matrix((data_ib, pat.gib_indices, pat.gib_indptr), shape=(n_i, n_b))
     return AreaNormalBlocks(g_ii=g_ii, g_ib=g_ib, g_bb=g_bb, b_i=b_i, b_b=b_b)
+
+
+def explicit_assemble(vmap: AreaVariableMap, ms: MeasurementSet, x_i, x_b, pattern: AssemblyPattern = None):
+    """Materialize H and form the blocks by sparse triple products (reference assembly.py:531-572).
+
+    The template values are the device's (one ``gse_phase_assemble``, read back with ``gse_area_templates``);
+    the residuals are ``z - h`` from the host formulas; ``H^T W H`` and ``H^T W r`` are scipy products.  Returns
+    ``(JacobianTriplets, AreaNormalBlocks)`` like the reference.
+    """
+    from .measurement import StateVector, eval_h_all
+    pat = pattern if pattern is not None else build_patterns(vmap, ms)
+    pat.refresh(ms)
+    net = ms.net
+    va, vm = pat.scatter_state(net, np.asarray(x_i, float), np.asarray(x_b, float))
+    torch = pat._torch
+    pat._state.copy_(torch.from_numpy(np.stack([va, vm])))
+    torch.cuda.current_stream(pat._dev).synchronize()
+    pat.plan.phase_assemble(pat._state[0].data_ptr(), pat._state[1].data_ptr())
+    rows, slot_ptr, slot_var, g_flat, _ = pat.plan.area_templates(0)
+    row_ids = pat.row_ids
+    assert np.array_equal(rows, np.arange(len(row_ids)))         # the pattern's plan holds exactly the area's rows
+    n_i, n_b = vmap.n_interior, vmap.n_boundary
+    weights = ms.weight[row_ids]
+    resid = ms.z[row_ids] - eval_h_all(pat._ms, StateVector(va=va, vm=vm))
+    triplets = JacobianTriplets(rows=np.repeat(np.arange(len(row_ids)), np.diff(slot_ptr)), cols=slot_var.astype(int),
+                                vals=g_flat, weights=weights, residuals=resid, n_rows=len(row_ids), n_cols=n_i + n_b)
+    h_mat = triplets.to_csr()
+    hw = h_mat.multiply(weights[:, None]).tocsr()
+    g_full = (h_mat.T @ hw).tocsr()
+    g_full.sort_indices()
+    b_full = h_mat.T @ (weights * resid)
+    blocks = AreaNormalBlocks(g_ii=g_full[:n_i, :n_i].tocsr(), g_ib=g_full[:n_i, n_i:].tocsr(),
+                              g_bb=g_full[n_i:, n_i:].toarray(), b_i=b_full[:n_i], b_b=b_full[n_i:])
+    return triplets, blocks

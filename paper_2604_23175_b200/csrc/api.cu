@@ -971,7 +971,7 @@ int gse_area_dims(const gse_plan* plan, int32_t a, int32_t* out) {
     out[2] = (int)hp.ii_idx[a].size(); out[3] = (int)hp.ib_idx[a].size();
     int nfr = 0; int64_t lnz = 0;
     for (auto& f : hp.fronts) if (f.area == a && f.kind == 0) { ++nfr; lnz += (int64_t)(f.p + f.u1 - 1) * f.p; }
-    out[4] = 0; out[5] = 0; out[6] = nfr; out[7] = (int32_t)std::min<int64_t>(lnz, 2147483647);
+    out[4] = (int32_t)hp.tmpl_rows[a].size(); out[5] = (int32_t)hp.tmpl_slot_var[a].size(); out[6] = nfr; out[7] = (int32_t)std::min<int64_t>(lnz, 2147483647);
     return GSE_OK;
 }
 int gse_area_pattern(const gse_plan* plan, int32_t a, int32_t* ii_ptr, int32_t* ii_idx, int32_t* ib_ptr, int32_t* ib_idx) {
@@ -993,6 +993,25 @@ int gse_area_blocks(gse_plan* plan, int32_t a, double* data_ii, double* data_ib,
     CU(copy_sync(plan, g_bb, base + nii + nib, nb * nb * 8, cudaMemcpyDeviceToHost));
     CU(copy_sync(plan, b_i, base + nii + nib + nb * nb, ni * 8, cudaMemcpyDeviceToHost));
     CU(copy_sync(plan, b_b, base + nii + nib + nb * nb + ni, nb * 8, cudaMemcpyDeviceToHost));
+    return GSE_OK;
+}
+// The area's materialised template layer after gse_phase_assemble (the reference's explicit oracle path,
+// assembly.py:531-560: JacobianTriplets): per owned row k its global row id, slot range and local variable per slot
+// (reference numbering: interior x_i slots, then n_i + local boundary slot), the partial dh/dx per slot as the
+// template kernel wrote it, and the weighted residual w (z - h) per row.
+int gse_area_templates(gse_plan* plan, int32_t a, int32_t* rows, int32_t* slot_ptr, int32_t* slot_var, double* g, double* wr) {
+    const HostProgram& hp = plan->hp;
+    if (a < 0 || a >= hp.n_areas || !hp.owned[a]) return fail(plan, GSE_E_INVALID, "area not owned by this plan");
+    CU(cudaSetDevice(plan->device));
+    const size_t nr = hp.tmpl_rows[a].size(), ns = hp.tmpl_slot_var[a].size();
+    for (size_t k = 0; k < nr; ++k) rows[k] = hp.tmpl_rows[a][k];
+    for (size_t k = 0; k <= nr; ++k) slot_ptr[k] = hp.tmpl_slot_ptr[a][k];
+    for (size_t s = 0; s < ns; ++s) slot_var[s] = hp.tmpl_slot_var[a][s];
+    std::vector<double> pairs(2 * ns), allwr((size_t)hp.n_rows);
+    CU(copy_sync(plan, pairs.data(), plan->val.ptr + 2 * hp.tmpl_slot_base[a], pairs.size() * 8, cudaMemcpyDeviceToHost));
+    CU(copy_sync(plan, allwr.data(), plan->val.ptr + 2 * hp.n_slots, allwr.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t s = 0; s < ns; ++s) g[s] = pairs[2 * s];
+    for (size_t k = 0; k < nr; ++k) wr[k] = allwr[(size_t)hp.tmpl_rows[a][k]];
     return GSE_OK;
 }
 // packed lower (rows in front order) -> full symmetric in the caller's order; pos[i] = front row of item i

@@ -375,3 +375,44 @@ def test_inner_gn_steps_match_reference_golden(G, name, inner):
     # without the callback the same loop runs (inner steps are host-sequenced): identical result
     est2, rep2 = G.solve_multiarea(net, ms, part, config=G.SolverConfig(inner_gn_steps=inner))
     assert rep2.iterations == rep.iterations and np.array_equal(est2.va, est.va) and np.array_equal(est2.vm, est.vm)
+
+
+def test_fused_matches_explicit_jacobian_path(G):
+    """reference test_assembly.py:90-140: ``explicit_assemble`` materialises H (here: the template values the device
+    kernel wrote, read back through gse_area_templates) and forms the blocks by sparse triple products on the host;
+    ``fused_accumulate`` must agree, which isolates the device accumulation program.  The triplets also reproduce
+    the scalar per-row gradients."""
+    net, ms, part, _ = build_case("ieee118_k3")
+    bord, maps = G.build_variable_maps(net, part)
+    rng = np.random.default_rng(11)
+    va = rng.uniform(-0.15, 0.15, net.n_bus)
+    va[net.slack] = net.buses[net.slack].va_true
+    vm = rng.uniform(0.9, 1.1, net.n_bus)
+    st = G.StateVector(va=va, vm=vm)
+    for vmap in maps:
+        lb_ang = vmap.local_boundary_angle_buses()
+        x_i = vmap.gather_interior(va, vm)
+        x_b = np.concatenate([va[lb_ang], vm[vmap.local_boundary_buses]])
+        pat = G.build_patterns(vmap, ms)
+        fused = G.fused_accumulate(vmap, ms, x_i, x_b, pattern=pat)
+        trip, expl = G.explicit_assemble(vmap, ms, x_i, x_b, pattern=pat)
+        assert isinstance(trip, G.JacobianTriplets) and trip.n_cols == vmap.n_interior + vmap.n_boundary
+        h = trip.to_csr()
+        assert h.shape == (len(pat.row_ids), trip.n_cols)
+        scale = 1.0 + (abs(h).T @ (abs(h).multiply(trip.weights[:, None]))).toarray()
+        n_i = vmap.n_interior
+        assert np.max(np.abs(fused.g_ii.toarray() - expl.g_ii.toarray()) / scale[:n_i, :n_i]) < 1e-12
+        assert np.max(np.abs(fused.g_ib.toarray() - expl.g_ib.toarray()) / scale[:n_i, n_i:], initial=0.0) < 1e-12
+        assert np.max(np.abs(fused.g_bb - expl.g_bb) / scale[n_i:, n_i:], initial=0.0) < 1e-12
+        bscale = 1.0 + np.asarray(abs(h).T @ np.abs(trip.weights * trip.residuals)).ravel()
+        assert np.max(np.abs(fused.b_i - expl.b_i) / bscale[:n_i]) < 1e-12
+        assert np.max(np.abs(fused.b_b - expl.b_b) / bscale[n_i:], initial=0.0) < 1e-12
+        # a few rows against the scalar formulas
+        for k in range(0, len(pat.row_ids), 37):
+            r = int(pat.row_ids[k])
+            grad = G.eval_row_gradient(net, ms.mtype[r], ms.target[r], st)
+            dense_row = np.zeros(trip.n_cols)
+            for (b, q), v in grad:
+                dense_row[vmap.local_index(b, q)] += v
+            assert np.max(np.abs(h[k].toarray().ravel() - dense_row)) < 1e-12 * (1.0 + np.max(np.abs(dense_row)))
+            assert trip.residuals[k] == pytest.approx(ms.z[r] - G.eval_h(net, ms.mtype[r], ms.target[r], st), rel=1e-12, abs=1e-14)
