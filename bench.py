@@ -65,7 +65,7 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region (NVML every ~2 ms; nvidia-smi as the fallback)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -75,16 +75,49 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        # NVML (nvidia_ml_py, the library nvidia-smi itself reads) answers in well under a millisecond, so the short
+        # timed region of a latency-bound solve (tens of ms) still gets tens of samples; the nvidia-smi process
+        # (~50 ms per call) is the fallback when NVML cannot be loaded
+        nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            uuid = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            except Exception:
+                pass
+            h = None
+            if uuid:
+                for cand in (uuid, "GPU-" + uuid):
+                    try:
+                        h = pynvml.nvmlDeviceGetHandleByUUID(cand.encode() if isinstance(cand, str) else cand)
+                        break
+                    except Exception:
+                        h = None
+            nv = (pynvml, h if h is not None else pynvml.nvmlDeviceGetHandleByIndex(self.index))
+        except Exception:
+            nv = None
         while not self._stop.is_set():
             try:
+                if nv:
+                    P, h = nv
+                    r = P.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(P, "nvmlDeviceGetCurrentClocksEventReasons") \
+                        else P.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    flag = lambda bit: "Active" if r & bit else "Not Active"
+                    self.samples.append([str(P.nvmlDeviceGetClockInfo(h, P.NVML_CLOCK_SM)), str(P.nvmlDeviceGetMaxClockInfo(h, P.NVML_CLOCK_SM)),
+                                         flag(0x8), flag(0x40), flag(0x20), flag(0x4)])
+                    self._stop.wait(0.002)
+                    continue
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
                 if out:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                nv = None
+            self._stop.wait(0.2 if not nv else 0.002)
 
     def __enter__(self):
         self._t.start()

@@ -16,12 +16,13 @@ __device__ __forceinline__ void put_slot(const EvalProg& ep, int s, double gv, d
     reinterpret_cast<double2*>(ep.g)[s] = make_double2(gv, w * gv);      // (g, w*g) interleaved: one 16-byte store
 }
 
+// (w, z of the row are passed in: the caller fetches them for all rows of the unit in one round of independent
+// loads -- inside this function they would queue behind the stores of the previous row, one L2 round trip each)
 __device__ __forceinline__ void flow_row(const EvalProg& ep, int row, int slot, bool f_slack,
-                                         bool t_slack, double h, double d_thf, double d_tht,
+                                         bool t_slack, double w, double z, double h, double d_thf, double d_tht,
                                          double d_vf, double d_vt) {
     if (row < 0) return;
-    const double w = ep.w[row];
-    ep.wr[row] = w * (ep.z[row] - h);
+    ep.wr[row] = w * (z - h);
     int s = slot;
     if (!f_slack) put_slot(ep, s++, d_thf, w);
     if (!t_slack) put_slot(ep, s++, d_tht, w);
@@ -44,8 +45,14 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
         const double4* yy = reinterpret_cast<const double4*>(ep.br_y + 8 * (size_t)e);
         const double4 y0 = yy[0], y1 = yy[1];   // (ff.re ff.im ft.re ft.im) (tf.re tf.im tt.re tt.im)
         const double vf = ldc(vm + f), vt = ldc(vm + t);
+        const double thf = ldc(va + f), tht = ldc(va + t);
+        // weights and measured values of the unit's rows: independent loads, issued with the state loads
+        const int r6[6] = {rows.x, rows.y, rows.z, rows.w, irows.x, irows.y};
+        double w6[6], z6[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) { w6[k] = r6[k] >= 0 ? ep.w[r6[k]] : 0.0; z6[k] = r6[k] >= 0 ? ep.z[r6[k]] : 0.0; }
         double sn, cs;
-        sincos(ldc(va + f) - ldc(va + t), &sn, &cs);
+        sincos(thf - tht, &sn, &cs);
         const bool fs = f == ep.slack, ts = t == ep.slack;
         // from end: own = f, y_own = y_ff = a + jb, y_oth = y_ft = c + jd, delta = th_f - th_t
         {
@@ -53,9 +60,9 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
             const double ec = c * cs + d * sn, es = c * sn - d * cs;
             const double vv = vf * vt;
             // P = Vf^2 a + Vf Vt ec ; Q = -Vf^2 b + Vf Vt es
-            flow_row(ep, rows.x, slots.x, fs, ts, vf * (vf * a + vt * ec), -vv * es, vv * es,
+            flow_row(ep, rows.x, slots.x, fs, ts, w6[0], z6[0], vf * (vf * a + vt * ec), -vv * es, vv * es,
                      2.0 * vf * a + vt * ec, vf * ec);
-            flow_row(ep, rows.z, slots.z, fs, ts, vf * (-vf * b + vt * es), vv * ec, -vv * ec,
+            flow_row(ep, rows.z, slots.z, fs, ts, w6[2], z6[2], vf * (-vf * b + vt * es), vv * ec, -vv * ec,
                      -2.0 * vf * b + vt * es, vf * es);
         }
         // to end: own = t, y_own = y_tt, y_oth = y_tf, delta = th_t - th_f  (cos same, sin negated)
@@ -63,9 +70,9 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
             const double a = y1.z, b = y1.w, c = y1.x, d = y1.y;
             const double ec = c * cs - d * sn, es = -c * sn - d * cs;
             const double vv = vf * vt;
-            flow_row(ep, rows.y, slots.y, fs, ts, vt * (vt * a + vf * ec), vv * es, -vv * es,
+            flow_row(ep, rows.y, slots.y, fs, ts, w6[1], z6[1], vt * (vt * a + vf * ec), vv * es, -vv * es,
                      vt * ec, 2.0 * vt * a + vf * ec);
-            flow_row(ep, rows.w, slots.w, fs, ts, vt * (-vt * b + vf * es), -vv * ec, vv * ec,
+            flow_row(ep, rows.w, slots.w, fs, ts, w6[3], z6[3], vt * (-vt * b + vf * es), -vv * ec, vv * ec,
                      vt * es, -2.0 * vt * b + vf * es);
         }
         // current magnitudes (north_star template; the reference has none, measurement.py:27-34): with i = y_own V_o +
@@ -79,7 +86,7 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
             const double m2 = A * vf * vf + C * vt * vt + 2.0 * vv * E;
             const double h = sqrt(fmax(m2, 0.0)), ih = m2 > 1e-24 ? 1.0 / h : 0.0;
             const double dth = vv * (-al * sn - be * cs) * ih;
-            flow_row(ep, irows.x, islots.x, fs, ts, h, dth, -dth, (A * vf + vt * E) * ih, (C * vt + vf * E) * ih);
+            flow_row(ep, irows.x, islots.x, fs, ts, w6[4], z6[4], h, dth, -dth, (A * vf + vt * E) * ih, (C * vt + vf * E) * ih);
         }
         if (irows.y >= 0) {
             const double a = y1.z, b = y1.w, c = y1.x, d = y1.y;       // own = t: y_tt, y_tf; d = th_t - th_f (sin negated)
@@ -88,7 +95,7 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
             const double m2 = A * vt * vt + C * vf * vf + 2.0 * vv * E;
             const double h = sqrt(fmax(m2, 0.0)), ih = m2 > 1e-24 ? 1.0 / h : 0.0;
             const double dtt = vv * (al * sn - be * cs) * ih;
-            flow_row(ep, irows.y, islots.y, fs, ts, h, -dtt, dtt, (C * vf + vt * E) * ih, (A * vt + vf * E) * ih);
+            flow_row(ep, irows.y, islots.y, fs, ts, w6[5], z6[5], h, -dtt, dtt, (C * vf + vt * E) * ih, (A * vt + vf * E) * ih);
         }
         return;
     }
@@ -106,6 +113,7 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
         const int p0 = ep.y_ptr[i], p1 = ep.y_ptr[i + 1];
         const double vi = ldc(vm + i), thi = ldc(va + i);
         const double wp = rp >= 0 ? ep.w[rp] : 0.0, wq = rq >= 0 ? ep.w[rq] : 0.0;
+        const double zp = rp >= 0 ? ep.z[rp] : 0.0, zq = rq >= 0 ? ep.z[rq] : 0.0;      // (fetched with the weights, not after the row walk)
         double sum_p = 0.0, sum_q = 0.0, gd = 0.0, bd = 0.0;
         int dth = -1, dvm = -1, cth = 0;
         for (int pb = p0; pb < p1; pb += 4) {
@@ -135,12 +143,12 @@ __device__ __forceinline__ void eval_unit(const EvalProg& ep, int u, const doubl
             }
         }
         if (rp >= 0) {
-            ep.wr[rp] = wp * (ep.z[rp] - vi * (vi * gd + sum_p));
+            ep.wr[rp] = wp * (zp - vi * (vi * gd + sum_p));
             if (dth >= 0) put_slot(ep, sp + dth, -vi * sum_q, wp);
             put_slot(ep, sp + dvm, 2.0 * vi * gd + sum_p, wp);
         }
         if (rq >= 0) {
-            ep.wr[rq] = wq * (ep.z[rq] - vi * (-vi * bd + sum_q));
+            ep.wr[rq] = wq * (zq - vi * (-vi * bd + sum_q));
             if (dth >= 0) put_slot(ep, sq + dth, vi * sum_p, wq);
             put_slot(ep, sq + dvm, -2.0 * vi * bd + sum_q, wq);
         }
