@@ -710,6 +710,11 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
         return fail(plan, GSE_E_INVALID, "gse_solve: max_outer_iterations must be in [1, 64]; drive longer loops with gse_iterate");
     const int max_it = cfg->max_outer_iterations;
     const bool timed = cfg->time_phases != 0;
+    // rank-sharded plans: the loop needs the exchanges -- inside the kernels once the ranks are linked, else the
+    // caller's (gse_phase_*_async + collectives); a plain gse_solve would silently skip them
+    if (plan->hp.world > 1 && !(plan->linked && !timed))
+        return fail(plan, GSE_E_INVALID, plan->linked ? "gse_solve on a peer-linked plan: time_phases is not available (phases overlap across ranks)"
+                                                      : "gse_solve on a rank-sharded plan: link the ranks first (gse_peer_link) or drive the phases (gse_phase_*_async)");
     if (!timed && plan->persistent) return solve_persistent(plan, cfg, max_it, va, vm, rep);
     if (!timed) { int rc = ensure_graph(plan, va, vm); if (rc) return rc; }
     plan->launches_last = 0;
