@@ -123,6 +123,11 @@ int gse_set_rows_pinned(gse_plan *plan, const double *z_pinned, const double *w_
  * the host.  On GSE_E_NOT_SPD_* the report is partially filled. */
 int gse_solve(gse_plan *plan, const gse_config *cfg, double *va_dev, double *vm_dev,
               gse_report *report);
+/* The same solve with its transfers folded into the one enqueue: init_dev = start state (va | vm, 2 n_bus doubles on
+ * the device, e.g. the flat start of solver.py:236 kept resident) copied into va_dev / vm_dev first, or NULL;
+ * out_pinned = pinned host buffer that receives the final (va | vm), or NULL.  One host synchronisation per solve. */
+int gse_solve_io(gse_plan *plan, const gse_config *cfg, const double *init_dev, double *va_dev, double *vm_dev,
+                 double *out_pinned, gse_report *report);
 /* One outer iteration (used when the caller wants on_iteration callbacks, solver.py:334). */
 int gse_iterate(gse_plan *plan, double *va_dev, double *vm_dev, double *delta_inf);
 /* One inner GN step of every owned area with the boundary state held fixed: SolverConfig.inner_gn_steps > 1

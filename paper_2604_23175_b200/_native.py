@@ -113,6 +113,7 @@ def lib():
     L.gse_set_weights.argtypes = [vp, f64p]
     L.gse_set_measurements.argtypes = [vp, f64p]
     L.gse_solve.argtypes = [vp, C.POINTER(Config), vp, vp, C.POINTER(Report)]
+    L.gse_solve_io.argtypes = [vp, C.POINTER(Config), vp, vp, vp, vp, C.POINTER(Report)]
     L.gse_iterate.argtypes = [vp, vp, vp, f64p]
     L.gse_inner_step.argtypes = [vp, vp, vp, f64p]
     L.gse_phase_local_async.argtypes = [vp, vp, vp]
@@ -171,7 +172,7 @@ EXPORTED = [
     "gse_matrix_recover", "gse_assemble_boundary", "gse_phase_local_async", "gse_phase_boundary_async",
     "gse_phase_recover_async", "gse_debug_trace", "gse_solve_layout", "gse_partition_attempt", "gse_partition_thin_cuts",
     "gse_peer_info_get", "gse_peer_link", "gse_peer_solve_prepare",
-    "gse_matrix_perm", "gse_matrix_forward_get", "gse_matrix_backward", "gse_area_templates",
+    "gse_matrix_perm", "gse_matrix_forward_get", "gse_matrix_backward", "gse_area_templates", "gse_solve_io",
 ]
 
 
@@ -317,6 +318,14 @@ class Plan:
         cfg = Config(int(max_iter), float(tol), int(bool(time_phases)))
         rep = Report()
         self._call(lib().gse_solve(self._h, C.byref(cfg), va_ptr, vm_ptr, C.byref(rep)))
+        return rep
+
+    def solve_io(self, init_ptr, va_ptr, vm_ptr, out_pinned_ptr, max_iter=10, tol=1e-6, time_phases=False):
+        """``solve`` with the start-state copy (device) and the result copy (pinned host) in the same enqueue."""
+        cfg = Config(int(max_iter), float(tol), int(bool(time_phases)))
+        rep = Report()
+        self._call(lib().gse_solve_io(self._h, C.byref(cfg), C.c_void_p(init_ptr or None), va_ptr, vm_ptr,
+                                      C.c_void_p(out_pinned_ptr or None), C.byref(rep)))
         return rep
 
     # -- peer-linked multi-rank solve (exchanges inside the persistent kernel) ---------

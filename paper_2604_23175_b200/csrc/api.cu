@@ -102,6 +102,10 @@ struct gse_plan {
     bool persistent = false, stamps = true;
     // peer-linked multi-rank solve (gse_peer_link): exchanges inside the persistent kernel over peer memory
     bool linked = false, prepared = false, shares_device = false;
+    // gse_solve_io: start state (device) copied in and final state copied out (pinned host) on the plan's stream,
+    // inside the same enqueue as the launch -- one host synchronisation per solve
+    const double* io_init = nullptr;
+    double* io_out = nullptr;
     int n_gamma_fronts = 0;
     std::vector<void*> ipc_opened;            // allocations of other processes mapped with cudaIpcOpenMemHandle
 
@@ -654,7 +658,12 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     sp.max_it = max_it; sp.tol = cfg->convergence_tol;
     if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 32 * (size_t)sp.items_per_it * 16, s));
     auto t0 = std::chrono::steady_clock::now();
-    cudaEventRecord(plan->ev[6], s);
+    const size_t nb2 = sizeof(double) * (size_t)plan->hp.n_bus;
+    if (plan->io_init) {      // (va | vm) of the start state, contiguous like the caller's state block or not: two copies
+        CU(cudaMemcpyAsync(va, plan->io_init, nb2, cudaMemcpyDeviceToDevice, s));
+        CU(cudaMemcpyAsync(vm, plan->io_init + plan->hp.n_bus, nb2, cudaMemcpyDeviceToDevice, s));
+    }
+    cudaEventRecord(plan->ev[6], s);      // gpu_s: the loop itself (counter reset, launch, report readback), as gse_solve times it
     if (plan->linked) {
         // the sync block was cleared by gse_peer_solve_prepare BEFORE the ranks' barrier: a peer that starts
         // first may already be counting its area roots into it
@@ -666,6 +675,10 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     CU(launch_solve(sp, plan->ep, plan->ft, va, vm, plan->solve_grid, plan->solve_smem, s, !plan->shares_device));
     CU(cudaMemcpyAsync(plan->h_blk, plan->syncblk.ptr, sizeof(unsigned long long) * kBlkWords, cudaMemcpyDeviceToHost, s));
     cudaEventRecord(plan->ev[7], s);
+    if (plan->io_out) {
+        CU(cudaMemcpyAsync(plan->io_out, va, nb2, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(plan->io_out + plan->hp.n_bus, vm, nb2, cudaMemcpyDeviceToHost, s));
+    }
     CU(cudaStreamSynchronize(s));
     rep->loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     { float ms = 0; cudaEventElapsedTime(&ms, plan->ev[6], plan->ev[7]); rep->gpu_s = ms * 1e-3; }
@@ -744,6 +757,35 @@ int gse_solve(gse_plan* plan, const gse_config* cfg, double* va, double* vm, gse
     { float ms = 0; cudaEventElapsedTime(&ms, plan->ev[6], plan->ev[7]); rep->gpu_s = ms * 1e-3; }
     if (status != GSE_OK) return status;
     return gse_objective(plan, va, vm, &rep->objective);
+}
+
+// gse_solve with the start state and the result transfer folded into the same enqueue: init_dev = (va | vm) start
+// state on the device (2 n_bus doubles, e.g. the flat start kept resident) or NULL, out_pinned = pinned host buffer
+// for the final (va | vm) or NULL.  One host synchronisation per solve on the persistent path; the other paths
+// order the copies around the loop.
+int gse_solve_io(gse_plan* plan, const gse_config* cfg, const double* init_dev, double* va, double* vm, double* out_pinned,
+                 gse_report* rep) {
+    CU(cudaSetDevice(plan->device));
+    const bool fused = plan->persistent && !cfg->time_phases && cfg->max_outer_iterations >= 1 && cfg->max_outer_iterations <= 64
+                       && (plan->hp.world == 1 || plan->linked);
+    const size_t nb2 = sizeof(double) * (size_t)plan->hp.n_bus;
+    if (fused) {
+        plan->io_init = init_dev; plan->io_out = out_pinned;
+        const int rc = gse_solve(plan, cfg, va, vm, rep);
+        plan->io_init = nullptr; plan->io_out = nullptr;
+        return rc;
+    }
+    if (init_dev) {
+        CU(cudaMemcpyAsync(va, init_dev, nb2, cudaMemcpyDeviceToDevice, plan->stream));
+        CU(cudaMemcpyAsync(vm, init_dev + plan->hp.n_bus, nb2, cudaMemcpyDeviceToDevice, plan->stream));
+    }
+    const int rc = gse_solve(plan, cfg, va, vm, rep);
+    if (rc == GSE_OK && out_pinned) {
+        CU(cudaMemcpyAsync(out_pinned, va, nb2, cudaMemcpyDeviceToHost, plan->stream));
+        CU(cudaMemcpyAsync(out_pinned + plan->hp.n_bus, vm, nb2, cudaMemcpyDeviceToHost, plan->stream));
+        CU(cudaStreamSynchronize(plan->stream));
+    }
+    return rc;
 }
 
 // ---- generic Schur-mode matrix plans (standalone linear algebra of reference linalg.py) ---------
