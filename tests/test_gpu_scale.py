@@ -316,96 +316,33 @@ def test_distributed_estimator_single_rank_on_device(G):
     assert np.array_equal(st.va, ref.va) and np.array_equal(st.vm, ref.vm) and rep.objective == rref.objective
 
 
-def _linked_engines(G, net, ms, part, bord, maps, cfg, world, max_ctas):
-    """``world`` rank plans of one problem on the one GPU, peer-linked through their device addresses (the same
-    records a multi-process run exchanges through torch.distributed and maps with CUDA IPC)."""
-    from paper_2604_23175_b200.distributed import CudaEngine, area_work_estimate, assign_areas
-    area_rank = assign_areas(area_work_estimate(maps), world)
-    assert len(set(area_rank.tolist())) == world
-    engines = [CudaEngine(net, ms, part, bord, maps, cfg, r, world, area_rank, 0, max_ctas=max_ctas) for r in range(world)]
-    infos = [e.peer_info() for e in engines]
-    for e in engines:
-        e.peer_link(infos)
-    return engines, area_rank
-
-
-def _run_linked(engines, cfg, flat):
-    """One peer-linked solve: every rank's kernel is launched from its own host thread (the kernels of all ranks
-    must be resident together: they wait for each other's area roots, delta_x_Gamma pieces and norms)."""
-    import threading
-    for e in engines:
-        e.load_state(flat.va, flat.vm)
-        e.solve_prepare()
-    out = [None] * len(engines)
-
-    def work(k):
-        try:
-            out[k] = engines[k].solve_linked(cfg)
-        except Exception as exc:           # noqa: BLE001 -- handed to the asserting thread
-            out[k] = exc
-    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(engines))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    return out
+def _run_tool(script, *args, timeout=300):
+    """A tool script in a process of its own: kernels that wait for one another stay isolated from this session's
+    CUDA context (a watchdog abort is sticky for the process it happens in)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    return subprocess.run([sys.executable, os.path.join(root, "tools", script), *[str(a) for a in args]],
+                          capture_output=True, text=True, timeout=timeout)
 
 
 @pytest.mark.parametrize("name,world", [("ieee118_k6", 2), ("pegase2869_k8", 3), ("pegase9241_k16", 4)])
-def test_peer_linked_rank_plans_match_single_plan_bitwise(G, name, world):
+def test_peer_linked_rank_plans_match_single_plan_bitwise(name, world):
     """The exchanges INSIDE the persistent kernels (gse_peer_link): every rank plan runs the whole GN loop in one
     launch; area roots store (S_b | b_hat) into the coordinator's buffer, the coordinator's back-substitution
     tasks store delta_x_Gamma into every rank's solution vector, the norm is max-merged with atomics.  Same
-    iteration count, per-iteration norms and state bits as the single-plan solve, twice in a row (the counters
-    are re-armed per solve)."""
-    from conftest import build_case
-    net, ms, part, g = build_case(name)
-    bord, maps = G.build_variable_maps(net, part)
-    cfg = G.SolverConfig()
-    single = G.MultiAreaEstimator(net, ms, part, maps=(bord, maps), config=cfg)
-    try:
-        ref, rref = single.estimate()
-        ref_deltas = list(single.last_deltas)
-    finally:
-        single.close()
-    engines, area_rank = _linked_engines(G, net, ms, part, bord, maps, cfg, world, max_ctas=64)
-    try:
-        flat = G.StateVector.flat_start(net)
-        for _ in range(2):
-            reps = _run_linked(engines, cfg, flat)
-            for r in reps:
-                assert not isinstance(r, Exception), r
-                assert r.iterations == rref.iterations == int(g["iterations"]) and r.converged
-                assert [float(r.delta_inf[k]) for k in range(r.iterations)] == ref_deltas
-            state = engines[0].state.clone()
-            for r in range(1, world):
-                m = engines[r].owned_mask
-                state[:, m] = engines[r].state[:, m]
-            out = state.cpu().numpy()
-            assert np.array_equal(out[0], ref.va) and np.array_equal(out[1], ref.vm)
-            j = engines[0].plan.objective(state[0].data_ptr(), state[1].data_ptr())
-            assert j == rref.objective
-    finally:
-        for e in engines:
-            e.close()
+    iteration count, per-iteration norms, state bits and J as the single-plan solve, twice in a row
+    (tools/linked_check.py: ``world`` rank plans side by side on the one GPU)."""
+    out = _run_tool("linked_check.py", name, world)
+    assert out.returncode == 0 and "linked ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
 
 
-def test_peer_linked_solve_reports_unobservable_area_on_every_rank(G):
+def test_peer_linked_solve_reports_unobservable_area_on_every_rank():
     """A factorisation that fails on one rank stops ALL ranks at the end of that iteration with the same error
     (the failure code is max-merged into every rank's copy; reference solver.py:250-251)."""
-    from conftest import build_case
-    net, ms, part, g = build_case("ieee14_k2")
-    vm_only = G.apply_mask(ms, lambda t, tg: t != G.MeasurementType.VM)
-    bord, maps = G.build_variable_maps(net, part)
-    cfg = G.SolverConfig()
-    engines, _ = _linked_engines(G, net, vm_only, part, bord, maps, cfg, 2, max_ctas=32)
-    try:
-        reps = _run_linked(engines, cfg, G.StateVector.flat_start(net))
-        for r in reps:
-            assert isinstance(r, G.SolverError) and "likely locally unobservable" in str(r)
-    finally:
-        for e in engines:
-            e.close()
+    out = _run_tool("linked_check.py", "--unobservable")
+    assert out.returncode == 0 and "linked ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
 
 
 def test_peer_linked_ranks_in_separate_processes_over_cuda_ipc():
@@ -413,10 +350,5 @@ def test_peer_linked_ranks_in_separate_processes_over_cuda_ipc():
     other's buffers with CUDA IPC handles and solve with one persistent launch each -- here time-sharing the one
     GPU, on a node one process per GPU.  tools/ipc_two_process.py asserts bit-equality with the single-plan solve,
     twice in a row, through DistributedEstimator(exchange="peer")."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, os.path.join(root, "tools", "ipc_two_process.py"), "ieee118_k6", "2"],
-                         capture_output=True, text=True, timeout=240)
+    out = _run_tool("ipc_two_process.py", "ieee118_k6", 2, timeout=240)
     assert out.returncode == 0 and "ipc ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
