@@ -461,6 +461,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     plan->ft.task0 = plan->tasks.ptr; plan->ft.tbuf = nullptr; plan->ft.crecs = plan->crecs.ptr;
     std::vector<BwdTask> btasks;
     int pbase = 0;
+    std::vector<int> pivot_owner((size_t)hp.n_pos + 2, -1);       // solution position -> front that eliminates it (on this rank)
+    for (size_t f = 0; f < nf; ++f) for (int k = 0; k < hp.fronts[f].p; ++k) pivot_owner[hp.fronts[f].rows[k]] = (int)f;
     for (size_t i = 0; i < hp.bwd_levels.size(); ++i) {
         BwdLaunch B{(int)btasks.size(), 0, hp.bwd_phase[i]};
         for (int f : hp.bwd_levels[i]) {
@@ -474,6 +476,13 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
                 bt.front = f; bt.split = sp; bt.nsplit = ns; bt.pbase = pbase; bt.p = fr.p; bt.u = u;
                 bt.rows_off = frows_off[f]; bt.dinv_off = dinv_off[f]; bt.l_off = fr.l_off;
                 bt.dep = dep; bt.need = fr.nch; bt.phase = hp.bwd_phase[i];   // need: tasks that store a factor panel
+                // update rows are in elimination order, so the nearest ancestor's pivots come first (at most 64 of
+                // them: all inside split 0); rows 64 ... belong to the front that eliminates row 64 or to its ancestors
+                bt.dep2 = dep; bt.early = 0;
+                if (ns > 1 && dep >= 0) {
+                    const int o = pivot_owner[fr.rows[fr.p + 64]];
+                    if (o >= 0 && o != dep) { bt.dep2 = o; bt.early = 1; }
+                }
                 btasks.push_back(bt);
             }
             pbase += ns; B.count += ns;

@@ -159,6 +159,9 @@ __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec*
 // Dependency hooks of a front task.  The level-launch kernels run a whole tree level per launch,
 // so their hooks are empty; the persistent kernel spins on completion counters here.
 struct NoWait {
+    static constexpr bool kEarlySplits = false;      // one launch per level: every split of a level starts together
+    __device__ __forceinline__ void ancestor(const BwdTask&) const {}
+    __device__ __forceinline__ void splits(const int32_t*, int) const {}
     __device__ __forceinline__ void factor(const BwdTask&) const {}
     __device__ __forceinline__ void parent(const BwdTask&) const {}
     __device__ __forceinline__ void originals(const TaskRec&) const {}
@@ -691,7 +694,10 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
 #pragma unroll
         for (int i = 0; i < kBwdRows / 2; ++i) v[i] = (k < p && tid < 128 && a + i < b) ? ldc(col + (size_t)(a + i) * p) : 0.0;
     }
-    wait.parent(tk);
+    // Early splits (dataflow kernel): the later splits of a front only read entries of ancestors above the nearest
+    // one, so they wait for front dep2 and finish a level ahead; split 0 -- the only one on the chain -- combines.
+    const bool early = Wait::kEarlySplits && tk.early != 0;
+    if (early && tk.split > 0) wait.ancestor(tk); else wait.parent(tk);
     if (tid < kBwdRows) xs[tid] = xrow >= 0 ? ldc(xsol + xrow) : 0.0;
     __syncthreads();
     {
@@ -708,7 +714,18 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
         if (tid < 128) half[h][k] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
-    if (tk.nsplit > 1) {
+    if (early) {
+        if (tk.split > 0) {
+            if (tid < 64) bpart[(size_t)(tk.pbase + tk.split) * 64 + tid] = half[0][tid] + half[1][tid];
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd(&bcnt[f], 1);
+            asm volatile("cp.async.wait_group 0;\n" ::);
+            __syncthreads();
+            return false;
+        }
+        wait.splits(bcnt + f, tk.nsplit - 1);      // (long done when this split is released: they ran a level ahead)
+    } else if (tk.nsplit > 1) {
         if (tid < 64) bpart[(size_t)(tk.pbase + tk.split) * 64 + tid] = half[0][tid] + half[1][tid];
         __threadfence();
         __syncthreads();
@@ -724,6 +741,14 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
             // a single split (at most 64 update rows, most fronts): the partial sum never leaves the CTA
             // (0.0 + s, the same sum the general path forms after its round trip through global memory)
             acc = tid < p ? yk - (0.0 + (half[0][tid] + half[1][tid])) : 0.0;
+        } else if (early) {
+            // split 0 combines: its own partial from shared memory, the others' in split order (the same sum)
+            if (tid < p) {
+                const volatile double* bp = bpart + (size_t)tk.pbase * 64 + tid;
+                acc = 0.0 + (half[0][tid] + half[1][tid]);
+                for (int s = 1; s < tk.nsplit; ++s) acc += bp[(size_t)s * 64];
+                acc = yk - acc;
+            }
         } else if (tid < p) {
             const volatile double* bp = bpart + (size_t)tk.pbase * 64 + tid;
             int s = 0;

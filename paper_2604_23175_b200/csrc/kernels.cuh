@@ -41,7 +41,10 @@ struct TaskRec {                                      // 128 bytes
 // counted per area (CTR_AREA0).
 struct ChildRec { int64_t u_off; int32_t rel_off, eP, bI, eI, bJ, eJ; int32_t front, need, pad[2]; };   // 48 bytes
 // dep: nearest ancestor front with pivots (-1: none); need: forward tasks of the own front
-struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, dinv_off; int64_t l_off; int32_t dep, need, phase, pad[3]; };   // 64 bytes
+// dep2 / early: fronts with several splits whose later splits (update rows 64 ...) only read solution entries of
+// ancestors ABOVE the nearest one (its pivots are the first update rows): those splits wait for front dep2 instead and
+// finish a level early; split 0 -- the only one that needs the nearest ancestor -- combines (backward_body).
+struct BwdTask { int32_t front, split, nsplit, pbase, p, u, rows_off, dinv_off; int64_t l_off; int32_t dep, need, phase, dep2, early, pad; };   // 64 bytes
 static_assert(sizeof(TaskRec) == 128 && sizeof(ChildRec) == 48 && sizeof(BwdTask) == 64, "device record layout");
 
 

@@ -97,6 +97,16 @@ struct SpinWait {
     int n_fronts, front0;
     bool sys;                // peer-linked solve: child counters may be bumped by other GPUs
     unsigned gamma_need;     // non-coordinator ranks: pieces of delta_x_Gamma to wait for (0: none)
+    // early splits of the back-substitution (front_body.cuh): later splits wait for front dep2; split 0 for the others
+    static constexpr bool kEarlySplits = true;
+    __device__ __forceinline__ void ancestor(const BwdTask& tk) const {
+        if (threadIdx.x == 0) { wait_ge(ctr + front0 + 2 * n_fronts + tk.dep2, epoch); if (tr) tr[2] = globaltimer(); }
+        __syncthreads();
+    }
+    __device__ __forceinline__ void splits(const int32_t* cnt, int need) const {
+        if (threadIdx.x == 0) wait_ge(reinterpret_cast<const unsigned*>(cnt), (unsigned)need);
+        __syncthreads();
+    }
     // completion counter of a child: its front's, or -- root of an area another rank owns -- the area's
     __device__ __forceinline__ const unsigned* child_ctr(int cf) const { return cf >= 0 ? ctr + front0 + cf : ctr + CTR_AREA0 + (-cf - 1); }
     // backward tasks: own factor complete (all its panel-storing tasks), then the nearest ancestor solved
