@@ -120,3 +120,19 @@ for it in range(rep.iterations):
                 print(f"     p>={key[0]:2d} u{key[1]} | {int(n):6d} {d[1]:10.0f} {d[2]:10.0f} | {d[3]/n:5.1f} {d[4]/n:5.1f} {d[5]/n:5.1f} {d[6]/n:5.1f} {d[7]/n:5.1f}")
             bb = blk[bounds[3]:bounds[4]]
             print(f"   backward tasks: n={len(bb)} exec total {np.sum(bb[:,3]-np.maximum(bb[:,2],bb[:,0]))/1e3:.0f} us  held total {np.sum(bb[:,3]-bb[:,0])/1e3:.0f} us")
+        if os.environ.get("GSE_TRACE_FRONT"):
+            # every task of one front: tile, SM, when it was ready / ended, its phases; and which other front task shared its SM
+            want = int(os.environ["GSE_TRACE_FRONT"])
+            bf = blk[bounds[2]:bounds[3]]
+            s0 = blk[:, 0].min()
+            rows = []
+            for i in range(len(bf)):
+                f = int((bf[i, 6] >> 8) & 0xffffff)
+                rdy = max(bf[i, 1], bf[i, 2], bf[i, 0])
+                rows.append((f, int((bf[i, 6] >> 32) & 0xffff), int((bf[i, 6] >> 48) & 0xffff), int(bf[i, 4] & 0xffff), rdy - s0, bf[i, 3] - s0, bf[i, 8:16]))
+            print(f"   tasks of front {want} (ci cj sm | ready end exec | gather panel update | tasks of other fronts busy on the same SM meanwhile):")
+            for f, ci, cj, sm, rdy, end, st in rows:
+                if f != want: continue
+                mates = [(g, a, b) for g, a, b, sm2, r2, e2, _ in rows if sm2 == sm and not (g == f and a == ci and b == cj) and r2 < end and e2 > rdy]
+                cw = st[7]
+                print(f"     {ci:2d},{cj:2d} sm {sm:3d} | {rdy/1e3:7.1f} {end/1e3:7.1f} {(end-rdy)/1e3:5.1f} | {(st[3]-max(cw, rdy+s0))/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} {(st[5]-st[4])/1e3:5.1f} | {mates[:3]}")
