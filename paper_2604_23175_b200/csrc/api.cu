@@ -420,7 +420,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
                 TaskRec r{};
                 r.front = t.front; r.ci = t.ci; r.cj = t.cj; r.p = f.p; r.u1 = f.u1; r.T = T;
                 r.gval_off = f.gval_off; r.l_off = f.l_off; r.u_off = f.u_off; r.flags = (direct ? 1 : 0) | (f.n_orig > 0 ? 2 : 0) | ((f.kind == 1 && bo.world > 1 && bo.rank != 0) ? 4 : 0);
-                r.phase = phase; r.kind = kind; r.nch = f.nch; r.area = f.area;
+                r.phase = phase; r.kind = kind; r.nch = f.nch; r.area = f.area; r.level = f.level;
                 r.dinv_off = dinv_off[t.front];
                 const int32_t* rp = &hp.reg_ptr[hp.front_reg_off[t.front]];
                 const int ridI = (t.ci + 1) * (t.ci + 2) / 2, ridJ = (t.cj + 1) * (t.cj + 2) / 2;
@@ -531,6 +531,26 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         sp.gval = plan->gval.ptr; sp.lbuf = plan->lbuf.ptr; sp.ubuf = plan->ubuf.ptr; sp.xsol = plan->xsol.ptr;
         sp.bpart = plan->bpart.ptr; sp.obj_partial = plan->obj_partial.ptr; sp.bcnt = plan->bcnt.ptr;
         sp.front0 = ctr_front0(hp.n_areas);
+        // chain suffix of the task list: from the first boundary-phase level on whose level -- and every later one --
+        // has at most ~one task per SM.  Those tasks are the latency chain; the persistent kernel hands them to one
+        // CTA per SM only (two panel factorisations on one SM slow each other by a quarter).
+        sp.chain_first = n_solve_tasks;
+        {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
+            std::vector<int> per_level(hp.fwd_levels.size() + 1, 0);
+            for (int t = 0; t < n_solve_tasks; ++t) per_level[trecs[t].level]++;
+            int first = n_solve_tasks;
+            for (int t = n_solve_tasks - 1; t >= 0; --t) {
+                if (trecs[t].phase != 3 || per_level[trecs[t].level] > sms - 8) break;
+                first = t;
+            }
+            // (whole levels only)
+            while (first < n_solve_tasks && first > 0 && trecs[first - 1].level == trecs[first].level) ++first;
+            if (sp.items_per_it < 4 * 2 * sms) first = n_solve_tasks;     // small plans: a grid's worth of pulls spans iterations
+            if (const char* e = getenv("GSE_CHAIN_SM")) { if (!atoi(e)) first = n_solve_tasks; }
+            sp.chain_first = first;
+        }
         const size_t nctr = sp.front0 + 3 * nf;
         plan->sync_bytes = sizeof(unsigned long long) * kBlkWords + sizeof(unsigned) * nctr;
         CU(plan->syncblk.alloc(kBlkWords + (nctr + 1) / 2));

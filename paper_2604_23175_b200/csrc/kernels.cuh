@@ -31,7 +31,7 @@ struct TaskRec {                                      // 128 bytes
                                                       //       bit 1: the front has original entries (waits for the accumulation)
                                                       //       bit 2: area root of a non-coordinator rank -- its update matrix (S_b | b_hat)
                                                       //              goes straight into the coordinator's exchange buffer (peer memory)
-    int32_t phase, kind, nch, area, pad[4];           // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
+    int32_t phase, kind, nch, area, level, pad[3];    // phase: 1 local_condense, 2 boundary_assemble, 3 boundary_solve
                                                       // kind: 0 fused, 1 panel, 2 update (front_body.cuh); nch: row chunks of the front
                                                       // area: owning area of the front (-1: boundary front)
 };
@@ -120,7 +120,8 @@ constexpr int kEvalPerItem = 256, kUpdPerItem = 1024;
 enum { CTR_NEXT = 0, CTR_EVAL = 32, CTR_ACC = 64, CTR_FWD = 96, CTR_BWD = 128, CTR_UPD = 160, CTR_OBJ = 192,
        CTR_GAMMA = 224,      // peer-linked solve: boundary fronts whose share of delta_x_Gamma has arrived from the coordinator
        CTR_ITER = 256,       // peer-linked solve: ranks that have finished (and published the norm of) an iteration
-       CTR_AREA0 = 288 };    // peer-linked solve: per AREA, tasks of its root that have stored their tile of (S_b | b_hat) in the
+       CTR_SM0 = 288,        // per SM (512 slots): CTAs of this launch seen on it -- the second one keeps off the chain tasks (solve_kernel.cu)
+       CTR_AREA0 = 288 + 512 };    // peer-linked solve: per AREA, tasks of its root that have stored their tile of (S_b | b_hat) in the
                              // coordinator's buffer (fronts are numbered per rank, areas are not)
 // per-front counters from SolveProg::front0 = CTR_AREA0 + n_areas rounded up to 32: fdone[n_fronts] (tasks that
 // wrote U), pdone[n_fronts] (tasks that stored a factor panel), bdone[n_fronts] (backward solves)
@@ -146,7 +147,8 @@ struct PeerLink {
 struct SolveProg {
     int32_t n_eval_items, n_acc_items, n_tasks, n_btasks, n_upd_items, items_per_it;
     int32_t n_units, n_upd, n_bwd_fronts, n_fronts, n_rows, max_it;
-    int32_t front0, pad0;         // offset of the per-front counters inside ctr (ctr_front0(n_areas))
+    int32_t front0, chain_first;  // offset of the per-front counters inside ctr (ctr_front0(n_areas)); first task of the chain
+                                  // suffix: boundary-phase tasks of levels with at most one task per SM (n_tasks: none)
     int64_t n_gval;
     double tol;
     const TaskRec* tasks;

@@ -195,8 +195,37 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
     int known = 0;          // iterations [0, known) are complete and did not stop the loop
     int final_it = 0;       // iterations performed when the loop stopped
     int converged = 0, failed = 0;
+    // Two panel factorisations on one SM slow each other by a quarter (shared FP64 port and shared-memory pipes: panel
+    // 8.4 -> 10.5-12.5 us, tools/persist_trace.py GSE_TRACE_FRONT), and on the boundary chain the slowest task of a front
+    // sets the pace.  The chain suffix of the task list (SolveProg::chain_first: levels with at most one task per SM)
+    // is therefore handed out to ONE CTA per SM: the second CTA of an SM does not pull while the head of the queue is
+    // inside that suffix.  Items are still handed out in increasing order and the first CTAs never hold back, so the
+    // smallest unfinished item is always held by a running CTA, as before.
+    bool second_on_sm = false;
+    const int chain_lo = o_front + sp.chain_first;
+    if (tid == 0 && chain_lo < o_bwd) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+        second_on_sm = (atomicAdd(ctr + CTR_SM0 + (smid & 511u), 1u) & 1u) != 0u;
+    }
     for (;;) {
-        if (tid == 0) s_item = (int)atomicAdd(ctr + CTR_NEXT, 1u);
+        if (tid == 0) {
+            if (second_on_sm) {
+                // (bounded patience: a head that has not moved for ~60 us means the others have left the loop -- the
+                // solve has stopped -- or hold everything they can; pull then, like any CTA)
+                unsigned last = ~0u, still = 0;
+                for (;;) {
+                    const unsigned head = *reinterpret_cast<volatile unsigned*>(ctr + CTR_NEXT);
+                    const int l = (int)(head % (unsigned)sp.items_per_it);
+                    if (l < chain_lo || l >= o_bwd || head / (unsigned)sp.items_per_it >= (unsigned)sp.max_it) break;
+                    still = head == last ? still + 1 : 0;
+                    last = head;
+                    if (still > 200) break;
+                    __nanosleep(300);
+                }
+            }
+            s_item = (int)atomicAdd(ctr + CTR_NEXT, 1u);
+        }
         __syncthreads();
         const int item = s_item;
         const int it = min(item / sp.items_per_it, sp.max_it);
