@@ -531,25 +531,38 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         sp.gval = plan->gval.ptr; sp.lbuf = plan->lbuf.ptr; sp.ubuf = plan->ubuf.ptr; sp.xsol = plan->xsol.ptr;
         sp.bpart = plan->bpart.ptr; sp.obj_partial = plan->obj_partial.ptr; sp.bcnt = plan->bcnt.ptr;
         sp.front0 = ctr_front0(hp.n_areas);
-        // chain suffix of the task list: from the first boundary-phase level on whose level -- and every later one --
-        // has at most ~one task per SM.  Those tasks are the latency chain; the persistent kernel hands them to one
-        // CTA per SM only (two panel factorisations on one SM slow each other by a quarter).
-        sp.chain_first = n_solve_tasks;
+        // chain ranges of the task list: runs of levels with at most ~one panel task per SM (the top of the areas, the
+        // boundary tree).  Those tasks are the latency chains; the persistent kernel hands them to one CTA per SM only
+        // (two panel factorisations on one SM slow each other by a quarter).
+        sp.n_chain = 0;
         {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
-            std::vector<int> per_level(hp.fwd_levels.size() + 1, 0);
-            for (int t = 0; t < n_solve_tasks; ++t) per_level[trecs[t].level]++;
-            int first = n_solve_tasks;
-            for (int t = n_solve_tasks - 1; t >= 0; --t) {
-                if (trecs[t].phase != 3 || per_level[trecs[t].level] > sms - 8) break;
-                first = t;
+            std::vector<int> panels(hp.fwd_levels.size() + 1, 0), total(hp.fwd_levels.size() + 1, 0);
+            for (int t = 0; t < n_solve_tasks; ++t) { total[trecs[t].level]++; panels[trecs[t].level] += trecs[t].p > 0; }
+            bool on = sp.items_per_it >= 4 * 2 * sms;           // small plans: a grid's worth of pulls spans iterations
+            if (const char* e = getenv("GSE_CHAIN_SM")) on = on && atoi(e) != 0;
+            int mode = 1;                                       // 1: the boundary suffix (measured best), 2: every sparse run (the top interior levels too: 0.5 % slower)
+            if (const char* e = getenv("GSE_CHAIN_MODE")) mode = atoi(e);
+            auto sparse = [&](int t) {
+                const int lv = trecs[t].level;
+                if (mode == 1) return trecs[t].phase == 3 && total[lv] <= sms - 8;
+                return panels[lv] > 0 && panels[lv] <= sms - 8 && total[lv] <= 2 * sms;
+            };
+            for (int t = 0; on && t < n_solve_tasks;) {
+                if (!sparse(t)) { ++t; continue; }
+                int e = t;
+                while (e < n_solve_tasks && sparse(e)) ++e;
+                if (e - t >= 8) {
+                    if (sp.n_chain == 4) { sp.chain_hi[3] = e; }       // (more runs than slots: the last slot absorbs the rest)
+                    else { sp.chain_lo[sp.n_chain] = t; sp.chain_hi[sp.n_chain] = e; ++sp.n_chain; }
+                }
+                t = e;
             }
-            // (whole levels only)
-            while (first < n_solve_tasks && first > 0 && trecs[first - 1].level == trecs[first].level) ++first;
-            if (sp.items_per_it < 4 * 2 * sms) first = n_solve_tasks;     // small plans: a grid's worth of pulls spans iterations
-            if (const char* e = getenv("GSE_CHAIN_SM")) { if (!atoi(e)) first = n_solve_tasks; }
-            sp.chain_first = first;
+            if (mode == 1 && sp.n_chain) {                      // the suffix form: only a run that reaches the end of the list
+                if (sp.chain_hi[sp.n_chain - 1] == n_solve_tasks) { sp.chain_lo[0] = sp.chain_lo[sp.n_chain - 1]; sp.chain_hi[0] = n_solve_tasks; sp.n_chain = 1; }
+                else sp.n_chain = 0;
+            }
         }
         const size_t nctr = sp.front0 + 3 * nf;
         plan->sync_bytes = sizeof(unsigned long long) * kBlkWords + sizeof(unsigned) * nctr;

@@ -197,13 +197,12 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
     int converged = 0, failed = 0;
     // Two panel factorisations on one SM slow each other by a quarter (shared FP64 port and shared-memory pipes: panel
     // 8.4 -> 10.5-12.5 us, tools/persist_trace.py GSE_TRACE_FRONT), and on the boundary chain the slowest task of a front
-    // sets the pace.  The chain suffix of the task list (SolveProg::chain_first: levels with at most one task per SM)
-    // is therefore handed out to ONE CTA per SM: the second CTA of an SM does not pull while the head of the queue is
-    // inside that suffix.  Items are still handed out in increasing order and the first CTAs never hold back, so the
+    // sets the pace.  The chain ranges of the task list (SolveProg::chain_lo / chain_hi: runs of levels with at most one panel
+    // task per SM) are therefore handed out to ONE CTA per SM: the second CTA of an SM does not pull while the head of
+    // the queue is inside such a range.  Items are still handed out in increasing order and the first CTAs never hold back, so the
     // smallest unfinished item is always held by a running CTA, as before.
     bool second_on_sm = false;
-    const int chain_lo = o_front + sp.chain_first;
-    if (tid == 0 && chain_lo < o_bwd) {
+    if (tid == 0 && sp.n_chain > 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
         second_on_sm = (atomicAdd(ctr + CTR_SM0 + (smid & 511u), 1u) & 1u) != 0u;
@@ -217,7 +216,11 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
                 for (;;) {
                     const unsigned head = *reinterpret_cast<volatile unsigned*>(ctr + CTR_NEXT);
                     const int l = (int)(head % (unsigned)sp.items_per_it);
-                    if (l < chain_lo || l >= o_bwd || head / (unsigned)sp.items_per_it >= (unsigned)sp.max_it) break;
+                    const int t = l - o_front;
+                    bool in_chain = false;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) in_chain = in_chain || (k < sp.n_chain && t >= sp.chain_lo[k] && t < sp.chain_hi[k]);
+                    if (!in_chain || head / (unsigned)sp.items_per_it >= (unsigned)sp.max_it) break;
                     still = head == last ? still + 1 : 0;
                     last = head;
                     if (still > 200) break;
