@@ -322,6 +322,19 @@ void build_acc_items(HostProgram& hp) {
 
 }  // namespace
 
+
+// Cut point q of a node of nv pivots split into `pieces` fronts: even shares, moved up to the next multiple of 8 when
+// every piece still fits pmax -- the panel factorisation runs in 8-pivot blocks, so 116 pivots cost 8 + 7 blocks as
+// 64 + 52 but 8 + 8 as 58 + 58.
+static inline int piece_cut(int nv, int pieces, int q, int pmax) {
+    if (q <= 0) return 0;
+    if (q >= pieces) return nv;
+    const int even = (int)((int64_t)nv * q / pieces);
+    const int up = (even + 7) & ~7;
+    // the pieces before the cut get at most `up - previous cut` <= pmax when up <= q * pmax; the rest must fit too
+    if (up < nv && up <= q * pmax && nv - up <= (pieces - q) * pmax && up - (int)((int64_t)nv * (q - 1) / pieces) <= pmax + 7) return up;
+    return even;
+}
 std::string build_host_program(const gse_problem_desc& d, const BuildOptions& opt, HostProgram& hp) {
     const int nbus = d.n_bus, K = d.n_areas, m = d.n_rows, ng = d.n_gamma;
     if (nbus <= 0 || K <= 0 || m < 0) return "empty problem";
@@ -658,7 +671,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             int nv = (int)vars.size();
             int pieces = (nv + PMAX - 1) / PMAX;
             for (int q = 0; q < pieces; ++q) {
-                int lo = (int)((int64_t)nv * q / pieces), hi = (int)((int64_t)nv * (q + 1) / pieces);
+                int lo = piece_cut(nv, pieces, q, PMAX), hi = piece_cut(nv, pieces, q + 1, PMAX);
                 Front f; f.area = a; f.kind = 0; f.p = hi - lo;
                 for (int i = lo; i < hi; ++i) {
                     A.epos[vars[i]] = ep; A.order[ep] = vars[i];
@@ -874,7 +887,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             for (auto& slots : gamma_nodes) {
                 const int nv = (int)slots.size(), pieces = (nv + PMAX - 1) / PMAX;
                 for (int q = 0; q < pieces; ++q) {
-                    const int lo = (int)((int64_t)nv * q / pieces), hi = (int)((int64_t)nv * (q + 1) / pieces);
+                    const int lo = piece_cut(nv, pieces, q, PMAX), hi = piece_cut(nv, pieces, q + 1, PMAX);
                     Front f; f.kind = 3; f.p = hi - lo;
                     e_lo.push_back(hp.gamma_epos[slots[lo]]); e_hi.push_back(hp.gamma_epos[slots[lo]] + (hi - lo));
                     for (int i = lo; i < hi; ++i) { front_of_rank[hp.gamma_epos[slots[i]]] = (int)hp.fronts.size(); f.rows.push_back(hp.gamma_base + slots[i]); }
