@@ -323,6 +323,58 @@ void build_acc_items(HostProgram& hp) {
 }  // namespace
 
 
+// Fill-free amalgamation of nested-dissection nodes: a node whose update structure is exactly its parent's whole front
+// (pivots + update rows) is eliminated WITH the parent -- the same factor entries, one front and one dependency hop
+// less -- when that saves a front (nodes are cut into fronts of <= pmax pivots) and the node either fits the parent's
+// last front or is tiny (otherwise every task of the parent's fronts factors a taller pivot block: measured slower).
+// Moving the node's elimination to just before its parent is a valid reordering: everything in between belongs to
+// other subtrees.  nodes: vertex lists in elimination order; xadj / adj: the graph; ext: per vertex, ids of variables
+// that are never eliminated here (an area's boundary variables) and belong to every structure that reaches them.
+template <class SlotsOf>
+static void amalgamate_nodes(std::vector<std::vector<int>>& nodes, int nn, const std::vector<int>& xadj, const std::vector<int>& adj,
+                             const std::vector<std::vector<int>>* ext, SlotsOf slots_of, int pmax) {
+    int n_ext = 0;
+    if (ext) for (auto& e : *ext) for (int x : e) n_ext = std::max(n_ext, x + 1);
+    for (bool merged = true; merged;) {
+        merged = false;
+        const int nn_nodes = (int)nodes.size();
+        std::vector<int> node_of(nn, -1), pos_of(nn, -1);
+        { int q = 0; for (int i = 0; i < nn_nodes; ++i) for (int b : nodes[i]) { node_of[b] = i; pos_of[b] = q++; } }
+        // structure of every node (vertices eliminated later that its front reaches), children before parents
+        std::vector<std::vector<int>> st(nn_nodes), se(nn_nodes), kids(nn_nodes);
+        std::vector<int> parent(nn_nodes, -1), mark(nn, -1), emark(n_ext, -1);
+        for (int i = 0; i < nn_nodes; ++i) {
+            const int last = pos_of[nodes[i].back()];
+            auto add = [&](int b) { if (pos_of[b] > last && mark[b] != i) { mark[b] = i; st[i].push_back(b); } };
+            auto add_ext = [&](int x) { if (emark[x] != i) { emark[x] = i; se[i].push_back(x); } };
+            for (int b : nodes[i]) {
+                for (int e = xadj[b]; e < xadj[b + 1]; ++e) add(adj[e]);
+                if (ext) for (int x : (*ext)[b]) add_ext(x);
+            }
+            for (int c : kids[i]) { for (int b : st[c]) add(b); for (int x : se[c]) add_ext(x); }
+            if (st[i].empty()) continue;
+            int first = st[i][0];
+            for (int b : st[i]) if (pos_of[b] < pos_of[first]) first = b;
+            parent[i] = node_of[first];
+            kids[parent[i]].push_back(i);
+        }
+        auto pieces = [&](int v) { return (v + pmax - 1) / pmax; };
+        for (int i = 0; i < nn_nodes && !merged; ++i) {
+            const int q = parent[i];
+            if (q < 0) continue;
+            const int pi = slots_of(nodes[i]), pq = slots_of(nodes[q]);
+            if (pieces(pi + pq) >= pieces(pi) + pieces(pq)) continue;                 // must save a front
+            if (pi + pq > pmax && pi > 8) continue;
+            if (st[i].size() + se[i].size() != nodes[q].size() + st[q].size() + se[q].size()) continue;     // would add fill
+            std::vector<int> both = nodes[i];
+            both.insert(both.end(), nodes[q].begin(), nodes[q].end());
+            nodes[q] = std::move(both);
+            nodes.erase(nodes.begin() + i);
+            merged = true;
+        }
+    }
+}
+
 // Cut point q of a node of nv pivots split into `pieces` fronts: even shares, moved up to the next multiple of 8 when
 // every piece still fits pmax -- the panel factorisation runs in 8-pivot blocks, so 116 pivots cost 8 + 7 blocks as
 // 64 + 52 but 8 + 8 as 58 + 58.
@@ -407,52 +459,9 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         std::vector<int> all(nn); std::iota(all.begin(), all.end(), 0);
         std::vector<std::vector<int>> nodes;
         nd_recurse(g, all, std::max(1, opt.gamma_leaf_buses), nodes);
-        // Fill-free amalgamation: a node whose update structure is exactly its parent's whole front (pivots + update
-        // rows) is eliminated WITH the parent when that saves a front (nodes are cut into fronts of <= PMAX pivots) -- the same factor entries, one
-        // front and one dependency hop less on the boundary chain (a three-bus separator between two fat interfaces
-        // otherwise costs a full hand-off).  Moving the node's elimination to just before its parent is a valid
-        // reordering: everything in between belongs to other subtrees.
-        if (!getenv("GSE_NO_GAMMA_MERGE")) {
-            auto slots_of = [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (ang_slot[b] >= 0); return c; };
-            for (bool merged = true; merged;) {
-                merged = false;
-                const int nn_nodes = (int)nodes.size();
-                std::vector<int> node_of(nn, -1), pos_of(nn, -1);
-                { int q = 0; for (int i = 0; i < nn_nodes; ++i) for (int b : nodes[i]) { node_of[b] = i; pos_of[b] = q++; } }
-                // structure of every node (buses eliminated later that its front reaches), children before parents
-                std::vector<std::vector<int>> st(nn_nodes);
-                std::vector<int> parent(nn_nodes, -1), mark(nn, -1);
-                std::vector<std::vector<int>> kids(nn_nodes);
-                for (int i = 0; i < nn_nodes; ++i) {
-                    const int last = pos_of[nodes[i].back()];
-                    auto add = [&](int b) { if (pos_of[b] > last && mark[b] != i) { mark[b] = i; st[i].push_back(b); } };
-                    for (int b : nodes[i]) for (int e = g.xadj[b]; e < g.xadj[b + 1]; ++e) add(g.adj[e]);
-                    for (int c : kids[i]) for (int b : st[c]) add(b);
-                    if (st[i].empty()) continue;
-                    int first = st[i][0];
-                    for (int b : st[i]) if (pos_of[b] < pos_of[first]) first = b;
-                    parent[i] = node_of[first];
-                    kids[parent[i]].push_back(i);
-                }
-                for (int i = 0; i < nn_nodes && !merged; ++i) {
-                    const int q = parent[i];
-                    if (q < 0) continue;
-                    const int pi = slots_of(nodes[i]), pq = slots_of(nodes[q]);
-                    auto pieces = [&](int v) { return (v + PMAX - 1) / PMAX; };
-                    // (nodes are cut into fronts of <= PMAX pivots: the merge must save one; a node that does not fit
-                    // its parent's last front is only worth it when it is tiny -- otherwise every task of the parent's
-                    // fronts factors a taller pivot block: measured slower at PEGASE-9241/16)
-                    if (pieces(pi + pq) >= pieces(pi) + pieces(pq)) continue;
-                    if (pi + pq > PMAX && pi > 8) continue;
-                    if (st[i].size() != nodes[q].size() + st[q].size()) continue;     // would add fill
-                    std::vector<int> both = nodes[i];
-                    both.insert(both.end(), nodes[q].begin(), nodes[q].end());
-                    nodes[q] = std::move(both);
-                    nodes.erase(nodes.begin() + i);
-                    merged = true;
-                }
-            }
-        }
+        if (!getenv("GSE_NO_GAMMA_MERGE"))
+            amalgamate_nodes(nodes, nn, g.xadj, g.adj, nullptr,
+                             [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (ang_slot[b] >= 0); return c; }, PMAX);
         int rank = 0;
         for (auto& node : nodes) {
             std::vector<int> slots;
@@ -636,6 +645,15 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             g.sep_weight = opt.sep_weight;
             std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
             nd_recurse(g, all, std::max(1, opt.leaf_buses), nodes);
+            if (getenv("GSE_INTERIOR_MERGE")) {
+                // boundary variables coupled to each interior bus (they belong to the update structure of its front)
+                std::vector<std::vector<int>> ext(nib);
+                for (int u = 0; u < ni; ++u)
+                    for (int p = hp.ib_ptr[a][u]; p < hp.ib_ptr[a][u + 1]; ++p) ext[A.var_bus[u]].push_back(hp.ib_idx[a][p]);
+                for (auto& e : ext) { std::sort(e.begin(), e.end()); e.erase(std::unique(e.begin(), e.end()), e.end()); }
+                amalgamate_nodes(nodes, nib, g.xadj, g.adj, &ext,
+                                 [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (A.th_var[b] >= 0); return c; }, PMAX);
+            }
         }
     });
     sec(1);
