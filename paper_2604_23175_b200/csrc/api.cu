@@ -298,6 +298,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     if (const char* e = getenv("GSE_SEPW")) bo.sep_weight = atof(e);
     if (const char* e = getenv("GSE_GAMMA_SEPW")) bo.gamma_sep_weight = atof(e);
     if (const char* e = getenv("GSE_SPLIT_MIN")) { int v = atoi(e); if (v >= 1) bo.split_min_pivots = v; }
+    if (const char* e = getenv("GSE_SPLIT_TASKS")) { int v = atoi(e); if (v >= 1) bo.split_min_tasks = v; }
     if (const char* e = getenv("GSE_MAX_CTAS")) { int v = atoi(e); if (v >= 1) plan->max_ctas = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;

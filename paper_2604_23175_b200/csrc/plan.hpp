@@ -125,6 +125,7 @@ struct BuildOptions {
     // PEGASE-9241 shape (tools/gpu_sweep2.sh): the panel is bound by its serial 8x8 chain, not by its row count,
     // so the split only adds a hand-off (2.06 ms vs 2.03 ms per solve) -- off by default, kept for wide fronts.
     int split_min_pivots = 1 << 20;
+    int split_min_tasks = 0;   // ... and at least this many tile tasks (GSE_SPLIT_TASKS)
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;

@@ -1073,7 +1073,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         const int phase = f.kind <= 1 ? 1 : f.kind == 2 ? (sparse_gamma ? 5 : 2) : 3;
         // wide fronts: one panel task per row chunk (factor + solve, stored) and one update task per
         // tile (reads the stored panels) instead of tasks that each redo the pivot block
-        const bool split = f.p > 0 && f.nch >= 2 && f.p >= opt.split_min_pivots;
+        const bool split = f.p > 0 && f.nch >= 2 && f.p >= opt.split_min_pivots && f.nch * (f.nch + 1) / 2 >= opt.split_min_tasks;
         if (split) for (int ci = 0; ci < f.nch; ++ci) hp.fwd_levels[f.level].push_back({(int)fi, ci, ci, phase, 1});
         for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj, phase, split ? 2 : 0});
         hp.level_phase[f.level] = phase;
