@@ -1078,11 +1078,29 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         for (int ci = 0; ci < f.nch; ++ci) for (int cj = 0; cj <= ci; ++cj) hp.fwd_levels[f.level].push_back({(int)fi, ci, cj, phase, split ? 2 : 0});
         hp.level_phase[f.level] = phase;
     }
-    // within a level: panel and fused tasks (largest first), then the update tasks
+    // within a level: panel and fused tasks, then the update tasks.  Most critical first: when a level has more tasks
+    // than resident CTAs (the leaf levels), the ones left for the second wave should be the ones with the shortest way
+    // to the root -- remaining chain = estimated time from the front's start to the end of the factorisation along
+    // its ancestors (per front ~6 us of hand-off, gather and update plus 1 us per 8-pivot block of the panel).
+    // GSE_TASK_ORDER=size restores largest-first.
+    std::vector<double> remaining(hp.fronts.size(), 0.0);
+    {
+        std::vector<int> by_level(hp.fronts.size());
+        std::iota(by_level.begin(), by_level.end(), 0);
+        std::stable_sort(by_level.begin(), by_level.end(), [&](int a, int b) { return hp.fronts[a].level > hp.fronts[b].level; });
+        for (int fi : by_level) {
+            const Front& f = hp.fronts[fi];
+            const double cost = f.p > 0 ? 6.0 + (f.p + 7) / 8 : 3.0;
+            remaining[fi] = cost + (f.parent >= 0 ? remaining[f.parent] : 0.0);
+        }
+    }
+    const char* order_env = getenv("GSE_TASK_ORDER");
+    const bool by_size = order_env && !strcmp(order_env, "size");
     for (auto& lv : hp.fwd_levels)
         std::stable_sort(lv.begin(), lv.end(), [&](const Task& x, const Task& y) {
             if ((x.kind == 2) != (y.kind == 2)) return y.kind == 2;
             const Front& a = hp.fronts[x.front]; const Front& b = hp.fronts[y.front];
+            if (!by_size && remaining[x.front] != remaining[y.front]) return remaining[x.front] > remaining[y.front];
             return (int64_t)a.p * (a.p + a.u1) > (int64_t)b.p * (b.p + b.u1); });
     for (int lv = n_levels - 1; lv >= 0; --lv) {
         std::vector<int> fs; int phase = 4;
