@@ -1102,6 +1102,20 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             const Front& a = hp.fronts[x.front]; const Front& b = hp.fronts[y.front];
             if (!by_size && remaining[x.front] != remaining[y.front]) return remaining[x.front] > remaining[y.front];
             return (int64_t)a.p * (a.p + a.u1) > (int64_t)b.p * (b.p + b.u1); });
+    // back-substitution, top-down; within a level the fronts with the longest chain of fronts BELOW them first (the
+    // mirror of the forward order: what is left for a second wave should be what finishes the iteration soonest)
+    std::vector<double> below(hp.fronts.size(), 0.0);
+    {
+        std::vector<int> by_level(hp.fronts.size());
+        std::iota(by_level.begin(), by_level.end(), 0);
+        std::stable_sort(by_level.begin(), by_level.end(), [&](int a, int b) { return hp.fronts[a].level < hp.fronts[b].level; });
+        for (int fi : by_level) {
+            const Front& f = hp.fronts[fi];
+            double c = 0.0;
+            for (int ch : f.children) c = std::max(c, below[ch]);
+            below[fi] = c + (f.p > 0 ? 3.0 + f.p / 40.0 : 0.0);
+        }
+    }
     for (int lv = n_levels - 1; lv >= 0; --lv) {
         std::vector<int> fs; int phase = 4;
         for (size_t fi = 0; fi < hp.fronts.size(); ++fi) {
@@ -1110,6 +1124,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             if (f.area >= 0 && !hp.owned[f.area]) continue;
             fs.push_back((int)fi); if (f.kind == 3) phase = 3;
         }
+        if (!by_size) std::stable_sort(fs.begin(), fs.end(), [&](int a, int b) { return below[a] > below[b]; });
         if (!fs.empty()) { hp.bwd_levels.push_back(fs); hp.bwd_phase.push_back(phase); }
     }
 
