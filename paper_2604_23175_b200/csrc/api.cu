@@ -280,6 +280,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     // 1.51 ms, PEGASE-2869: 0.81 vs 0.85 ms per solve); throughput-bound plans with 48 (the ~100k-bus grid:
     // 5.60 vs 7.54 ms).  gse_options.tile_rows / GSE_TILE_ROWS override.
     bo.tile_rows = d->n_bus <= 30000 ? 32 : 48;
+    bo.interior_merge = d->n_bus <= 30000 ? 0.0 : 1.0;       // relaxed amalgamation of the interiors: throughput-bound plans only (plan.hpp)
     if (opt) {
         bo.dense = opt->backend_dense != 0;
         if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
@@ -299,6 +300,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     if (const char* e = getenv("GSE_GAMMA_SEPW")) bo.gamma_sep_weight = atof(e);
     if (const char* e = getenv("GSE_SPLIT_MIN")) { int v = atoi(e); if (v >= 1) bo.split_min_pivots = v; }
     if (const char* e = getenv("GSE_SPLIT_TASKS")) { int v = atoi(e); if (v >= 1) bo.split_min_tasks = v; }
+    if (const char* e = getenv("GSE_INTERIOR_MERGE")) bo.interior_merge = atof(e);
+    if (const char* e = getenv("GSE_GAMMA_MERGE")) bo.gamma_merge = atof(e);
     if (const char* e = getenv("GSE_MAX_CTAS")) { int v = atoi(e); if (v >= 1) plan->max_ctas = v; }
     plan->coordinator = bo.rank == 0;
     HostProgram& hp = plan->hp;

@@ -126,6 +126,12 @@ struct BuildOptions {
     // so the split only adds a hand-off (2.06 ms vs 2.03 ms per solve) -- off by default, kept for wide fronts.
     int split_min_pivots = 1 << 20;
     int split_min_tasks = 0;   // ... and at least this many tile tasks (GSE_SPLIT_TASKS)
+    // relaxed amalgamation of the area interiors' nested-dissection nodes: a node joins its parent's front when both fit
+    // one front and the node's columns grow by at most this fraction of explicit zeros (0: off).  Throughput-bound plans
+    // (the ~100k-bus grid) gain 8-11 % with 1.0 (fewer, fuller fronts: 6770 -> 4730); latency-bound ones lose (more
+    // pivots per front on the chains), measured on every BASELINE shape (profiles/r02_sweep_interior_merge.txt).
+    double interior_merge = 0.0;
+    double gamma_merge = 0.0;  // the same for the boundary tree on top of its fill-free amalgamation (0: fill-free only)
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
     int rank = 0, world = 1;
     std::vector<int> area_rank;

@@ -332,7 +332,7 @@ void build_acc_items(HostProgram& hp) {
 // that are never eliminated here (an area's boundary variables) and belong to every structure that reaches them.
 template <class SlotsOf>
 static void amalgamate_nodes(std::vector<std::vector<int>>& nodes, int nn, const std::vector<int>& xadj, const std::vector<int>& adj,
-                             const std::vector<std::vector<int>>* ext, SlotsOf slots_of, int pmax) {
+                             const std::vector<std::vector<int>>* ext, SlotsOf slots_of, int pmax, double fill_tol = 0.0) {
     int n_ext = 0;
     if (ext) for (auto& e : *ext) for (int x : e) n_ext = std::max(n_ext, x + 1);
     for (bool merged = true; merged;) {
@@ -365,7 +365,10 @@ static void amalgamate_nodes(std::vector<std::vector<int>>& nodes, int nn, const
             const int pi = slots_of(nodes[i]), pq = slots_of(nodes[q]);
             if (pieces(pi + pq) >= pieces(pi) + pieces(pq)) continue;                 // must save a front
             if (pi + pq > pmax && pi > 8) continue;
-            if (st[i].size() + se[i].size() != nodes[q].size() + st[q].size() + se[q].size()) continue;     // would add fill
+            // (fill_tol > 0: relaxed amalgamation -- the node's columns may grow by that fraction of explicit zeros,
+            // only into a single front)
+            const size_t have = st[i].size() + se[i].size(), want = nodes[q].size() + st[q].size() + se[q].size();
+            if (have != want && !(fill_tol > 0.0 && pi + pq <= pmax && (double)(want - have) <= fill_tol * (double)want)) continue;
             std::vector<int> both = nodes[i];
             both.insert(both.end(), nodes[q].begin(), nodes[q].end());
             nodes[q] = std::move(both);
@@ -461,7 +464,8 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
         nd_recurse(g, all, std::max(1, opt.gamma_leaf_buses), nodes);
         if (!getenv("GSE_NO_GAMMA_MERGE"))
             amalgamate_nodes(nodes, nn, g.xadj, g.adj, nullptr,
-                             [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (ang_slot[b] >= 0); return c; }, PMAX);
+                             [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (ang_slot[b] >= 0); return c; }, PMAX,
+                             opt.gamma_merge);
         int rank = 0;
         for (auto& node : nodes) {
             std::vector<int> slots;
@@ -645,14 +649,15 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
             g.sep_weight = opt.sep_weight;
             std::vector<int> all(nib); std::iota(all.begin(), all.end(), 0);
             nd_recurse(g, all, std::max(1, opt.leaf_buses), nodes);
-            if (getenv("GSE_INTERIOR_MERGE")) {
+            if (opt.interior_merge > 0.0) {
                 // boundary variables coupled to each interior bus (they belong to the update structure of its front)
                 std::vector<std::vector<int>> ext(nib);
                 for (int u = 0; u < ni; ++u)
                     for (int p = hp.ib_ptr[a][u]; p < hp.ib_ptr[a][u + 1]; ++p) ext[A.var_bus[u]].push_back(hp.ib_idx[a][p]);
                 for (auto& e : ext) { std::sort(e.begin(), e.end()); e.erase(std::unique(e.begin(), e.end()), e.end()); }
                 amalgamate_nodes(nodes, nib, g.xadj, g.adj, &ext,
-                                 [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (A.th_var[b] >= 0); return c; }, PMAX);
+                                 [&](const std::vector<int>& node) { int c = 0; for (int b : node) c += 1 + (A.th_var[b] >= 0); return c; }, PMAX,
+                                 opt.interior_merge);
             }
         }
     });
