@@ -281,6 +281,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     // 5.60 vs 7.54 ms).  gse_options.tile_rows / GSE_TILE_ROWS override.
     bo.tile_rows = d->n_bus <= 30000 ? 32 : 48;
     bo.interior_merge = d->n_bus <= 30000 ? 0.0 : 1.0;       // relaxed amalgamation of the interiors: throughput-bound plans only (plan.hpp)
+    if (d->n_bus > 30000) bo.leaf_buses = 32;                 // ... on finer leaves: the merges then fill the fronts up to the pivot cap
+                                                              // (5.39 -> 5.29 ms at ~100k / 128, tools/gpu_sweep5.sh)
     if (opt) {
         bo.dense = opt->backend_dense != 0;
         if (opt->leaf_buses > 0) bo.leaf_buses = opt->leaf_buses;
