@@ -188,6 +188,8 @@ void* hostsim_create(const gse_problem_desc* d, int dense, int leaf, int pmax, i
     if (const char* e = getenv("GSE_GAMMA_SEPW")) bo.gamma_sep_weight = atof(e);
     if (const char* e = getenv("GSE_GAMMA_LEAF")) bo.gamma_leaf_buses = atoi(e);
     if (const char* e = getenv("GSE_LEAF_BUSES")) bo.leaf_buses = atoi(e);
+    if (const char* e = getenv("GSE_INTERIOR_MERGE")) bo.interior_merge = atof(e);
+    if (const char* e = getenv("GSE_GAMMA_MERGE")) bo.gamma_merge = atof(e);
     if (area_rank) bo.area_rank.assign(area_rank, area_rank + d->n_areas);
     std::string e = build_host_program(*d, bo, s->hp);
     if (!e.empty()) { snprintf(msg, msglen, "%s", e.c_str()); delete s; return nullptr; }

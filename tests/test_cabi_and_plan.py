@@ -118,3 +118,28 @@ def test_plan_build_does_not_depend_on_the_host_thread_count(monkeypatch):
         assert st == outs[0][0] and it == outs[0][3]
         assert np.array_equal(va, outs[0][1]) and np.array_equal(vm, outs[0][2])
         assert np.array_equal(deltas, outs[0][4]) and np.array_equal(vals, outs[0][5])
+
+
+@pytest.mark.parametrize("name", ["ieee118_k3", "rand300_k3_maskpf", "pegase2869_k8"])
+def test_amalgamated_trees_solve_the_same_system(name, monkeypatch):
+    """The plan-time tree shaping of round 2 -- relaxed amalgamation of the area interiors (the default of plans above
+    30k buses), relaxed boundary amalgamation, fine leaves, 8-aligned supernode pieces -- only changes WHICH front
+    eliminates a variable: the host interpreter of the device program must reach the reference's iteration count and
+    state with every variant, and the merges must really reduce the number of fronts."""
+    from hostsim import HostSim
+    net, ms, part, g = build_case(name)
+    bord, maps = G.build_variable_maps(net, part)
+    base = HostSim(net, ms, part, bord, maps, leaf=8).stats()["fronts"]
+    for env in ({"GSE_INTERIOR_MERGE": "1.0"}, {"GSE_INTERIOR_MERGE": "0.3", "GSE_GAMMA_MERGE": "1.0"},
+                {"GSE_INTERIOR_MERGE": "1.0", "GSE_NO_GAMMA_MERGE": "1"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sim = HostSim(net, ms, part, bord, maps, leaf=8, pmax=32 if name == "ieee118_k3" else 0)
+        tol = 1e-6
+        va, vm, it, conv, deltas = sim.solve(tol=tol)
+        assert it == int(g["iterations"]) and conv == bool(g["converged"]), env
+        assert max(np.max(np.abs(va - g["va"])), np.max(np.abs(vm - g["vm"]))) < 1e-9, env
+        if name != "ieee118_k3":
+            assert sim.stats()["fronts"] < base, env
+        for k in env:
+            monkeypatch.delenv(k)
