@@ -149,6 +149,7 @@ class MultiAreaEstimator:
         self._state = torch.empty((2, net.n_bus), dtype=torch.float64, device=self.device)
         self._flat_dev = torch.from_numpy(self._flat).to(self.device)      # the flat start is a constant of the plan
         torch.cuda.current_stream(self.device).synchronize()              # (the plan's stream reads it from now on)
+        self._persistent = bool(self.plan.stats()["persistent"])
         self.setup_s = time.perf_counter() - t0
 
     # -- inputs ----------------------------------------------------------------------
@@ -216,7 +217,8 @@ class MultiAreaEstimator:
                 iterations, converged, j = rep.iterations, bool(rep.converged), rep.objective
                 self.last_deltas = [rep.delta_inf[i] for i in range(iterations)]
                 self.last_loop_s, self.last_gpu_s = rep.loop_s, rep.gpu_s
-                self.launches_per_solve = int(self.plan.stats()["launches_last"])
+                # (one launch per solve on the persistent path: no need to ask the plan after every solve)
+                self.launches_per_solve = 1 if (self._persistent and not cfg.profile_phases) else int(self.plan.stats()["launches_last"])
                 # persistent path: device globaltimer stamps per phase; profile_phases: CUDA events
                 # between the phases of the level-launch path
                 for p, v in zip(PHASES, rep.phase_s):
