@@ -440,4 +440,10 @@ class DistributedEstimator:
         return np.concatenate(idx).astype(np.int64) if idx else np.zeros(0, dtype=np.int64)
 
     def close(self):
+        # peer-linked plans map each other's buffers (CUDA IPC): nobody frees before everybody has stopped using them
+        if self.linked and self.world > 1:
+            try:
+                self.dist.barrier(group=self.group)
+            except Exception:       # (a rank that failed earlier must still be able to clean up)
+                pass
         self.engine.close()
