@@ -13,6 +13,9 @@ namespace gse {
 #ifndef GSE_PANEL_QUIET
 #define GSE_PANEL_QUIET 1
 #endif
+#ifndef GSE_GATHER_BY_CHILD
+#define GSE_GATHER_BY_CHILD 1
+#endif
 #ifndef GSE_UPDATE_NARROW
 #define GSE_UPDATE_NARROW 1
 #endif
@@ -125,6 +128,68 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
     }
 }
 
+// The LAST child of a batch -- by construction the one expected to finish last, so usually gathered alone, right after
+// the hand-off -- is walked by ITS rows instead of by the panel's: a child row holds its entries contiguously, so a
+// warp reads them coalesced (the panel-driven gather above picks them column by column through the inverse map) and
+// only rows the child really has are visited.  Every panel / tile entry still receives this child's contribution
+// exactly once and after the earlier children's (a CTA barrier separates them): the same sums, bit for bit.
+// fwd: FrontScratch::fwd of this child; eP / bI,eI / bJ,eJ: its row ranges (ChildRec).
+template <int G>
+__device__ __forceinline__ void gather_last_child(const GatherArgs& a, const ChildRec& cr, const int* __restrict__ fwd, int ri) {
+    const int p = a.p, ld = a.ld, ldt = a.ldt, rp = a.rp, warp = a.warp, lane = a.lane, nwarps = a.nwarps;
+    const double* Uc = a.ubuf + cr.u_off;
+    const int eP = p ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = a.diag ? 0 : cr.eJ - cr.bJ;
+    // panel: child rows that map into [pivots | chunk I | chunk J], child columns that map into the pivots
+    if (eP > 0) {
+        const int Rc = eP + nI + nJ;
+        for (int rb = warp; rb < Rc; rb += G * nwarps) {
+            double v[G][2];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int tt = rb + g * nwarps;
+                const int t = tt < eP ? tt : tt < eP + nI ? cr.bI + tt - eP : cr.bJ + tt - eP - nI;      // child row
+                const double* src = Uc + (size_t)t * (t + 1) / 2;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) { const int j = lane + 32 * h; v[g][h] = (tt < Rc && j < eP && j <= t) ? ldc(src + j) : 0.0; }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int tt = rb + g * nwarps;
+                if (tt >= Rc) continue;
+                const int t = tt < eP ? tt : tt < eP + nI ? cr.bI + tt - eP : cr.bJ + tt - eP - nI;
+                const int R = tt < eP ? fwd[tt] : tt < eP + nI ? rp + fwd[tt] : rp + ri + fwd[tt];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) { const int j = lane + 32 * h; if (j < eP && j <= t) a.pan[R * ld + fwd[j]] += v[g][h]; }
+            }
+        }
+    }
+    // tile: child rows in chunk I x child columns in chunk J (the lower triangle of the child's matrix)
+    if (!a.direct && nI > 0) {
+        const int bC = a.diag ? cr.bI : cr.bJ, nC = a.diag ? nI : nJ;       // child columns [bC, bC + nC) and where their map starts in fwd
+        const int fC = a.diag ? eP : eP + nI;
+        for (int cb = 0; cb < nC; cb += 64) {
+            for (int rb = warp; rb < nI; rb += G * nwarps) {
+                double v[G][2];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int ti = rb + g * nwarps, t = cr.bI + ti;
+                    const double* src = Uc + (size_t)t * (t + 1) / 2 + bC;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) { const int jj = cb + lane + 32 * h; v[g][h] = (ti < nI && jj < nC && bC + jj <= t) ? ldc(src + jj) : 0.0; }
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int ti = rb + g * nwarps, t = cr.bI + ti;
+                    if (ti >= nI) continue;
+                    const int R = fwd[eP + ti];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) { const int jj = cb + lane + 32 * h; if (jj < nC && bC + jj <= t) a.tile[R * ldt + fwd[fC + jj]] += v[g][h]; }
+                }
+            }
+        }
+    }
+}
+
 constexpr int kChildBatch = 32;
 
 // Diagonal 8x8 blocks of the pivot triangle are kept RIGHT-looking: as soon as a block column
@@ -149,6 +214,8 @@ struct __align__(16) FrontScratch {
     double rinv[64];           // reciprocal pivots of the whole front (stored for the backward pass)
     double colbuf[2][16];      // two columns of the 8x8 pivot block being eliminated (double-buffered)
     int nready;                // children of the current gather batch that are complete
+    int fwd[kInvRows];         // LAST child of the batch, child -> parent: [0, eP) pivot row / column, then the tile rows of its
+                               // rows in chunk I, then the tile columns of its rows in chunk J (gather_last_child)
 };
 
 __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec* __restrict__ task) {
@@ -302,10 +369,11 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
             const ChildRec& cr = crec[cbase + c];
             const int32_t* rel = ft.rel + cr.rel_off;
             const int eP = pp ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = diag ? 0 : cr.eJ - cr.bJ;
+            const bool last = c == nb - 1;
             for (int t = tid; t < eP + nI + nJ; t += nth) {
-                if (t < eP) s_inv[c][rel[t]] = t;
-                else if (t < eP + nI) { const int i = cr.bI + t - eP; s_inv[c][rp + rel[i] - p - i0] = i; }
-                else { const int i = cr.bJ + t - eP - nI; s_inv[c][rp + round8(ni) + rel[i] - p - j0] = i; }
+                if (t < eP) { const int r = rel[t]; s_inv[c][r] = t; if (last) S.fwd[t] = r; }
+                else if (t < eP + nI) { const int i = cr.bI + t - eP, r = rel[i] - p - i0; s_inv[c][rp + r] = i; if (last) S.fwd[t] = r; }
+                else { const int i = cr.bJ + t - eP - nI, r = rel[i] - p - j0; s_inv[c][rp + round8(ni) + r] = i; if (last) S.fwd[t] = r; }
             }
         }
         __syncthreads();
@@ -317,6 +385,12 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
             const int ready = wait.ready_children(hdr, ft.crecs + hdr.child_off + cb0, c, nb, &S.nready);
             GatherArgs ga{pan, tile, &s_inv[c][0], ubuf, pp, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
             const ChildRec* cb = crec + cbase + c;
+            if (GSE_GATHER_BY_CHILD && ready == 1 && c == nb - 1) {
+                __syncthreads();               // (the earlier children's sums are in place)
+                gather_last_child<8>(ga, *cb, S.fwd, ri);
+                c += ready;
+                continue;
+            }
             switch (ready) {
                 case 1: gather_batch<1, 8>(ga, cb); break;
                 case 2: gather_batch<2, 4>(ga, cb); break;
