@@ -546,7 +546,9 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plan->device);
             std::vector<int> panels(hp.fwd_levels.size() + 1, 0), total(hp.fwd_levels.size() + 1, 0);
             for (int t = 0; t < n_solve_tasks; ++t) { total[trecs[t].level]++; panels[trecs[t].level] += trecs[t].p > 0; }
-            bool on = sp.items_per_it >= 4 * 2 * sms;           // small plans: a grid's worth of pulls spans iterations
+            int min_items = 4 * 2 * sms;                        // small plans: a grid's worth of pulls spans iterations
+            if (const char* e = getenv("GSE_CHAIN_MIN_ITEMS")) min_items = atoi(e);
+            bool on = sp.items_per_it >= min_items;
             if (const char* e = getenv("GSE_CHAIN_SM")) on = on && atoi(e) != 0;
             int mode = 1;                                       // 1: the boundary suffix (measured best), 2: every sparse run (the top interior levels too: 0.5 % slower)
             if (const char* e = getenv("GSE_CHAIN_MODE")) mode = atoi(e);
