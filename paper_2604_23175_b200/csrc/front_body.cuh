@@ -135,7 +135,7 @@ __device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec
 // exactly once and after the earlier children's (a CTA barrier separates them): the same sums, bit for bit.
 // fwd: FrontScratch::fwd of this child; eP / bI,eI / bJ,eJ: its row ranges (ChildRec).
 template <int G>
-__device__ __forceinline__ void gather_last_child(const GatherArgs& a, const ChildRec& cr, const int* __restrict__ fwd, int ri) {
+__device__ __forceinline__ void gather_last_child(const GatherArgs& a, const ChildRec& cr, const int* __restrict__ fwd, int ri, long long* tb = nullptr) {
     const int p = a.p, ld = a.ld, ldt = a.ldt, rp = a.rp, warp = a.warp, lane = a.lane, nwarps = a.nwarps;
     const double* Uc = a.ubuf + cr.u_off;
     const int eP = p ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = a.diag ? 0 : cr.eJ - cr.bJ;
@@ -152,17 +152,28 @@ __device__ __forceinline__ void gather_last_child(const GatherArgs& a, const Chi
 #pragma unroll
                 for (int h = 0; h < 2; ++h) { const int j = lane + 32 * h; v[g][h] = (tt < Rc && j < eP && j <= t) ? ldc(src + j) : 0.0; }
             }
+            // (the sixteen read-modify-writes of a lane hit distinct panel entries, but the compiler cannot know: written
+            // one after the other they form a chain of shared-memory round trips.  All reads first, then all writes.)
+            int off[G][2];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const int tt = rb + g * nwarps;
-                if (tt >= Rc) continue;
                 const int t = tt < eP ? tt : tt < eP + nI ? cr.bI + tt - eP : cr.bJ + tt - eP - nI;
-                const int R = tt < eP ? fwd[tt] : tt < eP + nI ? rp + fwd[tt] : rp + ri + fwd[tt];
+                const int R = tt >= Rc ? 0 : tt < eP ? fwd[tt] : tt < eP + nI ? rp + fwd[tt] : rp + ri + fwd[tt];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) { const int j = lane + 32 * h; if (j < eP && j <= t) a.pan[R * ld + fwd[j]] += v[g][h]; }
+                for (int h = 0; h < 2; ++h) { const int j = lane + 32 * h; off[g][h] = (tt < Rc && j < eP && j <= t) ? R * ld + fwd[j] : -1; }
             }
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) if (off[g][h] >= 0) v[g][h] += a.pan[off[g][h]];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) if (off[g][h] >= 0) a.pan[off[g][h]] = v[g][h];
         }
     }
+    if (tb && threadIdx.x == 0) tb[17] = (long long)gtimer();
     // tile: child rows in chunk I x child columns in chunk J (the lower triangle of the child's matrix)
     if (!a.direct && nI > 0) {
         const int bC = a.diag ? cr.bI : cr.bJ, nC = a.diag ? nI : nJ;       // child columns [bC, bC + nC) and where their map starts in fwd
@@ -177,14 +188,22 @@ __device__ __forceinline__ void gather_last_child(const GatherArgs& a, const Chi
 #pragma unroll
                     for (int h = 0; h < 2; ++h) { const int jj = cb + lane + 32 * h; v[g][h] = (ti < nI && jj < nC && bC + jj <= t) ? ldc(src + jj) : 0.0; }
                 }
+                int off[G][2];
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const int ti = rb + g * nwarps, t = cr.bI + ti;
-                    if (ti >= nI) continue;
-                    const int R = fwd[eP + ti];
+                    const int R = ti < nI ? fwd[eP + ti] : 0;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) { const int jj = cb + lane + 32 * h; if (jj < nC && bC + jj <= t) a.tile[R * ldt + fwd[fC + jj]] += v[g][h]; }
+                    for (int h = 0; h < 2; ++h) { const int jj = cb + lane + 32 * h; off[g][h] = (ti < nI && jj < nC && bC + jj <= t) ? R * ldt + fwd[fC + jj] : -1; }
                 }
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) if (off[g][h] >= 0) v[g][h] += a.tile[off[g][h]];
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) if (off[g][h] >= 0) a.tile[off[g][h]] = v[g][h];
             }
         }
     }
@@ -387,7 +406,9 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
             const ChildRec* cb = crec + cbase + c;
             if (GSE_GATHER_BY_CHILD && ready == 1 && c == nb - 1) {
                 __syncthreads();               // (the earlier children's sums are in place)
-                gather_last_child<8>(ga, *cb, S.fwd, ri);
+                if (tb && tid == 0) tb[16] = (long long)gtimer();
+                gather_last_child<8>(ga, *cb, S.fwd, ri, tb);
+                if (tb && tid == 0) tb[18] = (long long)gtimer();
                 c += ready;
                 continue;
             }

@@ -19,6 +19,10 @@
 // result is bit-identical to the level-launch path whatever the CTA interleaving.
 #include "front_body.cuh"
 
+#ifndef GSE_POLL_NS
+#define GSE_POLL_NS 40
+#endif
+
 namespace gse {
 
 namespace {
@@ -59,7 +63,7 @@ __device__ __forceinline__ void wait_ge(const unsigned* p, unsigned target, bool
     unsigned long long t0 = 0;
     unsigned v;
     while ((v = (sys ? ld_acquire_sys(p) : ld_acquire(p))) < target) {
-        __nanosleep(40);
+        __nanosleep(GSE_POLL_NS);
         // watchdog: a dependency that never completes would hang the device; after ~10 s of waiting
         // the kernel aborts instead (the launch then fails with an error the host reports)
         if ((++polls & 0xffffu) == 0) {

@@ -129,10 +129,11 @@ for it in range(rep.iterations):
             for i in range(len(bf)):
                 f = int((bf[i, 6] >> 8) & 0xffffff)
                 rdy = max(bf[i, 1], bf[i, 2], bf[i, 0])
-                rows.append((f, int((bf[i, 6] >> 32) & 0xffff), int((bf[i, 6] >> 48) & 0xffff), int(bf[i, 4] & 0xffff), rdy - s0, bf[i, 3] - s0, bf[i, 8:16]))
+                rows.append((f, int((bf[i, 6] >> 32) & 0xffff), int((bf[i, 6] >> 48) & 0xffff), int(bf[i, 4] & 0xffff), rdy - s0, bf[i, 3] - s0, bf[i, 8:16], bf[i, 24:27]))
             print(f"   tasks of front {want} (ci cj sm | ready end exec | gather panel update | tasks of other fronts busy on the same SM meanwhile):")
-            for f, ci, cj, sm, rdy, end, st in rows:
+            for f, ci, cj, sm, rdy, end, st, sub in rows:
                 if f != want: continue
-                mates = [(g, a, b) for g, a, b, sm2, r2, e2, _ in rows if sm2 == sm and not (g == f and a == ci and b == cj) and r2 < end and e2 > rdy]
+                mates = [(g, a, b) for g, a, b, sm2, r2, e2, _, _ in rows if sm2 == sm and not (g == f and a == ci and b == cj) and r2 < end and e2 > rdy]
                 cw = st[7]
-                print(f"     {ci:2d},{cj:2d} sm {sm:3d} | {rdy/1e3:7.1f} {end/1e3:7.1f} {(end-rdy)/1e3:5.1f} | {(st[3]-max(cw, rdy+s0))/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} {(st[5]-st[4])/1e3:5.1f} | {mates[:3]}")
+                print(f"     {ci:2d},{cj:2d} sm {sm:3d} | {rdy/1e3:7.1f} {end/1e3:7.1f} {(end-rdy)/1e3:5.1f} | {(st[3]-max(cw, rdy+s0))/1e3:5.1f} {(st[4]-st[3])/1e3:5.1f} {(st[5]-st[4])/1e3:5.1f} | {mates[:3]}"
+                      + (f"  last child: ready->start {(sub[0]-(rdy+s0))/1e3:4.1f} panel {(sub[1]-sub[0])/1e3:4.1f} tile {(sub[2]-sub[1])/1e3:4.1f} ->gather end {(st[3]-sub[2])/1e3:4.1f}" if sub[0] else ""))
