@@ -254,6 +254,7 @@ struct NoWait {
     __device__ __forceinline__ void children(const TaskRec&, const ChildRec*) const {}
     __device__ __forceinline__ int ready_children(const TaskRec&, const ChildRec*, int c, int nb, int*) const { return nb - c; }
     __device__ __forceinline__ void panels(const TaskRec&) const {}
+    __device__ __forceinline__ void tile_done(const TaskRec&) const {}
 };
 
 // One front task; S.hdr is loaded and visible to the whole CTA.  tb: optional 8 clock stamps.
@@ -597,22 +598,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
 #undef GSE_PC
         if (tb && tid == 0) for (int k = 0; k < 7; ++k) tb[8 + k] = pc[k];
     }
-    // ---- factor panel to global (diagonal tasks own their row chunk): one TMA bulk store per row,
-    // issued as soon as the panel is final so that the copies overlap the trailing update
     const bool bulk_panel = HAS_PIVOTS && pp && diag && (p & 1) == 0;
-    if (bulk_panel) {
-        fence_proxy_async();            // the rows were written with ordinary shared-memory stores
-        __syncthreads();
-        double* L = lbuf + hdr.l_off;
-        const int n0 = ci == 0 ? p : 0;                       // pivot rows (first chunk only), then the rows of chunk I
-        if (tid < n0 + ni) {
-            const int r = tid < n0 ? tid : tid - n0;
-            const double* src = tid < n0 ? pan + (size_t)r * ld : pan + (size_t)(rp + r) * ld;
-            double* dst = tid < n0 ? L + (size_t)r * p : L + (size_t)(p + i0 + r) * p;
-            tma_store_1d(dst, src, (unsigned)(p * sizeof(double)));
-            tma_store_commit();
-        }
-    }
     GSE_TICK(4);
 
     // ---- update tasks: the front's finished panels come back from the factor storage -----------
@@ -708,9 +694,27 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     }
     GSE_TICK(5);
     {
-        // ---- factor panel to global (diagonal tasks own their row chunk) ----------------------
+        // ---- factor panel to global (diagonal tasks own their row chunk): one TMA bulk store per row.  Nothing ahead of
+        // this front in the forward pass reads the factor -- only its own back-substitution does -- while the parent waits
+        // for the update matrix: a fused task therefore reports its tile FIRST (wait.tile_done: the dataflow kernel's
+        // hand-off to the parent) and stores its slice of the factor afterwards.  Starting the ~90 bulk stores of a
+        // first-chunk task costs ~1 us, which used to sit on the critical path of every level: the diagonal tasks were
+        // the last of their front to finish.
         if (HAS_PIVOTS && pp && diag) {
+            if (kind == 0) wait.tile_done(hdr);
             double* L = lbuf + hdr.l_off;
+            if (bulk_panel) {
+                fence_proxy_async();            // the rows were written with ordinary shared-memory stores
+                __syncthreads();
+                const int n0 = ci == 0 ? p : 0;                       // pivot rows (first chunk only), then the rows of chunk I
+                if (tid < n0 + ni) {
+                    const int r = tid < n0 ? tid : tid - n0;
+                    const double* src = tid < n0 ? pan + (size_t)r * ld : pan + (size_t)(rp + r) * ld;
+                    double* dst = tid < n0 ? L + (size_t)r * p : L + (size_t)(p + i0 + r) * p;
+                    tma_store_1d(dst, src, (unsigned)(p * sizeof(double)));
+                    tma_store_commit();
+                }
+            }
             if (ci == 0 && tid < p) dinv[hdr.dinv_off + tid] = s_rinv[tid];
             if (bulk_panel) {
                 tma_store_wait_all();            // (threads without a pending group return at once)

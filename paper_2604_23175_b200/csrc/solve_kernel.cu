@@ -101,6 +101,7 @@ struct SpinWait {
     int n_fronts, front0;
     bool sys;                // peer-linked solve: child counters may be bumped by other GPUs
     unsigned gamma_need;     // non-coordinator ranks: pieces of delta_x_Gamma to wait for (0: none)
+    bool early_tile = false; // latency-bound plans: fused diagonal tasks report their tile before they store the factor
     // early splits of the back-substitution (front_body.cuh): later splits wait for front dep2; split 0 for the others
     static constexpr bool kEarlySplits = true;
     __device__ __forceinline__ void ancestor(const BwdTask& tk) const {
@@ -135,6 +136,17 @@ struct SpinWait {
         if (!(hdr.flags & 2)) return;
         if (threadIdx.x == 0) { wait_ge(ctr + CTR_ACC, acc_target); if (tr) tr[1] = globaltimer(); }
         __syncthreads();
+    }
+    // a fused diagonal task has stored its tile of the update matrix: the parent may go on while the task stores its
+    // slice of the factor (counted again, under pdone, when the task ends)
+    __device__ __forceinline__ void tile_done(const TaskRec& hdr) const {
+        if (!early_tile) return;      // (throughput-bound plans: one hand-off per task -- a second fence costs more CTA time than the parent gains)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            fence_release();
+            atomicAdd(const_cast<unsigned*>(ctr) + front0 + hdr.front, 1u);
+            if (tr) tr[30] = globaltimer();
+        }
     }
     __device__ __forceinline__ void panels(const TaskRec& hdr) const {
         if (threadIdx.x == 0) {
@@ -301,7 +313,7 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
                 tr[6] = (unsigned long long)S.hdr.kind | ((unsigned long long)S.hdr.front << 8) | ((unsigned long long)S.hdr.ci << 32) | ((unsigned long long)S.hdr.cj << 48);
                 tr[7] = (unsigned long long)S.hdr.p | ((unsigned long long)S.hdr.u1 << 16) | ((unsigned long long)S.hdr.nchild << 32) | ((unsigned long long)S.hdr.phase << 48);
             }
-            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr, sp.n_fronts, sp.front0, linked, 0u};
+            const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr, sp.n_fronts, sp.front0, linked, 0u, fused_update};
             if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
             else front_task_body<0>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
             __syncthreads();
@@ -316,7 +328,8 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
                 fence_release();
                 const int kind = S.hdr.p ? S.hdr.kind : 0;
                 if (kind != 2 && S.hdr.p && S.hdr.ci == S.hdr.cj) atomicAdd(pdone + S.hdr.front, 1u);
-                if (kind != 1) atomicAdd(fdone + S.hdr.front, 1u);
+                const bool reported = fused_update && S.hdr.p && kind == 0 && S.hdr.ci == S.hdr.cj;     // (SpinWait::tile_done, before the factor stores)
+                if (kind != 1 && !reported) atomicAdd(fdone + S.hdr.front, 1u);
                 atomicAdd(ctr + CTR_FWD, 1u);
                 GSE_STAMP(it, 1 + S.hdr.phase);
             }
