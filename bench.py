@@ -322,7 +322,8 @@ def run_gpu(args):
 
     t0 = time.perf_counter()
     if world > 1:
-        est = DistributedEstimator(net, ms, part, device=local)
+        # (GSE_BENCH_EXCHANGE=collective keeps the ranks on the level-launch path with torch.distributed collectives)
+        est = DistributedEstimator(net, ms, part, device=local, exchange=os.environ.get("GSE_BENCH_EXCHANGE", "auto"))
     else:
         est = G.MultiAreaEstimator(net, ms, part, device=local)
     plan_s = time.perf_counter() - t0

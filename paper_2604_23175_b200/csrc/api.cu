@@ -294,6 +294,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         if (opt->area_rank) bo.area_rank.assign(opt->area_rank, opt->area_rank + d->n_areas);
     }
     if (const char* e = getenv("GSE_TILE_ROWS")) { int v = atoi(e); if (v >= 8 && v <= kMaxTile) bo.tile_rows = v / 8 * 8; }
+    if (const char* e = getenv("GSE_GAMMA_TILE_ROWS")) { int v = atoi(e); if (v >= 8 && v <= kMaxTile) bo.gamma_tile_rows = v / 8 * 8; }
     if (const char* e = getenv("GSE_BOUNDARY")) { int v = atoi(e); if (v >= 0 && v <= 2) bo.boundary_mode = v; }
     if (const char* e = getenv("GSE_GAMMA_LEAF")) { int v = atoi(e); if (v >= 1) bo.gamma_leaf_buses = v; }
     if (const char* e = getenv("GSE_MAX_PIVOTS")) { int v = atoi(e); if (v == 32 || v == 64) bo.max_pivots = v; }

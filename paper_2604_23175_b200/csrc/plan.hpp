@@ -133,6 +133,7 @@ struct BuildOptions {
     double interior_merge = 0.0;
     double gamma_merge = 0.0;  // the same for the boundary tree on top of its fill-free amalgamation (0: fill-free only)
     int tile_rows = 48;   // update-row chunk (task tile) size (48: best measured on PEGASE-9241 shape)
+    int gamma_tile_rows = 0;   // the same for the fronts of the boundary tree (0: tile_rows); GSE_GAMMA_TILE_ROWS
     int rank = 0, world = 1;
     std::vector<int> area_rank;
     // generic matrix plan (gse_matrix_plan_create): one area whose G_ii / G_ib patterns come from the

@@ -934,7 +934,7 @@ std::string build_host_program(const gse_problem_desc& d, const BuildOptions& op
                 f.u1 = (int)st.size() + 1;
                 for (int r : st) f.rows.push_back(hp.gamma_base + gamma_slot_of_rank[r]);
                 if (!st.empty()) { int par = front_of_rank[st[0]] - first_gf; gkids[par].push_back(fi); f.parent = first_gf + par; }
-                choose_chunks(f, opt.tile_rows);
+                choose_chunks(f, opt.gamma_tile_rows > 0 ? opt.gamma_tile_rows : opt.tile_rows);
             }
             auto local_index = [&](int fi, int r) -> int {   // rank r inside front fi: pivots then update rows
                 if (r < e_hi[fi]) return r - e_lo[fi];
