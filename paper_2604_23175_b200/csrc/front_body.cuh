@@ -868,13 +868,21 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
         // the lanes carry s_i = t_i / L_ii, so the serial chain per pivot is one shuffle and one FMA:
         // x_c = s_c, then s_i -= (L_ci / L_ii) x_c with the scaled factor entry formed off the chain
         t0 *= r0; t1 *= r1;
-#pragma unroll 4
-        for (int c = p - 1; c >= 0; --c) {
-            const double lc0 = tid < c ? l11[c * p + tid] * r0 : 0.0;
-            const double lc1 = tid + 32 < c ? l11[c * p + tid + 32] * r1 : 0.0;
+        // Two pivots per round: x_c, the not yet reduced s_{c-1} and the factor entry between the two come by three
+        // independent shuffles, every lane forms x_{c-1} itself, and both updates follow -- the same operations in the same
+        // order as one pivot per round (bit for bit), with one shuffle latency per PAIR on the chain.
+#pragma unroll 2
+        for (int c = p - 1; c >= 1; c -= 2) {
+            const double la0 = tid < c ? l11[c * p + tid] * r0 : 0.0;
+            const double la1 = tid + 32 < c ? l11[c * p + tid + 32] * r1 : 0.0;
+            const double lb0 = tid < c - 1 ? l11[(c - 1) * p + tid] * r0 : 0.0;
+            const double lb1 = tid + 32 < c - 1 ? l11[(c - 1) * p + tid + 32] * r1 : 0.0;
             const double xc = __shfl_sync(0xffffffffu, c < 32 ? t0 : t1, c & 31);
-            t0 = fma(-lc0, xc, t0);
-            t1 = fma(-lc1, xc, t1);
+            const double sm1 = __shfl_sync(0xffffffffu, c - 1 < 32 ? t0 : t1, (c - 1) & 31);
+            const double lcc = __shfl_sync(0xffffffffu, c - 1 < 32 ? la0 : la1, (c - 1) & 31);
+            const double xm1 = fma(-lcc, xc, sm1);
+            t0 = fma(-lb0, xm1, fma(-la0, xc, t0));
+            t1 = fma(-lb1, xm1, fma(-la1, xc, t1));
         }
         if (prow0 >= 0) xsol[prow0] = t0;
         if (prow1 >= 0) xsol[prow1] = t1;
