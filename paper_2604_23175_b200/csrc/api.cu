@@ -538,6 +538,8 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
         sp.gval = plan->gval.ptr; sp.lbuf = plan->lbuf.ptr; sp.ubuf = plan->ubuf.ptr; sp.xsol = plan->xsol.ptr;
         sp.bpart = plan->bpart.ptr; sp.obj_partial = plan->obj_partial.ptr; sp.bcnt = plan->bcnt.ptr;
         sp.front0 = ctr_front0(hp.n_areas);
+        sp.bwd_poll = 1; sp.pad0 = 0;
+        if (const char* e = getenv("GSE_BWD_POLL")) sp.bwd_poll = atoi(e) != 0;
         // chain ranges of the task list: runs of levels with at most ~one panel task per SM (the top of the areas, the
         // boundary tree).  Those tasks are the latency chains; the persistent kernel hands them to one CTA per SM only
         // (two panel factorisations on one SM slow each other by a quarter).

@@ -255,7 +255,17 @@ struct NoWait {
     __device__ __forceinline__ int ready_children(const TaskRec&, const ChildRec*, int c, int nb, int*) const { return nb - c; }
     __device__ __forceinline__ void panels(const TaskRec&) const {}
     __device__ __forceinline__ void tile_done(const TaskRec&) const {}
+    __device__ __forceinline__ bool poll_x() const { return false; }
+    __device__ __forceinline__ double load_x(const double* p) const { return ldc(p); }
 };
+
+// Back-substitution hand-off through the data (dataflow kernel, single rank): the forward task that owns a front's pivots
+// arms their entries of the solution vector with this pattern (all ones: a NaN no arithmetic produces; the producers
+// store the canonical NaN instead of any other), the front's back-substitution overwrites them, and the descendants
+// poll the entries they read instead of a completion counter followed by a load -- no fence and no atomic on the
+// chain of twelve levels, and every split waits for exactly the ancestors it reads.
+__device__ __forceinline__ double x_unset() { return __longlong_as_double(-1LL); }
+__device__ __forceinline__ bool x_is_unset(double v) { return __double_as_longlong(v) == -1LL; }
 
 // One front task; S.hdr is loaded and visible to the whole CTA.  tb: optional 8 clock stamps.
 // Task kinds (TaskRec::kind):
@@ -271,7 +281,7 @@ struct NoWait {
 template <int HAS_PIVOTS, class Wait>
 __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, const FrontTab& ft, const double* gval,
                                                 double* lbuf, double* ubuf, unsigned long long* err, long long* tb,
-                                                const Wait& wait) {
+                                                const Wait& wait, double* xarm = nullptr) {
     double* dinv = ft.dinv;
     const TaskRec& hdr = S.hdr;
     ChildRec* crec = S.crec;
@@ -296,6 +306,9 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     const int ldt = round8(nj) | 1;
     double* pan = sm;
     double* tile = sm + (size_t)(rp + ri + rj) * ld;
+    // (dataflow kernel) the task that owns the front's pivots arms their solution entries for this iteration's
+    // back-substitution: every reader of the previous iteration's values finished before this iteration started
+    if (HAS_PIVOTS && xarm && pp && ci == 0 && cj == 0 && tid < p) xarm[ft.rows[ft.rows_off[f] + tid]] = x_unset();
     // first batch of child records: issue now, consume after the zero fill
     const int nchild = hdr.nchild;
     if (tid < 3 * min(nchild, kChildBatch))
@@ -796,8 +809,13 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
     // Early splits (dataflow kernel): the later splits of a front only read entries of ancestors above the nearest
     // one, so they wait for front dep2 and finish a level ahead; split 0 -- the only one on the chain -- combines.
     const bool early = Wait::kEarlySplits && tk.early != 0;
-    if (early && tk.split > 0) wait.ancestor(tk); else wait.parent(tk);
-    if (tid < kBwdRows) xs[tid] = xrow >= 0 ? ldc(xsol + xrow) : 0.0;
+    if (wait.poll_x()) {
+        // every thread polls the solution entry it reads (armed by the forward pass, see x_unset)
+        if (tid < kBwdRows) xs[tid] = xrow >= 0 ? wait.load_x(xsol + xrow) : 0.0;
+    } else {
+        if (early && tk.split > 0) wait.ancestor(tk); else wait.parent(tk);
+        if (tid < kBwdRows) xs[tid] = xrow >= 0 ? ldc(xsol + xrow) : 0.0;
+    }
     __syncthreads();
     {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -884,8 +902,9 @@ __device__ __forceinline__ bool backward_body(BwdScratch& B, const BwdTask& tk, 
             t0 = fma(-lb0, xm1, fma(-la0, xc, t0));
             t1 = fma(-lb1, xm1, fma(-la1, xc, t1));
         }
-        if (prow0 >= 0) xsol[prow0] = t0;
-        if (prow1 >= 0) xsol[prow1] = t1;
+        // (a NaN leaves as the canonical one: the armed pattern of x_unset never comes out of a solve)
+        if (prow0 >= 0) xsol[prow0] = t0 == t0 ? t0 : __longlong_as_double(0x7ff8000000000000LL);
+        if (prow1 >= 0) xsol[prow1] = t1 == t1 ? t1 : __longlong_as_double(0x7ff8000000000000LL);
     }
     __syncthreads();
     return true;

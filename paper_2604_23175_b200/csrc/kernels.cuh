@@ -148,6 +148,7 @@ struct SolveProg {
     int32_t n_eval_items, n_acc_items, n_tasks, n_btasks, n_upd_items, items_per_it;
     int32_t n_units, n_upd, n_bwd_fronts, n_fronts, n_rows, max_it;
     int32_t front0, n_chain;      // offset of the per-front counters inside ctr (ctr_front0(n_areas)); chain ranges in use
+    int32_t bwd_poll, pad0;       // back-substitution hand-off through the solution entries themselves (front_body.cuh: kXUnset)
     int32_t chain_lo[4], chain_hi[4];   // task-index ranges [lo, hi) of runs of levels with at most one panel task per SM:
                                   // the latency chains (top of the areas, boundary tree), handed to one CTA per SM only
     int64_t n_gval;

@@ -102,6 +102,23 @@ struct SpinWait {
     bool sys;                // peer-linked solve: child counters may be bumped by other GPUs
     unsigned gamma_need;     // non-coordinator ranks: pieces of delta_x_Gamma to wait for (0: none)
     bool early_tile = false; // latency-bound plans: fused diagonal tasks report their tile before they store the factor
+    bool poll = false;       // back-substitution: the solution entries are the hand-off (x_unset, front_body.cuh)
+    __device__ __forceinline__ bool poll_x() const { return poll; }
+    __device__ __forceinline__ double load_x(const double* p) const {
+        unsigned polls = 0;
+        unsigned long long t0 = 0;
+        double v;
+        while (x_is_unset(v = __ldcg(p))) {
+            __nanosleep(GSE_POLL_NS);
+            if ((++polls & 0xffffu) == 0) {          // watchdog, as in wait_ge
+                const unsigned long long now = globaltimer();
+                if (t0 == 0) t0 = now;
+                else if (now - t0 > g_watchdog_ns) __trap();
+            }
+        }
+        if (tr && threadIdx.x == 0) tr[2] = globaltimer();
+        return v;
+    }
     // early splits of the back-substitution (front_body.cuh): later splits wait for front dep2; split 0 for the others
     static constexpr bool kEarlySplits = true;
     __device__ __forceinline__ void ancestor(const BwdTask& tk) const {
@@ -314,7 +331,8 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
                 tr[7] = (unsigned long long)S.hdr.p | ((unsigned long long)S.hdr.u1 << 16) | ((unsigned long long)S.hdr.nchild << 32) | ((unsigned long long)S.hdr.phase << 48);
             }
             const SpinWait w{ctr, epoch, (unsigned)sp.n_acc_items * epoch, tr, sp.n_fronts, sp.front0, linked, 0u, fused_update};
-            if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
+            if (S.hdr.p) front_task_body<1>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w,
+                                             (!linked && sp.bwd_poll) ? sp.xsol : nullptr);
             else front_task_body<0>(S, sm, ft, sp.gval, sp.lbuf, sp.ubuf, sp.err, tr ? (long long*)(tr + 8) : nullptr, w);
             __syncthreads();
             if (tid == 0 && linked && (S.hdr.flags & 4)) {
@@ -336,7 +354,7 @@ __device__ __forceinline__ void gn_solve_body(const SolveProg& sp, const EvalPro
         } else if (loc < o_upd) {
             // ---- backward substitution task ---------------------------------------------------------
             const BwdTask tk = sp.btasks[loc - o_bwd];
-            const SpinWait w{ctr, epoch, 0u, tr, sp.n_fronts, sp.front0, linked, gamma_need};
+            const SpinWait w{ctr, epoch, 0u, tr, sp.n_fronts, sp.front0, linked, gamma_need, false, !linked && sp.bwd_poll != 0};
             const bool solved = backward_body(*reinterpret_cast<BwdScratch*>(sm), tk, ft, sp.lbuf, sp.xsol, sp.bpart, sp.bcnt, w);
             if (solved && linked && lk.rank == 0 && tk.phase == 3) {
                 // coordinator, boundary front: this front's pivots are a piece of delta_x_Gamma -- store it into every
