@@ -145,6 +145,32 @@ def test_persistent_kernel_matches_level_path_bitwise(G, name):
     assert ra.objective == rb.objective
 
 
+@pytest.mark.parametrize("name", ["ieee118_k6", "pegase2869_k8", "pegase9241_k16"])
+def test_backsubstitution_handoff_through_the_data_matches_the_counter_handoff_bitwise(G, name, monkeypatch):
+    """The persistent kernel hands the solution entries of the back-substitution over through the entries themselves
+    (armed by the forward pass, polled by the descendants; ``GSE_BWD_POLL=0`` keeps the completion counters).  Same
+    arithmetic either way: identical bits, also on the third solve of one plan and after a level-launch solve
+    (which does not arm anything) in between."""
+    from conftest import build_case
+    net, ms, part, g = build_case(name)
+    est = G.MultiAreaEstimator(net, ms, part)                      # (plans read the override when they are built)
+    monkeypatch.setenv("GSE_BWD_POLL", "0")
+    ctr = G.MultiAreaEstimator(net, ms, part)
+    monkeypatch.delenv("GSE_BWD_POLL")
+    try:
+        a, ra = est.estimate()
+        b, rb = ctr.estimate()
+        assert ra.iterations == rb.iterations == int(g["iterations"])
+        assert np.array_equal(a.va, b.va) and np.array_equal(a.vm, b.vm) and ra.objective == rb.objective
+        lv, rl = G.solve_multiarea(net, ms, part, config=G.SolverConfig(profile_phases=True))      # level path, same cached plan family
+        for _ in range(2):
+            c, rc = est.estimate()
+            assert rc.iterations == ra.iterations and np.array_equal(c.va, a.va) and np.array_equal(c.vm, a.vm)
+        assert np.array_equal(lv.va, a.va) and np.array_equal(lv.vm, a.vm)
+    finally:
+        est.close(); ctr.close()
+
+
 def test_persistent_kernel_iteration_cap_and_failure(G):
     """max_outer_iterations is honoured inside the kernel (converged=False, last iterate returned --
     reference test_solver.py:271-276) and a non-SPD area still raises (test_solver.py:335-342)."""
