@@ -331,8 +331,11 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
     CU(plan->br_y.upload(std::vector<double>(d->br_y, d->br_y + 8 * (size_t)d->n_branch)));
     CU(plan->m_type.upload(std::vector<int32_t>(d->m_type, d->m_type + d->n_rows)));
     CU(plan->m_target.upload(std::vector<int32_t>(d->m_target, d->m_target + d->n_rows)));
-    CU(plan->z.upload(std::vector<double>(d->m_z, d->m_z + d->n_rows)));
-    CU(plan->w.upload(std::vector<double>(d->m_w, d->m_w + d->n_rows)));
+    {   // measured values and weights in ONE block [z | w]: a scan's refresh from a contiguous pinned block is one copy
+        std::vector<double> zw(d->m_z, d->m_z + d->n_rows);
+        zw.insert(zw.end(), d->m_w, d->m_w + d->n_rows);
+        CU(plan->z.upload(zw));
+    }
     // ---- evaluation units ----
     CU(plan->vm_bus.upload(hp.vm_bus)); CU(plan->vm_row.upload(hp.vm_row)); CU(plan->vm_slot.upload(hp.vm_slot));
     CU(plan->fl_branch.upload(hp.fl_branch)); CU(plan->fl_from.upload(hp.fl_from)); CU(plan->fl_to.upload(hp.fl_to));
@@ -348,7 +351,7 @@ static int create_plan(const gse_problem_desc* d, const gse_options* opt, BuildO
                        plan->gval.ptr, (int32_t)(hp.acc_items.size() / 8)};
     EvalProg& ep = plan->ep;
     ep.y_ptr = plan->y_ptr.ptr; ep.y_idx = plan->y_idx.ptr; ep.y_g = plan->y_g.ptr; ep.y_b = plan->y_b.ptr;
-    ep.br_y = plan->br_y.ptr; ep.z = plan->z.ptr; ep.w = plan->w.ptr; ep.slack = d->slack;
+    ep.br_y = plan->br_y.ptr; ep.z = plan->z.ptr; ep.w = plan->z.ptr + d->n_rows; ep.slack = d->slack;
     ep.n_vm = (int)hp.vm_bus.size(); ep.n_fl = (int)hp.fl_branch.size(); ep.n_inj = (int)hp.inj_bus.size();
     ep.has_current = 0;
     for (int r = 0; r < d->n_rows; ++r) if (d->m_type[r] >= 7) { ep.has_current = 1; break; }
@@ -633,11 +636,16 @@ static int stage_rows(gse_plan* plan, int which, const double* src, double* dst_
 int gse_set_rows_pinned(gse_plan* plan, const double* z_pinned, const double* w_pinned) {
     CU(cudaSetDevice(plan->device));
     const size_t bytes = sizeof(double) * plan->hp.n_rows;
+    double* w_dev = plan->z.ptr + plan->hp.n_rows;
+    if (z_pinned && w_pinned == z_pinned + plan->hp.n_rows && bytes) {
+        CU(cudaMemcpyAsync(plan->z.ptr, z_pinned, 2 * bytes, cudaMemcpyHostToDevice, plan->stream));
+        return GSE_OK;
+    }
     if (z_pinned && bytes) CU(cudaMemcpyAsync(plan->z.ptr, z_pinned, bytes, cudaMemcpyHostToDevice, plan->stream));
-    if (w_pinned && bytes) CU(cudaMemcpyAsync(plan->w.ptr, w_pinned, bytes, cudaMemcpyHostToDevice, plan->stream));
+    if (w_pinned && bytes) CU(cudaMemcpyAsync(w_dev, w_pinned, bytes, cudaMemcpyHostToDevice, plan->stream));
     return GSE_OK;
 }
-int gse_set_weights(gse_plan* plan, const double* w) { return stage_rows(plan, 1, w, plan->w.ptr); }
+int gse_set_weights(gse_plan* plan, const double* w) { return stage_rows(plan, 1, w, plan->z.ptr + plan->hp.n_rows); }
 int gse_set_measurements(gse_plan* plan, const double* z) { return stage_rows(plan, 0, z, plan->z.ptr); }
 
 int gse_check(gse_plan* plan) {
@@ -713,9 +721,13 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     if (sp.trace) CU(cudaMemsetAsync(sp.trace, 0, sizeof(unsigned long long) * 32 * (size_t)sp.items_per_it * 16, s));
     auto t0 = std::chrono::steady_clock::now();
     const size_t nb2 = sizeof(double) * (size_t)plan->hp.n_bus;
-    if (plan->io_init) {      // (va | vm) of the start state, contiguous like the caller's state block or not: two copies
-        CU(cudaMemcpyAsync(va, plan->io_init, nb2, cudaMemcpyDeviceToDevice, s));
-        CU(cudaMemcpyAsync(vm, plan->io_init + plan->hp.n_bus, nb2, cudaMemcpyDeviceToDevice, s));
+    const bool one_block = vm == va + plan->hp.n_bus;      // (va | vm) contiguous like the start state and the host block: one copy each way
+    if (plan->io_init) {
+        if (one_block) CU(cudaMemcpyAsync(va, plan->io_init, 2 * nb2, cudaMemcpyDeviceToDevice, s));
+        else {
+            CU(cudaMemcpyAsync(va, plan->io_init, nb2, cudaMemcpyDeviceToDevice, s));
+            CU(cudaMemcpyAsync(vm, plan->io_init + plan->hp.n_bus, nb2, cudaMemcpyDeviceToDevice, s));
+        }
     }
     cudaEventRecord(plan->ev[6], s);      // gpu_s: the loop itself (counter reset, launch, report readback), as gse_solve times it
     if (plan->linked) {
@@ -730,8 +742,11 @@ static int solve_persistent(gse_plan* plan, const gse_config* cfg, int max_it, d
     CU(cudaMemcpyAsync(plan->h_blk, plan->syncblk.ptr, sizeof(unsigned long long) * kBlkWords, cudaMemcpyDeviceToHost, s));
     cudaEventRecord(plan->ev[7], s);
     if (plan->io_out) {
-        CU(cudaMemcpyAsync(plan->io_out, va, nb2, cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(plan->io_out + plan->hp.n_bus, vm, nb2, cudaMemcpyDeviceToHost, s));
+        if (one_block) CU(cudaMemcpyAsync(plan->io_out, va, 2 * nb2, cudaMemcpyDeviceToHost, s));
+        else {
+            CU(cudaMemcpyAsync(plan->io_out, va, nb2, cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(plan->io_out + plan->hp.n_bus, vm, nb2, cudaMemcpyDeviceToHost, s));
+        }
     }
     CU(cudaStreamSynchronize(s));
     rep->loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
