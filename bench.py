@@ -74,11 +74,11 @@ class ClockSampler:
         self.index, self.samples, self._stop = index, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
-    def _run(self):
+    def _setup(self):
         # NVML (nvidia_ml_py, the library nvidia-smi itself reads) answers in well under a millisecond, so the short
         # timed region of a latency-bound solve (tens of ms) still gets tens of samples; the nvidia-smi process
-        # (~50 ms per call) is the fallback when NVML cannot be loaded
-        nv = None
+        # (~50 ms per call) is the fallback when NVML cannot be loaded.  Loaded BEFORE the timed region starts (import +
+        # nvmlInit + handle lookup take tens of ms: done inside the sampling thread they left one sample per run).
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -96,9 +96,12 @@ class ClockSampler:
                         break
                     except Exception:
                         h = None
-            nv = (pynvml, h if h is not None else pynvml.nvmlDeviceGetHandleByIndex(self.index))
+            self._nv = (pynvml, h if h is not None else pynvml.nvmlDeviceGetHandleByIndex(self.index))
         except Exception:
-            nv = None
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
         while not self._stop.is_set():
             try:
                 if nv:
@@ -120,6 +123,7 @@ class ClockSampler:
             self._stop.wait(0.2 if not nv else 0.002)
 
     def __enter__(self):
+        self._setup()
         self._t.start()
         return self
 
