@@ -114,7 +114,8 @@ const gse_error *gse_last_error(const gse_plan *plan);
 int gse_set_weights(gse_plan *plan, const double *w);
 int gse_set_measurements(gse_plan *plan, const double *z);
 /* The same refresh from caller-owned pinned host memory: asynchronous copies on the plan's stream, no
- * staging; either pointer may be NULL.  The buffers must stay unchanged until the next solve returns. */
+ * staging; either pointer may be NULL (w_pinned == z_pinned + n_rows: one copy for both).  The buffers must stay
+ * unchanged until the next solve returns. */
 int gse_set_rows_pinned(gse_plan *plan, const double *z_pinned, const double *w_pinned);
 
 /* ---- the solve (solve_multiarea, solver.py:204-346) -------------------------------- */

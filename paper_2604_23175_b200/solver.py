@@ -169,7 +169,7 @@ class MultiAreaEstimator:
     def pinned_inputs(self):
         """(z, w) numpy views of pinned host buffers owned by the estimator.  A data front end writes
         the next scan's values / weights there in place; ``update_from_pinned`` then moves them to the
-        device with two asynchronous copies (no staging, no host synchronisation)."""
+        device with one asynchronous copy of the contiguous block (no staging, no host synchronisation)."""
         if getattr(self, "_pin", None) is None:
             self._pin = self.torch.empty((2, self.ms.m), dtype=self.torch.float64).pin_memory()
             self._pin[0].numpy()[:] = self.ms.z
