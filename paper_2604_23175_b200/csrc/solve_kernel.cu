@@ -22,6 +22,9 @@
 #ifndef GSE_POLL_NS
 #define GSE_POLL_NS 40
 #endif
+#ifndef GSE_XPOLL_NS
+#define GSE_XPOLL_NS 40     // back-substitution: interval between two looks at an armed solution entry
+#endif
 
 namespace gse {
 
@@ -109,7 +112,7 @@ struct SpinWait {
         unsigned long long t0 = 0;
         double v;
         while (x_is_unset(v = __ldcg(p))) {
-            __nanosleep(GSE_POLL_NS);
+            __nanosleep(GSE_XPOLL_NS);
             if ((++polls & 0xffffu) == 0) {          // watchdog, as in wait_ge
                 const unsigned long long now = globaltimer();
                 if (t0 == 0) t0 = now;
