@@ -16,6 +16,15 @@ namespace gse {
 #ifndef GSE_GATHER_BY_CHILD
 #define GSE_GATHER_BY_CHILD 1
 #endif
+#ifndef GSE_BATCH1_G
+#define GSE_BATCH1_G 8     // panel-driven gather, one child / several children at a time: row groups per warp and sweep
+#endif
+#ifndef GSE_BATCHN_G
+#define GSE_BATCHN_G 4
+#endif
+#ifndef GSE_LAST_G
+#define GSE_LAST_G 4       // last child of a batch: child rows per warp and sweep (8: +1.6 % at PEGASE-9241/16, +4 % at ACTIVSg10k/32; 3 equal, 2 and 1 slower)
+#endif
 #ifndef GSE_CHAIN_G
 #define GSE_CHAIN_G 8      // chain pieces: child rows per warp and sweep of the direct copy (two loads per lane and row in flight; 6: +0.4 %, 10: no better)
 #endif
@@ -424,16 +433,16 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
             if (GSE_GATHER_BY_CHILD && ready == 1 && c == nb - 1) {
                 __syncthreads();               // (the earlier children's sums are in place)
                 if (tb && tid == 0) tb[16] = (long long)gtimer();
-                gather_last_child<8>(ga, *cb, S.fwd, ri, tb);
+                gather_last_child<GSE_LAST_G>(ga, *cb, S.fwd, ri, tb);
                 if (tb && tid == 0) tb[18] = (long long)gtimer();
                 c += ready;
                 continue;
             }
             switch (ready) {
-                case 1: gather_batch<1, 8>(ga, cb); break;
-                case 2: gather_batch<2, 4>(ga, cb); break;
-                case 3: gather_batch<3, 4>(ga, cb); break;
-                default: gather_batch<4, 4>(ga, cb); break;
+                case 1: gather_batch<1, GSE_BATCH1_G>(ga, cb); break;
+                case 2: gather_batch<2, GSE_BATCHN_G>(ga, cb); break;
+                case 3: gather_batch<3, GSE_BATCHN_G>(ga, cb); break;
+                default: gather_batch<4, GSE_BATCHN_G>(ga, cb); break;
             }
             c += ready;
         }

@@ -116,7 +116,10 @@ cudaError_t configure_unit_kernels();
 //   [eval blocks | accumulate blocks | front tasks (level order) | backward tasks (top-down) | update blocks]
 // CTAs pull item indices from a global counter and spin on per-front completion counters.
 constexpr int kSolveThreads = 256;
-constexpr int kEvalPerItem = 256, kUpdPerItem = 1024;
+#ifndef GSE_EVAL_PER_ITEM
+#define GSE_EVAL_PER_ITEM 256
+#endif
+constexpr int kEvalPerItem = GSE_EVAL_PER_ITEM, kUpdPerItem = 1024;
 enum { CTR_NEXT = 0, CTR_EVAL = 32, CTR_ACC = 64, CTR_FWD = 96, CTR_BWD = 128, CTR_UPD = 160, CTR_OBJ = 192,
        CTR_GAMMA = 224,      // peer-linked solve: boundary fronts whose share of delta_x_Gamma has arrived from the coordinator
        CTR_ITER = 256,       // peer-linked solve: ranks that have finished (and published the norm of) an iteration
