@@ -13,17 +13,8 @@ namespace gse {
 #ifndef GSE_PANEL_QUIET
 #define GSE_PANEL_QUIET 1
 #endif
-#ifndef GSE_GATHER_BY_CHILD
-#define GSE_GATHER_BY_CHILD 1
-#endif
-#ifndef GSE_BATCH1_G
-#define GSE_BATCH1_G 8     // panel-driven gather, one child / several children at a time: row groups per warp and sweep
-#endif
-#ifndef GSE_BATCHN_G
-#define GSE_BATCHN_G 4
-#endif
-#ifndef GSE_LAST_G
-#define GSE_LAST_G 4       // last child of a batch: child rows per warp and sweep (8: +1.6 % at PEGASE-9241/16, +4 % at ACTIVSg10k/32; 3 equal, 2 and 1 slower)
+#ifndef GSE_CHILD_G
+#define GSE_CHILD_G 3      // extend-add: child rows per warp and sweep (4: +0.2 %, 6: +2 %, 8: +4 % at PEGASE-9241/16; 2 and 1 slower)
 #endif
 #ifndef GSE_CHAIN_G
 #define GSE_CHAIN_G 8      // chain pieces: child rows per warp and sweep of the direct copy (two loads per lane and row in flight; 6: +0.4 %, 10: no better)
@@ -37,117 +28,27 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// Extend-add as a GATHER: every destination entry of the task's shared-memory panels / tile is
-// owned by one thread, which adds the contributions of the children in child order.  No barrier
-// between children, no read-modify-write chains, and the loads of all children of a batch are in
-// flight together -- the phase costs a few L2 latencies instead of several per child.
-// inv[c][panel row] = row of child c that maps there (or -1), built from the child's rel map.
+// Extend-add as a GATHER in fixed child order: no atomics, no read-modify-write chains in global memory.  Each child is
+// walked by ITS rows -- a child row holds its entries contiguously, so a warp reads them coalesced, and only rows the
+// child really has are visited -- and added to the task's shared-memory panels / tile through its child -> parent map;
+// a CTA barrier separates two children, so every entry takes the children's contributions one after the other, in
+// child order (the sums do not depend on which children were already complete when the task started).
+// (A panel-driven form -- every destination entry owned by one thread that adds the children of a batch in order, the
+// loads of up to four children in flight together -- was the first implementation; it picks the entries column by
+// column through inverse maps, uncoalesced, and lost against this one on every shape: profiles/r02_sweep_build_constants.txt.)
 constexpr int kInvRows = 64 + 2 * kMaxTile;
 constexpr int kGatherBatch = 4;
 
 struct GatherArgs {
-    double* pan; double* tile; const int* inv; const double* ubuf;
-    int p, ld, ldt, rp, Rp, ni, nj, diag, direct, warp, lane, nwarps;
+    double* pan; double* tile; const double* ubuf;
+    int p, ld, ldt, rp, ni, nj, diag, direct, warp, lane, nwarps;
 };
 
-// NB children of one batch, compile-time so that empty child slots cost no instructions.
-// G row groups per warp and sweep: G * 2 * NB independent loads per thread in flight (16 with the
-// usual two children and G = 4; G = 8 only for a single child: more would spill under the 128-register cap
-// of the persistent kernel).
-template <int NB, int G>
-__device__ __forceinline__ void gather_batch(const GatherArgs& a, const ChildRec* __restrict__ crec) {
-    const int p = a.p, ld = a.ld, ldt = a.ldt, rp = a.rp, Rp = a.Rp, ni = a.ni, nj = a.nj;
-    const int warp = a.warp, lane = a.lane, nwarps = a.nwarps;
-    const double* Ub[NB];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) Ub[c] = a.ubuf + crec[c].u_off;
-    // panel rows [pivots | I | J] x pivot columns
-    if (p) {
-        for (int Rb = warp; Rb < Rp; Rb += G * nwarps) {
-            double v[NB][2 * G];
-#pragma unroll
-            for (int c = 0; c < NB; ++c) {
-                const int* inv = a.inv + c * kInvRows;
-                int ic[2];
-#pragma unroll
-                for (int cp = 0; cp < 2; ++cp) { const int C = lane + 32 * cp; ic[cp] = C < p ? inv[C] : -1; }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int R = Rb + g * nwarps;
-                    const int ir = R < Rp ? inv[R] : -1;
-                    const int irc = ir > 0 ? ir : 0;
-                    const double* row = Ub[c] + (size_t)irc * (irc + 1) / 2;
-#pragma unroll
-                    for (int cp = 0; cp < 2; ++cp)
-                        v[c][2 * g + cp] = (ir >= 0 && ic[cp] >= 0 && ic[cp] <= ir) ? ldc(row + ic[cp]) : 0.0;
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const int R = Rb + g * nwarps;
-#pragma unroll
-                for (int cp = 0; cp < 2; ++cp) {
-                    const int C = lane + 32 * cp;
-                    if (R < Rp && C < p) {
-                        double acc = a.pan[R * ld + C];
-#pragma unroll
-                        for (int c = 0; c < NB; ++c) acc += v[c][2 * g + cp];
-                        a.pan[R * ld + C] = acc;
-                    }
-                }
-            }
-        }
-    }
-    // tile: rows of chunk I x rows of chunk J
-    if (!a.direct) {
-        const int irow0 = rp, jrow0 = a.diag ? rp : rp + round8(ni);   // index of tile row / column 0 in inv
-        for (int Cb = 0; Cb < nj; Cb += 64) {
-            for (int Rb = warp; Rb < ni; Rb += G * nwarps) {
-                double v[NB][2 * G];
-#pragma unroll
-                for (int c = 0; c < NB; ++c) {
-                    const int* inv = a.inv + c * kInvRows;
-                    int ic[2];
-#pragma unroll
-                    for (int cp = 0; cp < 2; ++cp) { const int C = Cb + lane + 32 * cp; ic[cp] = C < nj ? inv[jrow0 + C] : -1; }
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const int R = Rb + g * nwarps;
-                        const int ir = R < ni ? inv[irow0 + R] : -1;
-                        const int irc = ir > 0 ? ir : 0;
-                        const double* row = Ub[c] + (size_t)irc * (irc + 1) / 2;
-#pragma unroll
-                        for (int cp = 0; cp < 2; ++cp)
-                            v[c][2 * g + cp] = (ir >= 0 && ic[cp] >= 0 && ic[cp] <= ir) ? ldc(row + ic[cp]) : 0.0;
-                    }
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int R = Rb + g * nwarps;
-#pragma unroll
-                    for (int cp = 0; cp < 2; ++cp) {
-                        const int C = Cb + lane + 32 * cp;
-                        if (R < ni && C < nj) {
-                            double acc = a.tile[R * ldt + C];
-#pragma unroll
-                            for (int c = 0; c < NB; ++c) acc += v[c][2 * g + cp];
-                            a.tile[R * ldt + C] = acc;
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
-// The LAST child of a batch -- by construction the one expected to finish last, so usually gathered alone, right after
-// the hand-off -- is walked by ITS rows instead of by the panel's: a child row holds its entries contiguously, so a
-// warp reads them coalesced (the panel-driven gather above picks them column by column through the inverse map) and
-// only rows the child really has are visited.  Every panel / tile entry still receives this child's contribution
-// exactly once and after the earlier children's (a CTA barrier separates them): the same sums, bit for bit.
-// fwd: FrontScratch::fwd of this child; eP / bI,eI / bJ,eJ: its row ranges (ChildRec).
+// One child.  fwd: its child -> parent map (FrontScratch::fwd[c]): [0, eP) pivot row / column, then the tile rows of its
+// rows in chunk I, then the tile columns of its rows in chunk J; eP / bI,eI / bJ,eJ: its row ranges (ChildRec).
+// G child rows per warp and sweep.
 template <int G>
-__device__ __forceinline__ void gather_last_child(const GatherArgs& a, const ChildRec& cr, const int* __restrict__ fwd, int ri, long long* tb = nullptr) {
+__device__ __forceinline__ void gather_child(const GatherArgs& a, const ChildRec& cr, const int* __restrict__ fwd, int ri, long long* tb = nullptr) {
     const int p = a.p, ld = a.ld, ldt = a.ldt, rp = a.rp, warp = a.warp, lane = a.lane, nwarps = a.nwarps;
     const double* Uc = a.ubuf + cr.u_off;
     const int eP = p ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = a.diag ? 0 : cr.eJ - cr.bJ;
@@ -240,13 +141,12 @@ __device__ __forceinline__ void diag_rank8(double* pan, int ld, int t, int kc, i
 struct __align__(16) FrontScratch {
     TaskRec hdr;
     ChildRec crec[kChildBatch];
-    int inv[kGatherBatch][kInvRows];
+    int fwd[kGatherBatch][kInvRows];   // per child of the current batch, child -> parent: [0, eP) pivot row / column, then the tile
+                               // rows of its rows in chunk I, then the tile columns of its rows in chunk J (gather_child)
     double ld8[2][48];         // published 8x8 diagonal factor (36) + reciprocal pivots (8), double-buffered
     double rinv[64];           // reciprocal pivots of the whole front (stored for the backward pass)
     double colbuf[2][16];      // two columns of the 8x8 pivot block being eliminated (double-buffered)
     int nready;                // children of the current gather batch that are complete
-    int fwd[kInvRows];         // LAST child of the batch, child -> parent: [0, eP) pivot row / column, then the tile rows of its
-                               // rows in chunk I, then the tile columns of its rows in chunk J (gather_last_child)
 };
 
 __device__ __forceinline__ void load_task_header(FrontScratch& S, const TaskRec* __restrict__ task) {
@@ -297,7 +197,7 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     double* dinv = ft.dinv;
     const TaskRec& hdr = S.hdr;
     ChildRec* crec = S.crec;
-    int (*s_inv)[kInvRows] = S.inv;
+    int (*s_fwd)[kInvRows] = S.fwd;
     double* s_ld = &S.ld8[0][0];
     double* s_rinv = S.rinv;
     const int tid = threadIdx.x, nth = blockDim.x;
@@ -400,49 +300,35 @@ __device__ __forceinline__ void front_task_body(FrontScratch& S, double* sm, con
     } else
     for (int cb0 = 0; cb0 < nchild; cb0 += kGatherBatch) {
         const int nb = min(kGatherBatch, nchild - cb0);
-        const int Rp = rp + ri + rj;
         if (cb0 && (cb0 % kChildBatch) == 0) {          // next page of child records
             __syncthreads();
             if (tid < 3 * min(kChildBatch, nchild - cb0))
                 reinterpret_cast<int4*>(crec)[tid] = reinterpret_cast<const int4*>(ft.crecs + hdr.child_off + cb0)[tid];
         }
         __syncthreads();
-        for (int t = tid; t < kGatherBatch * kInvRows; t += nth) (&s_inv[0][0])[t] = -1;
-        __syncthreads();
         const int cbase = cb0 % kChildBatch;
         for (int c = 0; c < nb; ++c) {
             const ChildRec& cr = crec[cbase + c];
             const int32_t* rel = ft.rel + cr.rel_off;
             const int eP = pp ? cr.eP : 0, nI = cr.eI - cr.bI, nJ = diag ? 0 : cr.eJ - cr.bJ;
-            const bool last = c == nb - 1;
             for (int t = tid; t < eP + nI + nJ; t += nth) {
-                if (t < eP) { const int r = rel[t]; s_inv[c][r] = t; if (last) S.fwd[t] = r; }
-                else if (t < eP + nI) { const int i = cr.bI + t - eP, r = rel[i] - p - i0; s_inv[c][rp + r] = i; if (last) S.fwd[t] = r; }
-                else { const int i = cr.bJ + t - eP - nI, r = rel[i] - p - j0; s_inv[c][rp + round8(ni) + r] = i; if (last) S.fwd[t] = r; }
+                if (t < eP) s_fwd[c][t] = rel[t];
+                else if (t < eP + nI) s_fwd[c][t] = rel[cr.bI + t - eP] - p - i0;
+                else s_fwd[c][t] = rel[cr.bJ + t - eP - nI] - p - j0;
             }
         }
         __syncthreads();
         if (cb0 == 0) GSE_TICK(7);
-        // children are taken in order, as many at a time as are already complete: the contributions of a
-        // child that finished early are folded in while the task still waits for its slower sibling
-        // (the sums are sequential per child either way, so the grouping does not change a bit)
+        // children in order; whatever is already complete is folded in while the task still waits for a slower sibling
+        const GatherArgs ga{pan, tile, ubuf, pp, ld, ldt, rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
         for (int c = 0; c < nb;) {
             const int ready = wait.ready_children(hdr, ft.crecs + hdr.child_off + cb0, c, nb, &S.nready);
-            GatherArgs ga{pan, tile, &s_inv[c][0], ubuf, pp, ld, ldt, rp, Rp, ni, nj, diag ? 1 : 0, (direct || no_tile) ? 1 : 0, warp, lane, nwarps};
-            const ChildRec* cb = crec + cbase + c;
-            if (GSE_GATHER_BY_CHILD && ready == 1 && c == nb - 1) {
+            for (int k = 0; k < ready; ++k) {
                 __syncthreads();               // (the earlier children's sums are in place)
-                if (tb && tid == 0) tb[16] = (long long)gtimer();
-                gather_last_child<GSE_LAST_G>(ga, *cb, S.fwd, ri, tb);
-                if (tb && tid == 0) tb[18] = (long long)gtimer();
-                c += ready;
-                continue;
-            }
-            switch (ready) {
-                case 1: gather_batch<1, GSE_BATCH1_G>(ga, cb); break;
-                case 2: gather_batch<2, GSE_BATCHN_G>(ga, cb); break;
-                case 3: gather_batch<3, GSE_BATCHN_G>(ga, cb); break;
-                default: gather_batch<4, GSE_BATCHN_G>(ga, cb); break;
+                const bool stamp = tb && c + k == nb - 1 && cb0 + nb == nchild;      // the task's last child
+                if (stamp && tid == 0) tb[16] = (long long)gtimer();
+                gather_child<GSE_CHILD_G>(ga, crec[cbase + c + k], &s_fwd[c + k][0], ri, stamp ? tb : nullptr);
+                if (stamp && tid == 0) tb[18] = (long long)gtimer();
             }
             c += ready;
         }
